@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark: megapixels/s of the full multiscale BLADE denoise (BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl blade|reference]
+
+Default workload: configs/c3.json = BASELINE.json configs[3] (64 frames of 1920x1080 RGB fp32,
+3-level pyramid, 144 buckets, 5x5 fine + 5x5 coarse phase-indexed pairs, AWGN 15/255). The
+batch is split evenly over the GPUs (no collective on the data path; NCCL only for the start
+barrier and the max-over-ranks time). One step = one blade_ms_denoise call over this rank's
+frames: K1 decimation, K2 selector and K3 stage kernels for every level (all of SURVEY.md §8(a)).
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + cuda synchronize, CUDA
+events on the launching stream, max over ranks. Inputs (1.59 GB at N=1) exceed the 126 MB L2,
+so no flush is needed between steps. nvidia-smi clocks are sampled during the timed region.
+
+`--impl reference` times the fp64 CPU oracle (oracle/) on the host cores, on bounded samples
+of the same workload (the tier's reference arm); rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+import blade_synth as bs  # noqa: E402
+
+FP32_LANES_PER_SM = 128  # B200: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / guide unit counts)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU time of the oracle sample (cpu_baseline)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampled every 50 ms in the background; keeps (t, fields) per line."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), [s.strip() for s in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0: float, t1: float) -> dict:
+        win = [f for t, f in self.samples if t0 <= t <= t1 + 0.05]
+        if not win:  # region shorter than one period: take the nearest samples
+            win = [f for t, f in self.samples if t0 - 0.2 <= t <= t1 + 0.2]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"],
+                    "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return float("nan")
+        sm = [num(f[0]) for f in win]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for f in win:
+            for name, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.nanmedian(sm)), "sm_max_mhz": num(win[0][1]),
+                "power_w_max": float(np.nanmax([num(f[2]) for f in win])),
+                "reasons": sorted(reasons), "samples": len(win)}
+
+
+# ----------------------------------------------------------------------------- work model
+
+def level_dims(H, W, L):
+    d = [(H, W)]
+    for _ in range(L - 1):
+        d.append(((d[-1][0] + 1) // 2, (d[-1][1] + 1) // 2))
+    return d
+
+
+def algorithmic_work(cfg, N):
+    """Algorithmic bytes / FLOPs per kernel launch."""
+    d = level_dims(cfg.H, cfg.W, cfg.levels)
+    L = cfg.levels
+    nf2 = cfg.fine_size ** 2
+    nc2 = cfg.coarse_size ** 2 if L > 1 else 0
+    out = {}
+    for l in range(L - 1):  # K1: read z^l (12 B/px), write z^{l+1}
+        px, px1 = d[l][0] * d[l][1], d[l + 1][0] * d[l + 1][1]
+        out[("decimate", l)] = dict(bytes=N * 12 * (px + px1), flops=N * 3 * px1 * 2 * 16)
+    nsel = 1 if L == 1 else L - 1
+    for l in range(nsel):
+        px = d[l][0] * d[l][1]
+        out[("selector", l)] = dict(bytes=N * (12 * px + px), flops=None)
+        px1 = d[l + 1][0] * d[l + 1][1] if L > 1 else 0
+        out[("stage", l)] = dict(bytes=N * (12 * px + 12 * px1 + px + 12 * px),
+                                 flops=N * px * 3 * 2 * (nf2 + nc2))
+    return out
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def oracle_sample_rate(cfg, target_s: float, rows_cap: int | None = None):
+    """Time the fp64 oracle on bounded samples of the workload: full-width row bands of
+    successive frames (each band treated as an image), until ~target_s of CPU time."""
+    import oracle
+    oracle.build()
+    W = cfg.W
+    # calibrate on a small band
+    rows = min(cfg.H, 64)
+    z = cfg.frame(0, row0=0, rows=rows)
+    sub = bs.Config(**{**cfg.__dict__, "H": rows})
+    t = time.perf_counter()
+    oracle.denoise_config(sub, z)
+    per_px = (time.perf_counter() - t) / (rows * W)
+    rows = int(min(cfg.H, max(16, target_s / max(per_px, 1e-12) / W)))
+    if rows_cap:
+        rows = min(rows, rows_cap)
+    sub = bs.Config(**{**cfg.__dict__, "H": rows})
+    z = cfg.frame(0, row0=0, rows=rows)
+    t = time.perf_counter()
+    oracle.denoise_config(sub, z)
+    dt = time.perf_counter() - t
+    mp = rows * W / 1e6
+    return mp / dt, dt, rows, oracle.max_threads()
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return 0
+    cfg = bs.load_config(args.config)
+    import oracle
+    oracle.build()
+    # one step = one bounded sample (a full-width band of one frame, ~0.25 MP)
+    rows = int(min(cfg.H, max(16, 250_000 // cfg.W)))
+    sub = bs.Config(**{**cfg.__dict__, "H": rows})
+    taps = cfg.taps()
+    frames = [cfg.frame(i % max(cfg.N, 1), row0=0, rows=rows) for i in range(min(4, args.steps + args.warmup))]
+    for i in range(args.warmup):
+        oracle.denoise_config(sub, frames[i % len(frames)], taps)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        oracle.denoise_config(sub, frames[i % len(frames)], taps)
+    dt = (time.perf_counter() - t) / max(args.steps, 1)
+    mp = rows * cfg.W / 1e6
+    val = mp / dt
+    sample = (f"one {rows}x{cfg.W} full-width band of a {cfg.name} frame per step "
+              f"(treated as an image), fp64 oracle, OpenMP over rows")
+    line = {"impl": "reference", "metric": "megapixels/sec full multiscale denoise",
+            "value": val, "unit": "MP/s", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "desc": cfg.description, "frames": cfg.N,
+                       "H": cfg.H, "W": cfg.W, "levels": cfg.levels},
+            "cpu_baseline": {"value": val, "unit": "MP/s", "cores": oracle.max_threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "MP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- blade arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    rank, local, world = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_1802_06130_b200 import BladeMS
+    cfg = bs.load_config(args.config)
+    if cfg.N % world:
+        raise SystemExit(f"{cfg.name}: {cfg.N} frames do not split over {world} GPUs")
+    n_local = cfg.N // world
+    f0 = rank * n_local
+    H, W = cfg.H, cfg.W
+
+    # ---- inputs: this rank's frames, generated on the host (seeded), copied once to HBM
+    x_host = torch.empty((n_local, 3, H, W), dtype=torch.float32).pin_memory()
+    xn = x_host.numpy()
+    for i in range(n_local):
+        bs.scene(cfg.seed, f0 + i, H, W, cfg.n_grat, cfg.n_disk, cfg.noise, cfg.p0, cfg.p1,
+                 out=xn[i])
+    x = x_host.to(dev, non_blocking=False)
+    out = torch.empty_like(x)
+    h = BladeMS.from_config(cfg, device=local)
+    ws = h.workspace(n_local, H, W)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        h.denoise(x, out, ws, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    sampler = ClockSampler(local)
+    time.sleep(0.4)  # nvidia-smi start-up
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.time()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t1 = time.time()
+    barrier()
+    time.sleep(0.1)
+    sampler.stop()
+    clocks = sampler.summary(t0, t1)
+    ms = e0.elapsed_time(e1)
+    t_max = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    ms_per_step = ms_max / args.steps
+    total_px = cfg.N * H * W
+    value = total_px / 1e6 / (ms_per_step / 1e3)
+
+    # ---- per-kernel breakdown: same steps again with events around every launch
+    h.set_profiling(True)
+    for _ in range(args.steps):
+        step()
+    prof = h.profile_read()
+    h.set_profiling(False)
+    torch.cuda.synchronize(dev)
+
+    # ---- end to end through the C ABI with host buffers (H2D + compute + D2H per step)
+    out_host = torch.empty_like(x_host).pin_memory()
+    d_in = torch.empty_like(x)
+    e2e_ms = []
+    h.denoise_host(x_host, out_host, d_in, out, ws, stream)  # warm
+    for _ in range(max(args.e2e_steps, 1)):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        h.denoise_host(x_host, out_host, d_in, out, ws, stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_t = torch.tensor([float(np.median(e2e_ms))], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_val = total_px / 1e6 / (float(e2e_t.item()) / 1e3)
+    io_bytes = n_local * 3 * H * W * 4
+
+    # ---- roofline of the dominant kernel
+    work = algorithmic_work(cfg, n_local)
+    kern = {k: (t / c, c) for k, (t, c) in prof.items()}
+    step_kernel_ms = sum(t for t, _ in prof.values()) / args.steps
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms = kern[dom][0]
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = n_sm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
+    w = work[dom]
+    traffic = None
+    ncu_path = ROOT / "profiles" / "ncu_summary.json"
+    if ncu_path.exists():
+        try:
+            nsum = json.loads(ncu_path.read_text())
+            ent = nsum.get("kernels", {}).get(f"{cfg.name}:{dom[0]}:{dom[1]}")
+            if ent:
+                traffic = ent.get("dram_bytes_per_launch")
+        except (ValueError, OSError):
+            traffic = None
+    if w["flops"]:
+        ach = w["flops"] / (dom_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "kernel": f"k_stage level {dom[1]}" if dom[0] == "stage" else dom[0],
+                "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                "traffic": traffic,
+                "peak_source": f"derived: {n_sm} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz",
+                "algorithmic_flops_per_launch": w["flops"],
+                "algorithmic_bytes_per_launch": w["bytes"], "ms_per_launch": dom_ms,
+                "hbm_frac_of_measured": w["bytes"] / (dom_ms / 1e3) / 1e9 / hbm_peak}
+    else:
+        ach = w["bytes"] / (dom_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom[0], "achieved": ach, "peak": hbm_peak,
+                "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
+                "ms_per_launch": dom_ms}
+    step_bytes = sum(v["bytes"] for v in work.values())
+    hbm_ach = step_bytes * world / (ms_per_step / 1e3) / 1e9 / world
+    breakdown = {f"{k[0]}{k[1]}": round(t, 4) for k, (t, c) in sorted(kern.items())}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            mps, dt, rows, cores = oracle_sample_rate(cfg, args.cpu_seconds)
+            cpu = {"value": mps, "unit": "MP/s", "cores": cores, "kind": "oracle",
+                   "sample": f"one {rows}x{W} full-width band of a {cfg.name} frame, fp64 oracle "
+                             f"({dt:.1f} s)"}
+        except Exception as e:  # the baseline must never break the GPU line
+            cpu = {"value": None, "unit": "MP/s", "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "megapixels/sec full multiscale denoise",
+            "value": value, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "desc": cfg.description, "frames": cfg.N,
+                       "frames_per_gpu": n_local, "H": H, "W": W, "levels": cfg.levels,
+                       "fine": cfg.fine_size, "coarse": cfg.coarse_size, "buckets": cfg.K,
+                       "parallelism": f"frames split over {world} GPU(s), no collective",
+                       "l2": "inputs larger than L2 (no flush)"},
+            "roofline": roof,
+            "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm_ach / hbm_peak,
+                    "bytes_per_step_per_gpu": step_bytes,
+                    "note": "level-materialised algorithmic bytes of all kernels / step time"},
+            "kernel_ms_per_step": breakdown,
+            "kernel_sum_ms_per_step": step_kernel_ms,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "MP/s", "h2d_bytes_per_step": io_bytes,
+                    "d2h_bytes_per_step": io_bytes, "ms_per_step": float(e2e_t.item())},
+            "gpu_launches": args.steps * h.launch_count(n_local, H, W) * world,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

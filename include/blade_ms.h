@@ -1,0 +1,201 @@
+/*
+ * blade_ms.h — C ABI of the B200 (sm_100a) multiscale BLADE denoiser, inference path.
+ *
+ * Method: arxiv 1802.06130 (reference text /root/reference/PAPER.md; citations below are
+ * "PAPER.md:<lines> (<section>, <equation>)"). The library computes, for each RGB frame z:
+ *
+ *   pyramid      z^{l+1} = bicubic 2x decimation of z^l          PAPER.md:260-263 (§4)
+ *   selector     s^l(i)  = bucket(orientation, strength, coherence of the joint-colour
+ *                          structure tensor T_i of z^l)           PAPER.md:131-148 (§3, Eq. 6)
+ *   stage        u^l_i   = sum_j f^{l,s(i)}_j u^{l+1}_{i/2+j} + sum_j g^{l,s(i)}_j z^l_{i+j}
+ *                                                                 PAPER.md:269-271 (§4, Eq. 9)
+ *   cascade      u^{L-1} = z^{L-1}; l = L-2 .. 0                  PAPER.md:284-289 (§4)
+ *   single-level (L == 1): u_i = sum_j h^{s(i)}_j z_{i+j}         PAPER.md:81-83 (§3, Eq. 1)
+ *
+ * Readings of points the paper leaves open (border, gradient, window, quantiser, phase,
+ * normalisation, ...) are DESIGN.md R1..R24; the ones that shape this interface are cited
+ * inline as [Rn].
+ *
+ * Conventions
+ *   - Images are planar fp32 NCHW with C = 3 (R, G, B), contiguous, values on any scale
+ *     (the configs use [0, 1]) [R1]. Row y runs down, column x runs right.
+ *   - Border handling is half-sample symmetric (numpy 'symmetric'), periodic for offsets
+ *     beyond one period, applied to every level's image [R2].
+ *   - Level dims: H_{l+1} = ceil(H_l / 2), W likewise [R16]. "levels" = number of pyramid
+ *     images L (L-1 decimations, L-1 stages; L == 1 is fixed-scale Eq. 1).
+ *   - All entry points are asynchronous on the caller's CUDA stream (cudaStream_t passed as
+ *     void*; NULL = legacy default stream) unless stated; no host synchronisation happens.
+ *   - Errors: every argument error is detected BEFORE any launch (no partial writes) and
+ *     returned as a blade_status; blade_ms_last_error() returns a thread-local message.
+ *     Asynchronous device faults surface at the caller's next synchronisation.
+ *   - Thread safety: a handle is immutable after create; concurrent calls with distinct
+ *     workspaces/outputs (on any streams) are safe. destroy must not race pending work.
+ *   - Non-finite PIXEL values are not checked (it would cost a pass); outputs are then
+ *     unspecified. Non-finite TAPS and thresholds are rejected at create.
+ */
+#ifndef BLADE_MS_H
+#define BLADE_MS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct blade_ms* blade_ms_t; /* opaque handle; immutable after create */
+
+typedef enum {
+  BLADE_OK = 0,
+  BLADE_EINVAL = 1,       /* bad argument: null pointer, bad size, overlap, ...          */
+  BLADE_ENONFINITE = 2,   /* NaN/Inf tap or threshold                      */
+  BLADE_ESHAPE = 3,       /* tap count / workspace size / band extent mismatch           */
+  BLADE_EDEVICE = 4,      /* pointer not on the handle's device, or bad device ordinal   */
+  BLADE_ENOMEM = 5,       /* device allocation failed at create                          */
+  BLADE_ECUDA = 6,        /* a CUDA call or launch failed (message in last_error)        */
+  BLADE_EUNSUPPORTED = 7  /* valid per the paper but not built (e.g. per-channel banks)  */
+} blade_status;
+
+typedef struct {
+  int32_t levels;            /* L >= 1 pyramid images; 1 => fixed-scale Eq. 1; max 12           */
+  int32_t fine_size;         /* n_f: odd, 1..9; the g block (and the single-level h)           */
+  int32_t coarse_size;       /* n_c: odd, 1..9 if L >= 2; must be 0 if L == 1 (f block)         */
+  int32_t n_phases;          /* 4 = pair indexed by (2(y mod 2) + (x mod 2), bucket) [R9];
+                                1 = bucket only (SPEC.md reading); must be 1 if L == 1          */
+  int32_t n_filter_channels; /* 1 = one filter for R, G and B [R13]. (3 = per-channel YCbCr
+                                banks, returns BLADE_EUNSUPPORTED)            */
+  int32_t window_size;       /* structure-tensor window, odd 1..7 (configs: 5) [R4]             */
+  float window_sigma;        /* Gaussian std of the window, > 0 (configs: 1.5) [R4]             */
+  int32_t clamp_output;      /* 0 = raw cascade output (parity); 1 = clamp final u^0 to [0,1]
+                                (SPEC.md:447 clamps only at the end) [R24]                      */
+} blade_ms_config;
+
+typedef struct {
+  int32_t n_orient;    /* n_o >= 1 orientation bins over [0, pi) (configs: 16)                 */
+  int32_t n_strength;  /* n_s >= 1 (configs: 3)                                                */
+  int32_t n_coherence; /* n_c >= 1 (configs: 3); K = n_o * n_s * n_c <= 256 (uint8 maps)       */
+  /* Thresholds per stage, stage index = output level l (0 = finest), n_stages = max(L-1, 1):
+     strength_thresholds[stage * (n_s - 1) + t], coherence_thresholds[stage * (n_c - 1) + t];
+     strictly ascending and finite within a stage. Quantiser [R7]:
+       o = floor(theta * n_o / pi) mod n_o, s = #{t <= S}, k = #{t <= C},
+       bucket = (o * n_s + s) * n_c + k.
+     The device compares fp32 features with fp32 thresholds: pass fp32-representable values
+     (a double that is not is rounded UP to the next fp32, which keeps "t <= S" exact for
+     fp32 S). May be NULL when the matching count is 1. Copied at create. */
+  const double* strength_thresholds;
+  const double* coherence_thresholds;
+} blade_bucket_layout;
+
+/*
+ * Create a handle on CUDA device `device` (ordinal).
+ *   taps: HOST fp32, n_taps = n_stages * n_filter_channels * n_phases * K * (n_f^2 + n_c^2),
+ *         layout [stage][channel][phase][bucket][ fine n_f*n_f row-major | coarse n_c*n_c ];
+ *         tap (dy, dx) (row-major from (-r, -r)) multiplies the sample at (y+dy, x+dx) of z^l
+ *         (fine) or (floor(y/2)+dy, floor(x/2)+dx) of u^{l+1} (coarse): correlation, as in
+ *         Eq. 1 "z_{i+j}" [R12]. Copied (and re-laid for the kernels) at create; the caller
+ *         may free its arrays on return.
+ * Errors: EINVAL (null/bad config), ESHAPE (n_taps), ENONFINITE, EUNSUPPORTED, EDEVICE,
+ *         ENOMEM, ECUDA. On error *out is set to NULL.
+ */
+blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layout* buckets,
+                             const float* taps, size_t n_taps, int device, blade_ms_t* out);
+
+/* Bytes of device workspace blade_ms_denoise / _selector / _pyramid need for a batch of N
+ * frames of H x W (levels >= 1 images, u^l intermediates, bucket maps, 256-B aligned). */
+blade_status blade_ms_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t W, size_t* bytes);
+
+/*
+ * Denoise a batch: in, out DEVICE fp32 [N][3][H][W] on the handle's device; N >= 0 (0 is a
+ * no-op), H, W >= 1. `out` must not overlap `in` (EINVAL). workspace: device, >= the size
+ * from blade_ms_workspace_size (ESHAPE otherwise); contents on return are the pyramid
+ * levels, intermediate stage outputs and bucket maps (see blade_ms_workspace_layout).
+ * Output equals a per-frame loop bit-exactly.
+ */
+blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t N, int32_t H,
+                              int32_t W, void* workspace, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * End-to-end variant with HOST buffers: copies in_host -> d_in, denoises into d_out and copies
+ * d_out -> out_host, all on `cuda_stream`, frame-pipelined (the copy of frame n+1 overlaps the
+ * compute of frame n) when the host buffers are page-locked. d_in / d_out: device staging
+ * buffers of N*3*H*W floats each. Synchronises the stream before returning (the output is in
+ * out_host on return).
+ */
+blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* out_host,
+                                   int32_t N, int32_t H, int32_t W, float* d_in, float* d_out,
+                                   void* workspace, size_t ws_bytes, void* cuda_stream);
+
+/*
+ * Row bands (one huge image split over GPUs, BASELINE.json configs[4]).
+ * blade_ms_band_rows: input rows [*in_row0, *in_row0 + *in_rows) of the full H-row image needed
+ * to produce output rows [out_row0, out_row0 + out_rows) bit-identically to the full-image call
+ * (the union of the cascade's dependency cone, clamped to [0, H)).
+ */
+blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32_t out_rows,
+                                int32_t* in_row0, int32_t* in_rows);
+
+/* Workspace bytes for a band call (depends on the band's input extent). */
+blade_status blade_ms_band_workspace_size(blade_ms_t h, int32_t H, int32_t W, int32_t out_row0,
+                                          int32_t out_rows, size_t* bytes);
+
+/*
+ * Denoise output rows [out_row0, out_row0 + out_rows) of ONE frame of H_full x W, given input
+ * rows [in_row0, in_row0 + in_rows) (device, [3][in_rows][W]); the band must cover
+ * blade_ms_band_rows (ESHAPE otherwise). out_band: device [3][out_rows][W]. Rows equal the
+ * same rows of blade_ms_denoise on the full frame bit-exactly (all indices global: phases use
+ * global parity, folds happen at the true image border).
+ */
+blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t in_row0,
+                                   int32_t in_rows, float* out_band, int32_t out_row0,
+                                   int32_t out_rows, int32_t H_full, int32_t W, void* workspace,
+                                   size_t ws_bytes, void* cuda_stream);
+
+/*
+ * Diagnostic: the bucket maps s^l (uint8, device, [N][H_l][W_l]) for every selector level
+ * l = 0 .. n_stages-1 (maps_per_level[l]; a NULL entry skips that level). Also leaves the
+ * pyramid in the workspace.
+ */
+blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W,
+                               uint8_t* const* maps_per_level, void* workspace, size_t ws_bytes,
+                               void* cuda_stream);
+
+/* Diagnostic: pyramid levels 1..L-1 into levels[l-1] (device fp32 [N][3][H_l][W_l]). */
+blade_status blade_ms_pyramid(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W,
+                              float* const* levels, void* workspace, size_t ws_bytes,
+                              void* cuda_stream);
+
+/* Properties of a handle (host query). */
+typedef struct {
+  int32_t levels, fine_size, coarse_size, n_phases, n_stages, K;
+  int32_t device;
+  size_t bank_bytes_device;    /* device copy of the relaid bank                          */
+  size_t stage_smem_bytes;     /* dynamic shared memory of the stage kernel (K3)          */
+  int32_t stage_phase_groups;  /* 1: a CTA holds all phases; 2: CTAs specialised by row parity */
+} blade_ms_info;
+blade_status blade_ms_get_info(blade_ms_t h, blade_ms_info* info);
+
+/* Number of kernel launches one blade_ms_denoise(N, H, W) call issues. */
+blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t* count);
+
+/*
+ * Per-kernel timing (measurement support for bench.py). While enabled, every launch the handle
+ * enqueues is bracketed by two CUDA events recorded on the launching stream. blade_ms_profile_read
+ * synchronises on those events and returns, per kernel kind (0 = K1 decimate, 1 = K2 selector,
+ * 2 = K3 stage) and level l (< 16), the summed milliseconds ms[kind * 16 + l] and the launch count
+ * count[kind * 16 + l] since the last read, then clears the records. Enabling profiling makes the
+ * handle stateful: do not enqueue from several threads while it is on.
+ */
+blade_status blade_ms_set_profiling(blade_ms_t h, int32_t enable);
+blade_status blade_ms_profile_read(blade_ms_t h, double* ms /* [48] */, int32_t* count /* [48] */);
+
+/* Release the handle and its device bank. NULL is a no-op. */
+blade_status blade_ms_destroy(blade_ms_t h);
+
+const char* blade_ms_status_string(blade_status s);
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* blade_ms_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLADE_MS_H */

@@ -1,0 +1,827 @@
+// Host side of the C ABI declared in include/blade_ms.h: argument validation, filterbank
+// re-layout, workspace/band planning and the per-level launch sequence.
+//
+// The launch sequence for one call:
+//   down pass   K1 z^{l+1} = decimate(z^l),            l = 0 .. L-2
+//   up pass     K2 s^l = selector(z^l); K3 u^l = stage(z^l, u^{l+1}, s^l),  l = L-2 .. 0
+//               (u^{L-1} = z^{L-1}); L == 1: K2 + K3 (Eq. 1) at level 0.
+// Every call is described by a Plan: for each level the GLOBAL rows of z^l and u^l that must be
+// materialised. For a full image these are all rows; for a row band (blade_ms_denoise_rows) they
+// are the band's dependency cone, so the same code serves both and bands are bit-identical.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/blade_ms.h"
+#include "kernels.cuh"
+
+using namespace blade;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+blade_status fail(blade_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e__ = (expr);                                                              \
+    if (e__ != cudaSuccess)                                                                \
+      return fail(BLADE_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e__), __FILE__, \
+                  __LINE__);                                                               \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+using StageKernel = void (*)(StageArgs);
+using SelKernel = void (*)(LevelView, uint8_t*, int, int, int, int, SelParams);
+
+struct StageVariant {
+  int nf, nc, rs, by;
+  StageKernel fn;
+  int tile_floats;
+  int threads;
+  int trows, tcols;
+};
+
+template <int NF, int NC, int RS, int BY>
+StageVariant make_variant() {
+  using SS = StageShape<NF, NC, RS, BY>;
+  return StageVariant{NF, NC, RS, BY, &k_stage<NF, NC, RS, BY>, SS::tile_floats, SS::threads,
+                      SS::TROWS, SS::TCOLS};
+}
+
+// The instantiated stage kernels (which footprints are built).
+std::vector<StageVariant> stage_variants() {
+  return {
+      // fixed-scale (Eq. 1), all phases in one CTA (n_phases must be 1 when L == 1)
+      make_variant<3, 0, 1, 8>(), make_variant<5, 0, 1, 8>(), make_variant<7, 0, 1, 8>(),
+      make_variant<9, 0, 1, 8>(),
+      // multiscale pairs, CTAs specialised by output-row parity
+      make_variant<3, 3, 2, 8>(), make_variant<5, 5, 2, 8>(), make_variant<7, 7, 2, 8>(),
+      make_variant<7, 7, 2, 4>(), make_variant<9, 9, 2, 8>(), make_variant<9, 9, 2, 4>(),
+      make_variant<9, 9, 2, 2>(), make_variant<7, 5, 2, 8>(), make_variant<7, 5, 2, 4>(),
+      make_variant<5, 3, 2, 8>(), make_variant<9, 7, 2, 4>(), make_variant<9, 7, 2, 2>(),
+  };
+}
+
+SelKernel selector_kernel(int ws) {
+  switch (ws) {
+    case 1: return &k_selector<1>;
+    case 3: return &k_selector<3>;
+    case 5: return &k_selector<5>;
+    case 7: return &k_selector<7>;
+    default: return nullptr;
+  }
+}
+
+struct Range {
+  int lo = 0, hi = 0;  // [lo, hi)
+  int n() const { return hi - lo; }
+};
+
+int fold_host(long long i, long long n) {
+  long long p = 2 * n, m = i % p;
+  if (m < 0) m += p;
+  return (int)(m < n ? m : p - 1 - m);
+}
+
+// Hull of {fold(i, n) : lo <= i < hi}.
+Range fold_hull(long long lo, long long hi, int n) {
+  if (hi <= lo) return Range{0, 0};
+  if (hi - lo >= 2LL * n || (lo >= 0 && hi <= n)) {
+    if (hi - lo >= 2LL * n) return Range{0, n};
+    return Range{(int)lo, (int)hi};
+  }
+  int mn = n, mx = -1;
+  for (long long i = lo; i < hi; ++i) {
+    int f = fold_host(i, n);
+    mn = std::min(mn, f);
+    mx = std::max(mx, f);
+  }
+  return Range{mn, mx + 1};
+}
+
+Range hull(Range a, Range b) {
+  if (a.n() <= 0) return b;
+  if (b.n() <= 0) return a;
+  return Range{std::min(a.lo, b.lo), std::max(a.hi, b.hi)};
+}
+
+}  // namespace
+
+struct blade_ms {
+  blade_ms_config cfg;
+  int n_o, n_s, n_c, K;
+  int n_stages, nt, S, PS;
+  int device;
+  int num_sms;
+  float* d_bank = nullptr;  // [stage][phase][PS]
+  size_t bank_bytes = 0;
+  std::vector<SelParams> sel;  // per stage
+  StageVariant stage{};
+  size_t stage_smem = 0;
+  int stage_ctas_per_sm = 0;
+  SelKernel sel_fn = nullptr;
+  // profiling (blade_ms_set_profiling): event pairs around each launch
+  struct ProfRec { int kind, level; cudaEvent_t e0, e1; };
+  bool profiling = false;
+  std::vector<ProfRec> prof;        // recorded, not yet read
+  std::vector<cudaEvent_t> ev_pool;  // free events
+};
+
+namespace {
+
+struct Plan {
+  int L = 0, N = 0;
+  std::vector<int> H, W;
+  std::vector<Range> z;    // rows of z^l materialised (level 0: the input buffer's rows)
+  std::vector<Range> u;    // rows of u^l computed (stage output = map rows), l <= L-2 (or 0 if L==1)
+  size_t ws_bytes = 0;
+  std::vector<size_t> z_off, u_off, map_off;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Dependency cone of output rows [o0, o0+on) of the final output.
+void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) {
+  const int L = h->cfg.levels;
+  p.L = L;
+  p.N = N;
+  p.H.assign(L, 0);
+  p.W.assign(L, 0);
+  p.H[0] = H;
+  p.W[0] = W;
+  for (int l = 1; l < L; ++l) {
+    p.H[l] = (p.H[l - 1] + 1) / 2;
+    p.W[l] = (p.W[l - 1] + 1) / 2;
+  }
+  p.z.assign(L, Range{});
+  p.u.assign(L, Range{});
+  const int rf = h->cfg.fine_size / 2;
+  const int rc = h->cfg.coarse_size / 2;
+  const int ext = std::max(rf, h->cfg.window_size / 2 + 1);
+  p.u[0] = Range{o0, o0 + on};
+  if (L == 1) {
+    p.z[0] = fold_hull((long long)o0 - ext, (long long)o0 + on + ext, H);
+  } else {
+    for (int l = 0; l + 1 < L; ++l) {
+      p.z[l] = hull(p.z[l], fold_hull((long long)p.u[l].lo - ext, (long long)p.u[l].hi + ext, p.H[l]));
+      const long long clo = (long long)(p.u[l].lo / 2) - rc;
+      const long long chi = (long long)((p.u[l].hi - 1) / 2) + rc + 1;
+      p.u[l + 1] = fold_hull(clo, chi, p.H[l + 1]);
+    }
+    p.z[L - 1] = hull(p.z[L - 1], p.u[L - 1]);
+    for (int l = L - 1; l >= 1; --l) {
+      const long long dlo = 2LL * p.z[l].lo - 3;
+      const long long dhi = 2LL * (p.z[l].hi - 1) + 4 + 1;
+      p.z[l - 1] = hull(p.z[l - 1], fold_hull(dlo, dhi, p.H[l - 1]));
+    }
+  }
+  // workspace: z^l (l >= 1), u^l (1 <= l <= L-2), maps (selector levels)
+  size_t off = 0;
+  p.z_off.assign(L, 0);
+  p.u_off.assign(L, 0);
+  p.map_off.assign(L, 0);
+  for (int l = 1; l < L; ++l) {
+    p.z_off[l] = off;
+    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
+  }
+  for (int l = 1; l + 1 < L; ++l) {
+    p.u_off[l] = off;
+    off = align256(off + sizeof(float) * (size_t)N * 3 * p.u[l].n() * p.W[l]);
+  }
+  const int nsel = L == 1 ? 1 : L - 1;
+  for (int l = 0; l < nsel; ++l) {
+    p.map_off[l] = off;
+    off = align256(off + (size_t)N * p.u[l].n() * p.W[l]);
+  }
+  p.ws_bytes = std::max<size_t>(off, 256);
+}
+
+LevelView make_view(float* base, int H, int W, Range r) {
+  LevelView v;
+  v.p = base;
+  v.H = H;
+  v.W = W;
+  v.row0 = r.lo;
+  v.rows = r.n();
+  v.plane = (long long)r.n() * W;
+  v.frame = 3 * v.plane;
+  return v;
+}
+
+blade_status check_dev_ptr(const blade_ms* h, const void* p, const char* what) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BLADE_EDEVICE, "%s: not a CUDA pointer (%s)", what, cudaGetErrorString(e));
+  }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+    return fail(BLADE_EDEVICE, "%s: not device memory", what);
+  if (at.device != h->device)
+    return fail(BLADE_EDEVICE, "%s: on device %d, handle on device %d", what, at.device, h->device);
+  return BLADE_OK;
+}
+
+bool ranges_overlap(const void* a, size_t an, const void* b, size_t bn) {
+  const char* pa = (const char*)a;
+  const char* pb = (const char*)b;
+  return pa < pb + bn && pb < pa + an;
+}
+
+cudaEvent_t prof_event(blade_ms* h) {
+  if (!h->ev_pool.empty()) {
+    cudaEvent_t e = h->ev_pool.back();
+    h->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return e;
+}
+
+// Brackets one launch with events when profiling is on.
+struct ProfScope {
+  blade_ms* h;
+  cudaStream_t st;
+  int kind, level;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(const blade_ms* hc, cudaStream_t s, int k, int l)
+      : h(const_cast<blade_ms*>(hc)), st(s), kind(k), level(l) {
+    if (h->profiling && (e0 = prof_event(h))) cudaEventRecord(e0, st);
+  }
+  ~ProfScope() {
+    if (!e0) return;
+    cudaEvent_t e1 = prof_event(h);
+    if (!e1) return;
+    cudaEventRecord(e1, st);
+    h->prof.push_back(blade_ms::ProfRec{kind, level, e0, e1});
+  }
+};
+
+// Enqueue the whole cascade for plan p. in0: level-0 input buffer (rows p.z[0] ... or wider,
+// described by in_view); out_view: final output rows p.u[0].
+blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view,
+                     char* ws, cudaStream_t st, bool run_stages,
+                     uint8_t* const* maps_out, float* const* levels_out) {
+  const int L = p.L, N = p.N;
+  if (N == 0) return BLADE_OK;
+  std::vector<LevelView> zv(L);
+  zv[0] = in_view;
+  for (int l = 1; l < L; ++l) {
+    float* base = (levels_out && levels_out[l - 1]) ? levels_out[l - 1]
+                                                    : reinterpret_cast<float*>(ws + p.z_off[l]);
+    zv[l] = make_view(base, p.H[l], p.W[l], p.z[l]);
+  }
+  // ---- down pass (K1)
+  for (int l = 0; l + 1 < L; ++l) {
+    const Range r = p.z[l + 1];
+    if (r.n() <= 0) continue;
+    dim3 grid((p.W[l + 1] + dec::TX - 1) / dec::TX, (r.n() + dec::TY - 1) / dec::TY, N);
+    ProfScope ps(h, st, 0, l);
+    k_decimate<<<grid, dim3(32, 8), 0, st>>>(zv[l], zv[l + 1], r.lo, r.n());
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (levels_out && !run_stages && !maps_out) return BLADE_OK;
+  const int nsel = L == 1 ? 1 : L - 1;
+  for (int l = nsel - 1; l >= 0; --l) {
+    const Range r = p.u[l];
+    uint8_t* map = (maps_out && maps_out[l]) ? maps_out[l] : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
+    {
+      dim3 grid((p.W[l] + sel::TX - 1) / sel::TX, (r.n() + sel::TY - 1) / sel::TY, N);
+      ProfScope ps(h, st, 1, l);
+      h->sel_fn<<<grid, dim3(32, 8), 0, st>>>(zv[l], map, r.lo, r.n(), r.lo, r.n(), h->sel[l]);
+      CUDA_TRY(cudaGetLastError());
+    }
+    if (!run_stages) continue;
+    StageArgs a{};
+    a.z = zv[l];
+    if (L > 1) {
+      a.u1 = (l + 1 == L - 1) ? zv[L - 1]
+                              : make_view(reinterpret_cast<float*>(ws + p.u_off[l + 1]), p.H[l + 1],
+                                          p.W[l + 1], p.u[l + 1]);
+    }
+    a.out = (l == 0) ? out_view
+                     : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r);
+    a.map = map;
+    a.map_row0 = r.lo;
+    a.map_rows = r.n();
+    a.bank = h->d_bank + (size_t)l * h->cfg.n_phases * h->PS;
+    a.K = h->K;
+    a.S = h->S;
+    a.PS = h->PS;
+    a.n_phases = h->cfg.n_phases;
+    a.N = N;
+    a.out_r0 = r.lo;
+    a.out_rn = r.n();
+    const int y_base = r.lo & ~1;
+    a.tiles_x = (p.W[l] + h->stage.tcols - 1) / h->stage.tcols;
+    a.tiles_y = (r.hi - y_base + h->stage.trows - 1) / h->stage.trows;
+    a.n_tiles = N * a.tiles_x * a.tiles_y;
+    a.clamp = (l == 0 && h->cfg.clamp_output) ? 1 : 0;
+    long long grid = (long long)h->stage_ctas_per_sm * h->num_sms;
+    const long long need = (long long)a.n_tiles * h->stage.rs;
+    grid = std::min(grid, need);
+    if (h->stage.rs == 2) grid = std::max<long long>(2, grid & ~1LL);
+    ProfScope ps(h, st, 2, l);
+    h->stage.fn<<<(unsigned)grid, dim3(32, h->stage.by), h->stage_smem, st>>>(a);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return BLADE_OK;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+
+extern "C" {
+
+const char* blade_ms_status_string(blade_status s) {
+  switch (s) {
+    case BLADE_OK: return "ok";
+    case BLADE_EINVAL: return "invalid argument";
+    case BLADE_ENONFINITE: return "non-finite tap or threshold";
+    case BLADE_ESHAPE: return "size mismatch";
+    case BLADE_EDEVICE: return "wrong device";
+    case BLADE_ENOMEM: return "out of device memory";
+    case BLADE_ECUDA: return "CUDA error";
+    case BLADE_EUNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+const char* blade_ms_last_error(void) { return g_last_error.c_str(); }
+
+blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layout* bl,
+                             const float* taps, size_t n_taps, int device, blade_ms_t* out) {
+  g_last_error.clear();
+  if (!out) return fail(BLADE_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!cfg || !bl || !taps) return fail(BLADE_EINVAL, "cfg, buckets and taps must be non-NULL");
+  const blade_ms_config c = *cfg;
+  if (c.levels < 1 || c.levels > 12) return fail(BLADE_EINVAL, "levels must be in 1..12");
+  if (c.fine_size < 1 || c.fine_size > 9 || !(c.fine_size & 1))
+    return fail(BLADE_EINVAL, "fine_size must be odd in 1..9");
+  if (c.levels == 1 && c.coarse_size != 0) return fail(BLADE_EINVAL, "coarse_size must be 0 when levels == 1");
+  if (c.levels > 1 && (c.coarse_size < 1 || c.coarse_size > 9 || !(c.coarse_size & 1)))
+    return fail(BLADE_EINVAL, "coarse_size must be odd in 1..9 when levels > 1");
+  if (c.n_phases != 1 && c.n_phases != 4) return fail(BLADE_EINVAL, "n_phases must be 1 or 4");
+  if (c.levels == 1 && c.n_phases != 1) return fail(BLADE_EINVAL, "n_phases must be 1 when levels == 1");
+  if (c.n_filter_channels != 1 && c.n_filter_channels != 3)
+    return fail(BLADE_EINVAL, "n_filter_channels must be 1 or 3");
+  if (c.n_filter_channels == 3)
+    return fail(BLADE_EUNSUPPORTED, "per-channel (YCbCr) banks are not built (SURVEY.md §8 f1)");
+  if (c.window_size < 1 || c.window_size > 7 || !(c.window_size & 1))
+    return fail(BLADE_EINVAL, "window_size must be odd in 1..7");
+  if (!(c.window_sigma > 0.0f) || !std::isfinite(c.window_sigma))
+    return fail(BLADE_EINVAL, "window_sigma must be finite and > 0");
+  if (c.clamp_output != 0 && c.clamp_output != 1) return fail(BLADE_EINVAL, "clamp_output must be 0 or 1");
+  if (bl->n_orient < 1 || bl->n_strength < 1 || bl->n_coherence < 1)
+    return fail(BLADE_EINVAL, "bucket counts must be >= 1");
+  if (bl->n_strength - 1 > kMaxThr || bl->n_coherence - 1 > kMaxThr)
+    return fail(BLADE_EUNSUPPORTED, "at most %d thresholds per feature", kMaxThr);
+  const long long K = (long long)bl->n_orient * bl->n_strength * bl->n_coherence;
+  if (K > 256) return fail(BLADE_EUNSUPPORTED, "K = %lld > 256 needs uint16 maps (SURVEY.md §8 f2)", K);
+  if ((bl->n_strength > 1 && !bl->strength_thresholds) || (bl->n_coherence > 1 && !bl->coherence_thresholds))
+    return fail(BLADE_EINVAL, "threshold arrays must be non-NULL");
+  const int n_stages = std::max(c.levels - 1, 1);
+  const int nf2 = c.fine_size * c.fine_size;
+  const int nc2 = c.levels > 1 ? c.coarse_size * c.coarse_size : 0;
+  const int nt = nf2 + nc2;
+  const size_t expect = (size_t)n_stages * c.n_filter_channels * c.n_phases * K * nt;
+  if (n_taps != expect)
+    return fail(BLADE_ESHAPE, "n_taps = %zu, expected %zu = stages %d x channels %d x phases %d x K %lld x %d",
+                n_taps, expect, n_stages, c.n_filter_channels, c.n_phases, K, nt);
+  for (size_t i = 0; i < n_taps; ++i)
+    if (!std::isfinite(taps[i])) return fail(BLADE_ENONFINITE, "tap %zu is not finite", i);
+  auto check_thr = [&](const double* t, int cnt, const char* name) -> blade_status {
+    for (int s = 0; s < n_stages; ++s)
+      for (int i = 0; i < cnt; ++i) {
+        const double v = t[(size_t)s * cnt + i];
+        if (!std::isfinite(v)) return fail(BLADE_ENONFINITE, "%s threshold [%d][%d] not finite", name, s, i);
+        if (i > 0 && !(v > t[(size_t)s * cnt + i - 1]))
+          return fail(BLADE_EINVAL, "%s thresholds of stage %d not strictly ascending", name, s);
+      }
+    return BLADE_OK;
+  };
+  blade_status st;
+  if ((st = check_thr(bl->strength_thresholds, bl->n_strength - 1, "strength")) != BLADE_OK) return st;
+  if ((st = check_thr(bl->coherence_thresholds, bl->n_coherence - 1, "coherence")) != BLADE_OK) return st;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BLADE_EDEVICE, "no CUDA device");
+  }
+  if (device < 0 || device >= ndev) return fail(BLADE_EDEVICE, "device %d out of range (%d devices)", device, ndev);
+  DeviceGuard guard(device);
+  if (!guard.ok) return fail(BLADE_EDEVICE, "cudaSetDevice(%d) failed", device);
+
+  // ---- pick the stage kernel variant: largest BY whose shared memory fits
+  int max_smem = 0, nsm = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  const int S = nt | 1;                   // odd tap stride (bank-conflict spread)
+  const int PS = (int)((K * S + 3) & ~3LL);  // phase stride, 16-B aligned
+  const int want_rs = c.levels == 1 ? 1 : 2;
+  const StageVariant* best = nullptr;
+  size_t best_smem = 0;
+  static const std::vector<StageVariant> variants = stage_variants();
+  for (const auto& v : variants) {
+    if (v.nf != c.fine_size || v.nc != (c.levels > 1 ? c.coarse_size : 0) || v.rs != want_rs) continue;
+    const int nph_cta = c.n_phases == 4 ? (v.rs == 2 ? 2 : 4) : 1;
+    const size_t smem = sizeof(float) * ((((size_t)nph_cta * PS) + 3) / 4 * 4 + (size_t)v.tile_floats);
+    if (smem > (size_t)max_smem) continue;
+    if (!best || v.by > best->by) {
+      best = &v;
+      best_smem = smem;
+    }
+  }
+  if (!best)
+    return fail(BLADE_EUNSUPPORTED, "no stage kernel for fine %d / coarse %d with K = %lld (built: 3/5/7/9 "
+                "single-level; 3+3, 5+5, 7+7, 9+9, 7+5, 5+3, 9+7 pairs)", c.fine_size, c.coarse_size, K);
+
+  blade_ms* h = new blade_ms();
+  h->cfg = c;
+  h->n_o = bl->n_orient;
+  h->n_s = bl->n_strength;
+  h->n_c = bl->n_coherence;
+  h->K = (int)K;
+  h->n_stages = n_stages;
+  h->nt = nt;
+  h->S = S;
+  h->PS = PS;
+  h->device = device;
+  h->num_sms = nsm;
+  h->stage = *best;
+  h->stage_smem = best_smem;
+  h->sel_fn = selector_kernel(c.window_size);
+
+  // ---- selector parameters per stage: window weights (fp64 -> fp32), thresholds rounded up
+  const int r = c.window_size / 2;
+  double e[8], se = 0.0;
+  for (int d = -r; d <= r; ++d) {
+    e[d + r] = std::exp(-(double)(d * d) / (2.0 * (double)c.window_sigma * (double)c.window_sigma));
+    se += e[d + r];
+  }
+  auto round_up_f32 = [](double v) {
+    float f = (float)v;
+    if ((double)f < v) f = std::nextafter(f, INFINITY);
+    return f;
+  };
+  h->sel.resize(n_stages);
+  for (int s = 0; s < n_stages; ++s) {
+    SelParams& sp = h->sel[s];
+    memset(&sp, 0, sizeof sp);
+    for (int d = 0; d < c.window_size; ++d) sp.w[d] = (float)(e[d] / se);
+    sp.n_o = bl->n_orient;
+    sp.n_s = bl->n_strength;
+    sp.n_c = bl->n_coherence;
+    for (int i = 0; i < bl->n_strength - 1; ++i)
+      sp.ts[i] = round_up_f32(bl->strength_thresholds[(size_t)s * (bl->n_strength - 1) + i]);
+    for (int i = 0; i < bl->n_coherence - 1; ++i)
+      sp.tc[i] = round_up_f32(bl->coherence_thresholds[(size_t)s * (bl->n_coherence - 1) + i]);
+  }
+
+  // ---- bank re-layout: host [stage][ch=1][phase][K][nt] -> device [stage][phase][PS]
+  const size_t dev_floats = (size_t)n_stages * c.n_phases * PS;
+  std::vector<float> relaid(dev_floats, 0.0f);
+  for (int s = 0; s < n_stages; ++s)
+    for (int p = 0; p < c.n_phases; ++p)
+      for (long long k = 0; k < K; ++k) {
+        const float* src = taps + (((size_t)s * c.n_phases + p) * K + k) * nt;
+        float* dst = relaid.data() + ((size_t)s * c.n_phases + p) * PS + (size_t)k * S;
+        memcpy(dst, src, sizeof(float) * nt);
+      }
+  h->bank_bytes = sizeof(float) * dev_floats;
+  if (cudaMalloc(&h->d_bank, h->bank_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    delete h;
+    return fail(BLADE_ENOMEM, "cudaMalloc(%zu) for the bank failed", dev_floats * sizeof(float));
+  }
+  cudaError_t ce = cudaMemcpy(h->d_bank, relaid.data(), h->bank_bytes, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess)
+    ce = cudaFuncSetAttribute(h->stage.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->stage_smem);
+  int occ = 0;
+  if (ce == cudaSuccess)
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->stage.fn, h->stage.threads, h->stage_smem);
+  if (ce != cudaSuccess || occ < 1) {
+    cudaFree(h->d_bank);
+    delete h;
+    return fail(BLADE_ECUDA, "stage kernel setup failed: %s (occupancy %d)", cudaGetErrorString(ce), occ);
+  }
+  h->stage_ctas_per_sm = occ;
+  *out = h;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_set_profiling(blade_ms_t h, int32_t enable) {
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  h->profiling = enable != 0;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_profile_read(blade_ms_t h, double* ms, int32_t* count) {
+  if (!h || !ms || !count) return fail(BLADE_EINVAL, "NULL argument");
+  DeviceGuard guard(h->device);
+  for (int i = 0; i < 48; ++i) {
+    ms[i] = 0.0;
+    count[i] = 0;
+  }
+  blade_status rs = BLADE_OK;
+  for (auto& r : h->prof) {
+    float t = 0.0f;
+    cudaError_t e = cudaEventSynchronize(r.e1);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.e0, r.e1);
+    if (e != cudaSuccess && rs == BLADE_OK) rs = fail(BLADE_ECUDA, "profile read: %s", cudaGetErrorString(e));
+    const int idx = r.kind * 16 + std::min(r.level, 15);
+    ms[idx] += t;
+    count[idx] += 1;
+    h->ev_pool.push_back(r.e0);
+    h->ev_pool.push_back(r.e1);
+  }
+  h->prof.clear();
+  return rs;
+}
+
+blade_status blade_ms_destroy(blade_ms_t h) {
+  if (!h) return BLADE_OK;
+  DeviceGuard guard(h->device);
+  for (auto& r : h->prof) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  for (auto e : h->ev_pool) cudaEventDestroy(e);
+  cudaFree(h->d_bank);
+  delete h;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_get_info(blade_ms_t h, blade_ms_info* info) {
+  if (!h || !info) return fail(BLADE_EINVAL, "NULL argument");
+  info->levels = h->cfg.levels;
+  info->fine_size = h->cfg.fine_size;
+  info->coarse_size = h->cfg.coarse_size;
+  info->n_phases = h->cfg.n_phases;
+  info->n_stages = h->n_stages;
+  info->K = h->K;
+  info->device = h->device;
+  info->bank_bytes_device = h->bank_bytes;
+  info->stage_smem_bytes = h->stage_smem;
+  info->stage_phase_groups = h->stage.rs;
+  return BLADE_OK;
+}
+
+static blade_status check_dims(int32_t N, int32_t H, int32_t W) {
+  if (N < 0 || H < 1 || W < 1) return fail(BLADE_EINVAL, "need N >= 0, H >= 1, W >= 1 (got %d, %d, %d)", N, H, W);
+  if ((long long)H * W * 3 > (1LL << 31) - 1)
+    return fail(BLADE_EINVAL, "a frame of %d x %d exceeds 2^31 samples", H, W);
+  if (N > 65535) return fail(BLADE_EINVAL, "N > 65535 frames per call");
+  return BLADE_OK;
+}
+
+blade_status blade_ms_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t W, size_t* bytes) {
+  if (!h || !bytes) return fail(BLADE_EINVAL, "NULL argument");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  Plan p;
+  plan_rows(h, N, H, W, 0, H, p);
+  *bytes = p.ws_bytes;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t* count) {
+  if (!h || !count) return fail(BLADE_EINVAL, "NULL argument");
+  (void)H;
+  (void)W;
+  const int L = h->cfg.levels;
+  *count = N == 0 ? 0 : (L - 1) + 2 * (L == 1 ? 1 : L - 1);
+  return BLADE_OK;
+}
+
+static blade_status common_checks(blade_ms_t h, const void* in, const void* out, int32_t N, int32_t H,
+                                  int32_t W, void* ws, size_t ws_bytes, const Plan& p) {
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  if (N > 0 && !in) return fail(BLADE_EINVAL, "in is NULL");
+  if (N > 0 && !ws && p.ws_bytes > 0) return fail(BLADE_EINVAL, "workspace is NULL");
+  if (ws_bytes < p.ws_bytes) return fail(BLADE_ESHAPE, "workspace %zu bytes < required %zu", ws_bytes, p.ws_bytes);
+  (void)out;
+  (void)H;
+  (void)W;
+  blade_status s;
+  if (N > 0) {
+    if ((s = check_dev_ptr(h, in, "in")) != BLADE_OK) return s;
+    if ((s = check_dev_ptr(h, ws, "workspace")) != BLADE_OK) return s;
+  }
+  return BLADE_OK;
+}
+
+blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t N, int32_t H,
+                              int32_t W, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  if (N == 0) return BLADE_OK;
+  Plan p;
+  plan_rows(h, N, H, W, 0, H, p);
+  if ((s = common_checks(h, in, out, N, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  if (!out) return fail(BLADE_EINVAL, "out is NULL");
+  if ((s = check_dev_ptr(h, out, "out")) != BLADE_OK) return s;
+  const size_t img = sizeof(float) * (size_t)N * 3 * H * W;
+  if (ranges_overlap(in, img, out, img)) return fail(BLADE_EINVAL, "out overlaps in");
+  if (ranges_overlap(ws, p.ws_bytes, out, img) || ranges_overlap(ws, p.ws_bytes, in, img))
+    return fail(BLADE_EINVAL, "workspace overlaps in/out");
+  DeviceGuard guard(h->device);
+  LevelView inv = make_view(const_cast<float*>(in), H, W, Range{0, H});
+  LevelView outv = make_view(out, H, W, Range{0, H});
+  return enqueue(h, p, inv, outv, (char*)ws, (cudaStream_t)stream, true, nullptr, nullptr);
+}
+
+blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W,
+                               uint8_t* const* maps, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  if (!maps) return fail(BLADE_EINVAL, "maps_per_level is NULL");
+  if (N == 0) return BLADE_OK;
+  Plan p;
+  plan_rows(h, N, H, W, 0, H, p);
+  if ((s = common_checks(h, in, nullptr, N, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  for (int l = 0; l < h->n_stages; ++l)
+    if (maps[l] && (s = check_dev_ptr(h, maps[l], "maps_per_level[l]")) != BLADE_OK) return s;
+  DeviceGuard guard(h->device);
+  LevelView inv = make_view(const_cast<float*>(in), H, W, Range{0, H});
+  return enqueue(h, p, inv, LevelView{}, (char*)ws, (cudaStream_t)stream, false, maps, nullptr);
+}
+
+blade_status blade_ms_pyramid(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W,
+                              float* const* levels, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  if (!levels) return fail(BLADE_EINVAL, "levels is NULL");
+  if (N == 0) return BLADE_OK;
+  Plan p;
+  plan_rows(h, N, H, W, 0, H, p);
+  if ((s = common_checks(h, in, nullptr, N, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  for (int l = 1; l < h->cfg.levels; ++l) {
+    if (!levels[l - 1]) return fail(BLADE_EINVAL, "levels[%d] is NULL", l - 1);
+    if ((s = check_dev_ptr(h, levels[l - 1], "levels[l]")) != BLADE_OK) return s;
+  }
+  DeviceGuard guard(h->device);
+  LevelView inv = make_view(const_cast<float*>(in), H, W, Range{0, H});
+  return enqueue(h, p, inv, LevelView{}, (char*)ws, (cudaStream_t)stream, false, nullptr, levels);
+}
+
+blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32_t out_rows,
+                                int32_t* in_row0, int32_t* in_rows) {
+  if (!h || !in_row0 || !in_rows) return fail(BLADE_EINVAL, "NULL argument");
+  if (H < 1 || out_row0 < 0 || out_rows < 1 || out_row0 + out_rows > H)
+    return fail(BLADE_EINVAL, "bad band [%d, %d) of H = %d", out_row0, out_row0 + out_rows, H);
+  Plan p;
+  plan_rows(h, 1, H, 1, out_row0, out_rows, p);
+  *in_row0 = p.z[0].lo;
+  *in_rows = p.z[0].n();
+  return BLADE_OK;
+}
+
+blade_status blade_ms_band_workspace_size(blade_ms_t h, int32_t H, int32_t W, int32_t out_row0,
+                                          int32_t out_rows, size_t* bytes) {
+  if (!h || !bytes) return fail(BLADE_EINVAL, "NULL argument");
+  if (H < 1 || W < 1 || out_row0 < 0 || out_rows < 1 || out_row0 + out_rows > H)
+    return fail(BLADE_EINVAL, "bad band");
+  Plan p;
+  plan_rows(h, 1, H, W, out_row0, out_rows, p);
+  *bytes = p.ws_bytes;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t in_row0, int32_t in_rows,
+                                   float* out_band, int32_t out_row0, int32_t out_rows, int32_t H,
+                                   int32_t W, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(1, H, W);
+  if (s != BLADE_OK) return s;
+  if (out_row0 < 0 || out_rows < 1 || out_row0 + out_rows > H)
+    return fail(BLADE_EINVAL, "bad output band [%d, %d) of H = %d", out_row0, out_row0 + out_rows, H);
+  if (!in_band || !out_band) return fail(BLADE_EINVAL, "NULL band pointer");
+  Plan p;
+  plan_rows(h, 1, H, W, out_row0, out_rows, p);
+  if (in_row0 < 0 || in_rows < 1 || in_row0 > p.z[0].lo || in_row0 + in_rows < p.z[0].hi || in_row0 + in_rows > H)
+    return fail(BLADE_ESHAPE, "input band [%d, %d) does not cover the needed rows [%d, %d)", in_row0,
+                in_row0 + in_rows, p.z[0].lo, p.z[0].hi);
+  if ((s = common_checks(h, in_band, out_band, 1, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  if ((s = check_dev_ptr(h, out_band, "out_band")) != BLADE_OK) return s;
+  if (ranges_overlap(in_band, sizeof(float) * 3 * (size_t)in_rows * W, out_band,
+                     sizeof(float) * 3 * (size_t)out_rows * W))
+    return fail(BLADE_EINVAL, "out_band overlaps in_band");
+  DeviceGuard guard(h->device);
+  LevelView inv = make_view(const_cast<float*>(in_band), H, W, Range{in_row0, in_row0 + in_rows});
+  LevelView outv = make_view(out_band, H, W, Range{out_row0, out_row0 + out_rows});
+  return enqueue(h, p, inv, outv, (char*)ws, (cudaStream_t)stream, true, nullptr, nullptr);
+}
+
+blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* out_host, int32_t N,
+                                   int32_t H, int32_t W, float* d_in, float* d_out, void* ws,
+                                   size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  if (N == 0) return BLADE_OK;
+  if (!in_host || !out_host || !d_in || !d_out) return fail(BLADE_EINVAL, "NULL buffer");
+  Plan pfull;
+  plan_rows(h, N, H, W, 0, H, pfull);
+  if ((s = common_checks(h, d_in, d_out, N, H, W, ws, ws_bytes, pfull)) != BLADE_OK) return s;
+  if ((s = check_dev_ptr(h, d_out, "d_out")) != BLADE_OK) return s;
+  const size_t fbytes = sizeof(float) * 3 * (size_t)H * W;
+  if (ranges_overlap(d_in, fbytes * N, d_out, fbytes * N)) return fail(BLADE_EINVAL, "d_out overlaps d_in");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  // chunked frame pipeline: H2D (chunk i+1) || compute (chunk i) || D2H (chunk i-1)
+  const int nchunks = std::min<int>(N, 8);
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in(nchunks, nullptr), ev_done(nchunks, nullptr);
+  cudaEvent_t ev_start = nullptr;
+  blade_status rs = BLADE_OK;
+  auto cleanup = [&]() {
+    for (auto& e : ev_in) if (e) cudaEventDestroy(e);
+    for (auto& e : ev_done) if (e) cudaEventDestroy(e);
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+  };
+  cudaError_t ce = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  for (int i = 0; i < nchunks && ce == cudaSuccess; ++i) {
+    ce = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
+  }
+  // the copies must not start before work already queued on the caller's stream
+  if (ce == cudaSuccess) ce = cudaEventRecord(ev_start, st);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_in, ev_start, 0);
+  if (ce != cudaSuccess) {
+    cleanup();
+    return fail(BLADE_ECUDA, "stream/event setup: %s", cudaGetErrorString(ce));
+  }
+  int f0 = 0;
+  for (int i = 0; i < nchunks && rs == BLADE_OK; ++i) {
+    const int nf = (N - f0) / (nchunks - i);
+    const size_t off = (size_t)f0 * 3 * H * W;
+    ce = cudaMemcpyAsync(d_in + off, in_host + off, fbytes * nf, cudaMemcpyHostToDevice, s_in);
+    if (ce == cudaSuccess) ce = cudaEventRecord(ev_in[i], s_in);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(st, ev_in[i], 0);
+    if (ce != cudaSuccess) { rs = fail(BLADE_ECUDA, "H2D: %s", cudaGetErrorString(ce)); break; }
+    Plan p;
+    plan_rows(h, nf, H, W, 0, H, p);
+    LevelView inv = make_view(d_in + off, H, W, Range{0, H});
+    LevelView outv = make_view(d_out + off, H, W, Range{0, H});
+    rs = enqueue(h, p, inv, outv, (char*)ws, st, true, nullptr, nullptr);
+    if (rs != BLADE_OK) break;
+    ce = cudaEventRecord(ev_done[i], st);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_out, ev_done[i], 0);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpyAsync(out_host + off, d_out + off, fbytes * nf, cudaMemcpyDeviceToHost, s_out);
+    if (ce != cudaSuccess) { rs = fail(BLADE_ECUDA, "D2H: %s", cudaGetErrorString(ce)); break; }
+    f0 += nf;
+  }
+  ce = cudaStreamSynchronize(s_out);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  if (rs == BLADE_OK && ce != cudaSuccess) rs = fail(BLADE_ECUDA, "sync: %s", cudaGetErrorString(ce));
+  cleanup();
+  return rs;
+}
+
+}  // extern "C"

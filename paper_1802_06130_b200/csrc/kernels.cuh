@@ -1,0 +1,441 @@
+// Hot-path kernels of the multiscale BLADE denoiser for B200 (sm_100a).
+//
+//   K1 k_decimate : z^{l+1} = 8-tap antialiased bicubic 2x decimation of z^l
+//                   (§4 "Standard bicubic downsampling"; R14)
+//   K2 k_selector : s^l = bucket(theta, strength, coherence) of the joint-colour structure
+//                   tensor of z^l (§3 Eq. 6; R3-R8)
+//   K3 k_stage    : u^l = sum f u^{l+1}_{i/2+j} + sum g z^l_{i+j}  (§4 Eq. 9);
+//                   Eq. 1 when there is no coarse block.
+//
+// All arithmetic is FP32 on the CUDA cores (no fast-math: IEEE sqrt/div, accurate atan2f).
+// Tensor cores are not used: every pixel contracts with its own selected filter, so the
+// contraction is a batched dot product, not a GEMM.
+//
+// Images are viewed through LevelView: a level of a batch, possibly a row band of it. Every
+// index is GLOBAL (rows of the full level image); folds happen at the true image border
+// (R2 / H7), so a band computes bit-identical values to the full image.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace blade {
+
+struct LevelView {
+  float* p;         // frame 0, channel 0, buffer row 0
+  int H, W;         // global level dims
+  int row0, rows;   // the buffer holds global rows [row0, row0 + rows)
+  long long plane;  // floats per channel plane of the buffer (rows * W)
+  long long frame;  // floats per frame of the buffer (3 * plane)
+};
+
+// [R2] half-sample symmetric fold, periodic with period 2n.
+__device__ __forceinline__ int fold_idx(int i, int n) {
+  if (i >= 0 && i < n) return i;
+  if (i < 0 && i >= -n) return -i - 1;
+  if (i >= n && i < 2 * n) return 2 * n - 1 - i;
+  int p = 2 * n;
+  int m = i % p;
+  if (m < 0) m += p;
+  return m < n ? m : p - 1 - m;
+}
+
+// Buffer row of global row y (folded), clamped into the buffer as a safety net.
+__device__ __forceinline__ int view_row(const LevelView& v, int y) {
+  int r = fold_idx(y, v.H) - v.row0;
+  return min(max(r, 0), v.rows - 1);
+}
+
+// ------------------------------------------------------------------------------------------
+// K1 decimation. Weights: Keys cubic (a = -0.5) at |t|/2, t = -3.5..3.5, normalised:
+// [-3, -9, 29, 111, 111, 29, -9, -3] / 256, exact in fp32. Output (y, x) reads input rows
+// 2y-3 .. 2y+4 and columns 2x-3 .. 2x+4 (centre at 2y + 0.5). Separable: horizontal pass into
+// shared memory, then vertical. The per-pixel arithmetic does not depend on the tile.
+// ------------------------------------------------------------------------------------------
+namespace dec {
+constexpr int TX = 32, TY = 16;
+constexpr int IN_R = 2 * TY + 6, IN_C = 2 * TX + 6;
+}  // namespace dec
+
+__device__ __forceinline__ float dec_w(int a) {
+  // constexpr table in registers: fp32-exact k/256
+  const float w0 = -3.0f / 256.0f, w1 = -9.0f / 256.0f, w2 = 29.0f / 256.0f, w3 = 111.0f / 256.0f;
+  switch (a) {
+    case 0: case 7: return w0;
+    case 1: case 6: return w1;
+    case 2: case 5: return w2;
+    default: return w3;
+  }
+}
+
+// grid: (ceil(W_out / TX), ceil(out_rows / TY), N); block (32, 8)
+__global__ void __launch_bounds__(256) k_decimate(LevelView in, LevelView out, int out_r0,
+                                                  int out_rn) {
+  __shared__ float tile[dec::IN_R][dec::IN_C + 1];
+  __shared__ float hp[dec::IN_R][dec::TX + 1];
+  const int n = blockIdx.z;
+  const int ox0 = blockIdx.x * dec::TX;
+  const int oy0 = out_r0 + blockIdx.y * dec::TY;  // global output row of the tile
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const float* src = in.p + (long long)n * in.frame;
+  float* dst = out.p + (long long)n * out.frame;
+  for (int c = 0; c < 3; ++c) {
+    const float* sp = src + c * in.plane;
+    for (int i = tid; i < dec::IN_R * dec::IN_C; i += 256) {
+      const int r = i / dec::IN_C, q = i - r * dec::IN_C;
+      const int gy = 2 * oy0 - 3 + r, gx = 2 * ox0 - 3 + q;
+      tile[r][q] = __ldg(sp + (long long)view_row(in, gy) * in.W + fold_idx(gx, in.W));
+    }
+    __syncthreads();
+    for (int i = tid; i < dec::IN_R * dec::TX; i += 256) {
+      const int r = i / dec::TX, j = i - r * dec::TX;
+      float acc = 0.0f;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc = fmaf(dec_w(b), tile[r][2 * j + b], acc);
+      hp[r][j] = acc;
+    }
+    __syncthreads();
+    const int j = threadIdx.x;
+    const int ox = ox0 + j;
+#pragma unroll
+    for (int k = 0; k < dec::TY / 8; ++k) {
+      const int i = threadIdx.y + 8 * k;
+      const int oy = oy0 + i;
+      if (ox < out.W && oy < out_r0 + out_rn) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) acc = fmaf(dec_w(a), hp[2 * i + a][j], acc);
+        dst[c * out.plane + (long long)(oy - out.row0) * out.W + ox] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2 selector. Per pixel: central-difference gradients of the folded image [R3], per-channel
+// products summed over RGB (Eq. 6) kept as T = sum gx^2+gy^2, D = sum (gx-gy)(gx+gy) and
+// B = sum gx gy (D avoids the a - c cancellation), separable Gaussian window [R4], closed-form
+// eigen-features and the quantiser [R7]:
+//   lambda_{1,2} = T/2 +- sqrt((D/2)^2 + B^2), S = sqrt(l1), C = (sqrt l1 - sqrt l2)/(sqrt l1 +
+//   sqrt l2), theta = (atan2(2B, D)/2 + pi/2) mod pi  (0 when D == 0 and B == 0) [R5, R6],
+//   o = floor(theta n_o / pi) mod n_o = floor(atan2(2B, D) n_o/(2 pi) + n_o/2) mod n_o.
+// ------------------------------------------------------------------------------------------
+constexpr int kMaxThr = 15;
+struct SelParams {
+  float w[8];  // window weights e(d)/sum e, d = -r..r (normalised in fp64, rounded to fp32)
+  int n_o, n_s, n_c;
+  float ts[kMaxThr];  // strength thresholds (rounded up to fp32)
+  float tc[kMaxThr];  // coherence thresholds
+};
+
+namespace sel {
+constexpr int TX = 32, TY = 16;
+}
+
+template <int WS>
+__global__ void __launch_bounds__(256) k_selector(LevelView z, uint8_t* map, int map_row0,
+                                                  int map_rows, int out_r0, int out_rn,
+                                                  SelParams prm) {
+  constexpr int RW = WS / 2;    // window radius
+  constexpr int R = RW + 1;     // halo of the image tile
+  constexpr int ZR = sel::TY + 2 * R, ZC = sel::TX + 2 * R;
+  constexpr int FR = sel::TY + 2 * RW, FC = sel::TX + 2 * RW;
+  __shared__ float zt[3][ZR][ZC];
+  __shared__ float F[3][FR][FC + 1];
+  __shared__ float Hq[3][FR][sel::TX + 1];
+  const int n = blockIdx.z;
+  const int ox0 = blockIdx.x * sel::TX;
+  const int oy0 = out_r0 + blockIdx.y * sel::TY;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const float* src = z.p + (long long)n * z.frame;
+  for (int i = tid; i < 3 * ZR * ZC; i += 256) {
+    const int c = i / (ZR * ZC);
+    const int rem = i - c * ZR * ZC;
+    const int r = rem / ZC, q = rem - r * ZC;
+    zt[c][r][q] = __ldg(src + c * z.plane + (long long)view_row(z, oy0 - R + r) * z.W +
+                        fold_idx(ox0 - R + q, z.W));
+  }
+  __syncthreads();
+  for (int i = tid; i < FR * FC; i += 256) {
+    const int r = i / FC, q = i - r * FC;
+    float T = 0.0f, D = 0.0f, B = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float gx = (zt[c][r + 1][q + 2] - zt[c][r + 1][q]) * 0.5f;
+      const float gy = (zt[c][r + 2][q + 1] - zt[c][r][q + 1]) * 0.5f;
+      T = fmaf(gx, gx, fmaf(gy, gy, T));
+      D = fmaf(gx - gy, gx + gy, D);
+      B = fmaf(gx, gy, B);
+    }
+    F[0][r][q] = T;
+    F[1][r][q] = D;
+    F[2][r][q] = B;
+  }
+  __syncthreads();
+  for (int i = tid; i < 3 * FR * sel::TX; i += 256) {
+    const int f = i / (FR * sel::TX);
+    const int rem = i - f * FR * sel::TX;
+    const int r = rem / sel::TX, j = rem - r * sel::TX;
+    float acc = 0.0f;
+#pragma unroll
+    for (int d = 0; d < WS; ++d) acc = fmaf(prm.w[d], F[f][r][j + d], acc);
+    Hq[f][r][j] = acc;
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  const int ox = ox0 + j;
+  const float kTwoPiInv = 0.15915494309189535f;  // 1 / (2 pi)
+#pragma unroll
+  for (int k = 0; k < sel::TY / 8; ++k) {
+    const int i = threadIdx.y + 8 * k;
+    const int oy = oy0 + i;
+    if (ox >= z.W || oy >= out_r0 + out_rn) continue;
+    float T = 0.0f, D = 0.0f, B = 0.0f;
+#pragma unroll
+    for (int d = 0; d < WS; ++d) {
+      T = fmaf(prm.w[d], Hq[0][i + d][j], T);
+      D = fmaf(prm.w[d], Hq[1][i + d][j], D);
+      B = fmaf(prm.w[d], Hq[2][i + d][j], B);
+    }
+    const float half_tr = 0.5f * T;
+    const float hd = 0.5f * D;
+    const float r = sqrtf(fmaf(hd, hd, B * B));
+    const float l1 = half_tr + r;
+    const float l2 = fmaxf(half_tr - r, 0.0f);
+    const float s1 = sqrtf(fmaxf(l1, 0.0f)), s2 = sqrtf(l2);
+    const float coh = l1 > 0.0f ? __fdiv_rn(s1 - s2, s1 + s2) : 0.0f;
+    int o = 0;
+    if (!(D == 0.0f && B == 0.0f)) {
+      const float phi = atan2f(2.0f * B, D);
+      o = (int)floorf(fmaf(phi, (float)prm.n_o * kTwoPiInv, 0.5f * (float)prm.n_o));
+      o %= prm.n_o;
+      if (o < 0) o += prm.n_o;
+    }
+    int s = 0, kk = 0;
+    for (int t = 0; t < prm.n_s - 1; ++t) s += (prm.ts[t] <= s1);
+    for (int t = 0; t < prm.n_c - 1; ++t) kk += (prm.tc[t] <= coh);
+    map[(long long)n * map_rows * z.W + (long long)(oy - map_row0) * z.W + ox] =
+        (uint8_t)((o * prm.n_s + s) * prm.n_c + kk);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3 stage (Eq. 9 / Eq. 1). Persistent CTAs: each CTA copies the filterbank of its stage (the
+// phases it needs) into shared memory ONCE and then loops over output tiles. Per tile it
+// stages the fine patch of z^l (tile + r_f halo, 3 channels) and the coarse patch of u^{l+1}
+// (tile/2 + r_c halo) in shared memory, folded at the true image border. Each thread computes
+// a 2 x 2 pixel block: columns x, x+1 (same coarse column floor(x/2)) and rows y, y+RS.
+//   RS == 1: a CTA holds all phases; its rows are contiguous (a 2x2 quad shares the coarse
+//            centre).
+//   RS == 2: CTAs are specialised by output-row parity (the bank of two phases fits in
+//            shared memory for 7x7 / 9x9 pairs); a thread computes rows y and y + 2.
+// The three colour channels share the taps [R13]: one tap load feeds 3 FMAs.
+// ------------------------------------------------------------------------------------------
+struct StageArgs {
+  LevelView z;         // z^l
+  LevelView u1;        // u^{l+1} (unused when NC == 0)
+  LevelView out;       // u^l (output rows [out_r0, out_r0 + out_rn))
+  const uint8_t* map;  // s^l, [N][map_rows][W], buffer row 0 = global row map_row0
+  int map_row0, map_rows;
+  const float* bank;   // device bank of this stage: [phase][PS floats: K x S taps, padded]
+  int K, S, PS;        // buckets, padded tap stride (odd), phase stride (multiple of 4)
+  int n_phases;        // 1 or 4
+  int N;               // frames
+  int out_r0, out_rn;  // global output rows
+  int tiles_x, tiles_y, n_tiles;
+  int clamp;           // clamp output to [0, 1]
+};
+
+template <int NF, int NC, int RS, int BY>
+struct StageShape {
+  static constexpr int BX = 32;
+  static constexpr int RF = NF / 2, RC = NC / 2;
+  static constexpr int TCOLS = 2 * BX;             // output columns per tile
+  static constexpr int TROWS = 2 * BY * RS;        // output rows per tile (span)
+  static constexpr int FR = TROWS + 2 * RF;        // fine tile rows
+  static constexpr int FC = TCOLS + 2 * RF;        // fine tile cols
+  static constexpr int FCP = FC + ((FC & 1) ? 1 : 2);  // even pitch (float2 loads)
+  static constexpr int CR = NC ? TROWS / 2 + 2 * RC : 0;
+  static constexpr int CC = NC ? BX + 2 * RC : 0;
+  static constexpr int CCP = NC ? CC + 1 : 0;
+  static constexpr int NPH_CTA = RS == 2 ? 2 : 4;  // phases a CTA holds when n_phases == 4
+  static constexpr int tile_floats = 3 * FR * FCP + 3 * CR * CCP;
+  static constexpr int threads = BX * BY;
+};
+
+template <int NF, int NC, int RS, int BY>
+__global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
+  using SS = StageShape<NF, NC, RS, BY>;
+  constexpr int RF = SS::RF, RC = SS::RC;
+  extern __shared__ __align__(16) float smem[];
+  const int nph_cta = a.n_phases == 4 ? SS::NPH_CTA : 1;
+  const int bank_floats = nph_cta * a.PS;
+  float* sbank = smem;
+  float* sfine = smem + ((bank_floats + 3) & ~3);
+  float* scoarse = sfine + 3 * SS::FR * SS::FCP;
+
+  const int par = RS == 2 ? (int)(blockIdx.x & 1) : 0;  // output-row parity of this CTA
+  const int group = RS == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ngroups = RS == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int tid = threadIdx.y * SS::BX + threadIdx.x;
+
+  // ---- filterbank -> shared memory, once per CTA
+  {
+    const int ph0 = (a.n_phases == 4 && RS == 2) ? 2 * par : 0;
+    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)ph0 * a.PS);
+    float4* s4 = reinterpret_cast<float4*>(sbank);
+    const int n4 = bank_floats >> 2;
+    for (int i = tid; i < n4; i += SS::threads) s4[i] = __ldg(g4 + i);
+    for (int i = (n4 << 2) + tid; i < bank_floats; i += SS::threads)
+      sbank[i] = __ldg(a.bank + (long long)ph0 * a.PS + i);
+  }
+
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int y_base = (a.out_r0 & ~1);  // tiles start on an even global row
+
+  for (int t = group; t < a.n_tiles; t += ngroups) {
+    const int n = t / (a.tiles_x * a.tiles_y);
+    const int rem = t - n * a.tiles_x * a.tiles_y;
+    const int tyi = rem / a.tiles_x, txi = rem - tyi * a.tiles_x;
+    const int X0 = txi * SS::TCOLS;
+    const int Y0 = y_base + tyi * SS::TROWS;
+
+    __syncthreads();  // previous tile's reads of the staging buffers are done
+    // ---- stage the fine patch (rows Y0-RF .., cols X0-RF ..)
+    {
+      const float* zp = a.z.p + (long long)n * a.z.frame;
+      for (int i = tid; i < SS::FR * SS::FC; i += SS::threads) {
+        const int r = i / SS::FC, q = i - r * SS::FC;
+        const long long ro = (long long)view_row(a.z, Y0 - RF + r) * a.z.W + fold_idx(X0 - RF + q, a.z.W);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          sfine[(c * SS::FR + r) * SS::FCP + q] = __ldg(zp + c * a.z.plane + ro);
+      }
+    }
+    if constexpr (NC > 0) {
+      const float* up = a.u1.p + (long long)n * a.u1.frame;
+      const int CY0 = Y0 / 2 - RC, CX0 = X0 / 2 - RC;
+      for (int i = tid; i < SS::CR * SS::CC; i += SS::threads) {
+        const int r = i / SS::CC, q = i - r * SS::CC;
+        const long long ro = (long long)view_row(a.u1, CY0 + r) * a.u1.W + fold_idx(CX0 + q, a.u1.W);
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          scoarse[(c * SS::CR + r) * SS::CCP + q] = __ldg(up + c * a.u1.plane + ro);
+      }
+    }
+    __syncthreads();
+
+    // ---- this thread's 2x2 block
+    const int x = X0 + 2 * tx;                               // even column
+    const int ly = RS == 2 ? 4 * ty + par : 2 * ty;          // local row of pixel row 0
+    const int y0 = Y0 + ly;
+    const bool row_ok[2] = {y0 >= a.out_r0 && y0 < a.out_r0 + a.out_rn,
+                            y0 + RS >= a.out_r0 && y0 + RS < a.out_r0 + a.out_rn};
+    const bool col_ok[2] = {x < a.z.W, x + 1 < a.z.W};
+    if (!(row_ok[0] || row_ok[1]) || !col_ok[0]) continue;
+
+    const float* tp[2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int yy = y0 + i * RS, xx = min(x + j, a.z.W - 1);
+        int k = 0;
+        if (row_ok[i]) k = a.map[(long long)n * a.map_rows * a.z.W + (long long)(yy - a.map_row0) * a.z.W + xx];
+        int ps = 0;
+        if (a.n_phases == 4) ps = RS == 2 ? j : 2 * (yy & 1) + j;
+        tp[i][j] = sbank + ps * a.PS + k * a.S;
+      }
+
+    float acc[2][2][3];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[i][j][c] = 0.0f;
+
+    // coarse term first (matches nothing in particular; any order is a valid fp32 sum)
+    if constexpr (NC > 0) {
+      // coarse centre row of pixel row i: (y0 + i*RS)/2 -> local (ly + i*RS)/2 + RC - RC
+      const int cx = tx;  // local coarse col of the window start (centre tx + RC)
+#pragma unroll
+      for (int wr = 0; wr < NC + (RS == 2 ? 1 : 0); ++wr) {
+        const int crow = (ly >> 1) + wr;  // local coarse row
+        float v[3][NC];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int q = 0; q < NC; ++q) v[c][q] = scoarse[(c * SS::CR + crow) * SS::CCP + cx + q];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int dy = wr - (RS == 2 ? i : 0);
+          if (dy < 0 || dy >= NC) continue;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int dx = 0; dx < NC; ++dx) {
+              const float tap = tp[i][j][NF * NF + dy * NC + dx];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][dx], acc[i][j][c]);
+            }
+        }
+      }
+    }
+    // fine term
+#pragma unroll
+    for (int wr = 0; wr < NF + RS; ++wr) {
+      const int frow = ly + wr;  // local fine row (tile origin is Y0 - RF)
+      float v[3][NF + 1];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float* rp = sfine + (c * SS::FR + frow) * SS::FCP + 2 * tx;
+#pragma unroll
+        for (int q = 0; q + 1 < NF + 1; q += 2) {
+          const float2 t2 = *reinterpret_cast<const float2*>(rp + q);
+          v[c][q] = t2.x;
+          v[c][q + 1] = t2.y;
+        }
+        if ((NF + 1) & 1) v[c][NF] = rp[NF];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int dy = wr - i * RS;
+        if (dy < 0 || dy >= NF) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int dx = 0; dx < NF; ++dx) {
+            const float tap = tp[i][j][dy * NF + dx];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][j + dx], acc[i][j][c]);
+          }
+      }
+    }
+
+    // ---- store
+    float* op = a.out.p + (long long)n * a.out.frame;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (!row_ok[i]) continue;
+      const long long ro = (long long)(y0 + i * RS - a.out.row0) * a.out.W;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float v0 = acc[i][0][c], v1 = acc[i][1][c];
+        if (a.clamp) {
+          v0 = fminf(fmaxf(v0, 0.0f), 1.0f);
+          v1 = fminf(fmaxf(v1, 0.0f), 1.0f);
+        }
+        float* d = op + c * a.out.plane + ro + x;
+        if (col_ok[1] && ((reinterpret_cast<uintptr_t>(d) & 7) == 0)) {
+          *reinterpret_cast<float2*>(d) = make_float2(v0, v1);
+        } else {
+          d[0] = v0;
+          if (col_ok[1]) d[1] = v1;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace blade

@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs. Marked `gpu`; run on a B200 with `python -m pytest tests -m gpu`.
+
+Tolerances: bucket maps bit-exact except near-boundary pixels (counted,
+<= 1e-4 of a level); outputs within 1e-4 absolute outside the dependency cone of a bucket
+mismatch; pyramid levels within 1e-5 (8-tap fp32 FIR with L1 gain 1.41); integer/exact cases
+(delta banks, dyadic banks on constant images, band split, batch split) bit-exact.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import blade_synth as bs
+import oracle
+from tests.parity import OUT_ATOL, check_buckets, max_err_outside, taint_cone
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1802_06130_b200 import lib
+    lib()  # fail loudly if the extension is missing
+
+
+def _handle(cfg, taps=None, **kw):
+    from paper_1802_06130_b200 import BladeMS
+    return BladeMS.from_config(cfg, taps=taps, **kw)
+
+
+def _cfg_like(name, H, W, N=1, **over):
+    cfg = bs.load_config(name)
+    cfg.H, cfg.W, cfg.N = H, W, N
+    for k, v in over.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+def _full_parity(cfg, x_np, taps=None, label=""):
+    """Run GPU denoise + selector on x_np [N,3,H,W]; compare with the oracle frame by frame."""
+    taps = cfg.taps() if taps is None else taps
+    h = _handle(cfg, taps)
+    x = torch.from_numpy(x_np).cuda()
+    out = h.denoise(x)
+    maps = h.selector(x)
+    lv = h.pyramid(x)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy()
+    maps = [m.cpu().numpy() for m in maps]
+    lv = [t.cpu().numpy() for t in lv]
+    ts, tc = cfg.thresholds()
+    stats_all = []
+    worst = 0.0
+    for n in range(x_np.shape[0]):
+        parts = oracle.cascade_parts(cfg, x_np[n], taps)
+        for l in range(1, cfg.levels):
+            err = np.abs(lv[l - 1][n] - parts["levels"][l]).max()
+            assert err < 1e-5, f"{label} frame {n} pyramid level {l}: {err}"
+        mism = []
+        for l in range(len(parts["buckets"])):
+            m, st = check_buckets(maps[l][n], parts["buckets"][l], parts["features"][l],
+                                  cfg.n_orient, ts[l], tc[l], f"{label} frame {n} level {l}")
+            mism.append(m)
+            stats_all.append(st)
+        dims = [p.shape[1:] for p in parts["levels"]]
+        tainted = taint_cone(mism, dims, cfg.coarse_size // 2) if cfg.levels > 1 else mism[0]
+        err = max_err_outside(out[n], parts["outputs"][0], tainted)
+        assert err <= OUT_ATOL, f"{label} frame {n}: max |gpu - oracle| = {err}"
+        assert tainted.mean() < 0.01
+        worst = max(worst, err)
+    return out, stats_all, worst
+
+
+# ------------------------------------------------------------------------- the five configs
+
+def test_c0_single_level_full():
+    cfg = bs.load_config("c0")
+    _full_parity(cfg, cfg.batch(), label="c0")
+
+
+def test_c1_full():
+    cfg = bs.load_config("c1")
+    _full_parity(cfg, cfg.batch(), label="c1")
+
+
+def test_c3_frames_batched():
+    """c3 recipe (1080p, 5x5 pairs, L=3) on 2 full frames batched in one call."""
+    cfg = bs.load_config("c3")
+    _full_parity(cfg, cfg.batch(N=2), label="c3")
+
+
+def test_c2_full_size():
+    cfg = bs.load_config("c2")
+    _full_parity(cfg, cfg.batch(), label="c2")
+
+
+def test_c4_full_size():
+    cfg = bs.load_config("c4")
+    _full_parity(cfg, cfg.batch(), label="c4")
+
+
+# ------------------------------------------------------------------------- ragged / edge shapes
+
+@pytest.mark.parametrize("name,H,W,N", [("c1", 203, 333, 2), ("c1", 67, 129, 1), ("c2", 151, 97, 1),
+                                        ("c4", 77, 190, 1), ("c0", 45, 131, 3), ("c3", 130, 259, 2)])
+def test_ragged_shapes(name, H, W, N):
+    cfg = _cfg_like(name, H, W, N)
+    _full_parity(cfg, cfg.batch(), label=f"{name}@{H}x{W}")
+
+
+@pytest.mark.parametrize("name,H,W", [("c1", 1, 1), ("c1", 2, 3), ("c4", 3, 2), ("c0", 1, 5),
+                                      ("c2", 5, 1), ("c4", 9, 17)])
+def test_tiny_images_fold_wraps(name, H, W):
+    """Tiny levels (1x1 .. 2x3) where a 9x9 footprint folds over several periods."""
+    cfg = _cfg_like(name, H, W, 1)
+    _full_parity(cfg, cfg.batch(), label=f"{name}@{H}x{W}")
+
+
+def test_empty_batch_is_noop():
+    cfg = bs.load_config("c1")
+    h = _handle(cfg)
+    x = torch.empty((0, 3, 16, 16), device="cuda")
+    out = h.denoise(x)
+    assert out.shape == x.shape
+
+
+# ------------------------------------------------------------------------- exact cases
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c4"])
+def test_delta_bank_identity_bit_exact(name):
+    cfg = _cfg_like(name, 97, 131, 2)
+    nf = cfg.fine_size
+    nt = nf * nf + (cfg.coarse_size ** 2 if cfg.levels > 1 else 0)
+    taps = np.zeros((cfg.n_stages, 1, cfg.n_phases, cfg.K, nt), np.float32)
+    taps[..., (nf // 2) * nf + nf // 2] = 1.0
+    x = cfg.batch()
+    out = _handle(cfg, taps).denoise(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert np.array_equal(out, x)
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c4"])
+def test_constant_image_dyadic_bank_exact(name, rng):
+    """Filters summing to 1 leave a constant image unchanged (north star), exactly with dyadic
+    taps (products and partial sums are representable in fp32)."""
+    cfg = _cfg_like(name, 70, 90, 1)
+    nf = cfg.fine_size
+    nt = nf * nf + (cfg.coarse_size ** 2 if cfg.levels > 1 else 0)
+    taps = rng.integers(-8, 9, size=(cfg.n_stages, 1, cfg.n_phases, cfg.K, nt)).astype(np.float64)
+    taps[..., 0] += 64 - taps.sum(-1)
+    taps = (taps / 64).astype(np.float32)
+    x = np.full((1, 3, 70, 90), 0.625, np.float32)
+    out = _handle(cfg, taps).denoise(torch.from_numpy(x).cuda()).cpu().numpy()
+    assert (out == 0.625).all()
+    assert (oracle.denoise_config(cfg, x[0], taps) == 0.625).all()
+
+
+def test_batch_equals_per_frame_bit_exact():
+    cfg = _cfg_like("c1", 150, 170, 3)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    full = h.denoise(x)
+    for n in range(3):
+        one = h.denoise(x[n:n + 1].contiguous())
+        assert torch.equal(one[0], full[n])
+
+
+@pytest.mark.parametrize("name,H,W,bands", [("c4", 700, 300, 4), ("c2", 333, 260, 3),
+                                            ("c1", 257, 100, 5)])
+def test_row_bands_bit_identical(name, H, W, bands):
+    """blade_ms_denoise_rows: concatenated band outputs equal the full-image output bit-exactly
+    (BASELINE.json configs[4] split into row bands with a halo covering the pyramid)."""
+    cfg = _cfg_like(name, H, W, 1)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    full = h.denoise(x)[0]
+    edges = np.linspace(0, H, bands + 1).astype(int)
+    parts = []
+    for r0, r1 in zip(edges[:-1], edges[1:]):
+        i0, ni = h.band_rows(H, int(r0), int(r1 - r0))
+        band_in = x[0, :, i0:i0 + ni].contiguous()
+        parts.append(h.denoise_rows(band_in, i0, int(r0), int(r1 - r0), H))
+    assert torch.equal(torch.cat(parts, 1), full)
+
+
+def test_denoise_host_equals_device():
+    cfg = _cfg_like("c3", 120, 200, 5)
+    h = _handle(cfg)
+    xh = torch.from_numpy(cfg.batch()).pin_memory()
+    ref = h.denoise(xh.cuda())
+    outh = torch.empty_like(xh).pin_memory()
+    d_in, d_out = torch.empty_like(ref), torch.empty_like(ref)
+    ws = h.workspace(*cfg.batch().shape[:1], 120, 200)
+    h.denoise_host(xh, outh, d_in, d_out, ws)
+    assert torch.equal(outh, ref.cpu())
+
+
+def test_clamp_output_flag():
+    cfg = _cfg_like("c1", 64, 64, 1)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    raw = _handle(cfg).denoise(x)
+    cl = _handle(cfg, clamp_output=True).denoise(x)
+    assert torch.equal(cl, raw.clamp(0, 1))
