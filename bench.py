@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3")
+    ap.add_argument("--frames", type=int, default=None,
+                    help="override the frame count (profiling only; not a bench line)")
     ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -221,6 +223,8 @@ def main():
     dev = torch.device("cuda", local)
     from paper_1802_06130_b200 import BladeMS
     cfg = bs.load_config(args.config)
+    if args.frames:
+        cfg.N = args.frames
     if cfg.N % world:
         raise SystemExit(f"{cfg.name}: {cfg.N} frames do not split over {world} GPUs")
     n_local = cfg.N // world

@@ -64,7 +64,7 @@ typedef struct {
                                 1 = bucket only (SPEC.md reading); must be 1 if L == 1          */
   int32_t n_filter_channels; /* 1 = one filter for R, G and B [R13]. (3 = per-channel YCbCr
                                 banks, returns BLADE_EUNSUPPORTED)            */
-  int32_t window_size;       /* structure-tensor window, odd 1..7 (configs: 5) [R4]             */
+  int32_t window_size;       /* structure-tensor window: 1, 3 or 5 (configs: 5) [R4]            */
   float window_sigma;        /* Gaussian std of the window, > 0 (configs: 1.5) [R4]             */
   int32_t clamp_output;      /* 0 = raw cascade output (parity); 1 = clamp final u^0 to [0,1]
                                 (SPEC.md:447 clamps only at the end) [R24]                      */
@@ -107,8 +107,8 @@ blade_status blade_ms_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t
 /*
  * Denoise a batch: in, out DEVICE fp32 [N][3][H][W] on the handle's device; N >= 0 (0 is a
  * no-op), H, W >= 1. `out` must not overlap `in` (EINVAL). workspace: device, >= the size
- * from blade_ms_workspace_size (ESHAPE otherwise); contents on return are the pyramid
- * levels, intermediate stage outputs and bucket maps (see blade_ms_workspace_layout).
+ * from blade_ms_workspace_size (ESHAPE otherwise), 16-byte aligned; on return it holds the
+ * pyramid levels (fp32 and fp64 copies), intermediate stage outputs and bucket maps.
  * Output equals a per-frame loop bit-exactly.
  */
 blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t N, int32_t H,

@@ -18,7 +18,7 @@ CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB = PKG / "libblade_ms.so"
 SOURCES = [CSRC / "blade_ms.cu"]
-DEPS = SOURCES + [CSRC / "kernels.cuh", INCLUDE / "blade_ms.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [INCLUDE / "blade_ms.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

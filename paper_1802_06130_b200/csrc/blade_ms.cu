@@ -1,24 +1,34 @@
 // Host side of the C ABI declared in include/blade_ms.h: argument validation, filterbank
-// re-layout, workspace/band planning and the per-level launch sequence.
+// re-layout, workspace/band planning, TMA descriptors and the per-level launch sequence
+// (DESIGN.md §Boundary).
 //
 // The launch sequence for one call:
-//   down pass   K1 z^{l+1} = decimate(z^l),            l = 0 .. L-2
-//   up pass     K2 s^l = selector(z^l); K3 u^l = stage(z^l, u^{l+1}, s^l),  l = L-2 .. 0
-//               (u^{L-1} = z^{L-1}); L == 1: K2 + K3 (Eq. 1) at level 0.
+//   down pass   k_down(l): s^l = selector(z^l) and z^{l+1} = decimate(z^l)     l = 0 .. L-2
+//   up pass     k_stage(l): u^l = stage(z^l, u^{l+1}, s^l)                        l = L-2 .. 0
+//               (u^{L-1} = z^{L-1});  L == 1: k_down (selector only) + k_stage (Eq. 1).
 // Every call is described by a Plan: for each level the GLOBAL rows of z^l and u^l that must be
 // materialised. For a full image these are all rows; for a row band (blade_ms_denoise_rows) they
 // are the band's dependency cone, so the same code serves both and bands are bit-identical.
+//
+// Data in HBM: z^0 = the caller's fp32 input; for l >= 1, z^l is kept in
+// fp64 (selector and decimation chain, l <= L-2) and fp32 (stage input); u^l fp32; s^l uint8.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/blade_ms.h"
+#include "k_down.cuh"
+#include "k_stage_tma.cuh"
 #include "kernels.cuh"
 
 using namespace blade;
@@ -58,48 +68,107 @@ struct DeviceGuard {
   }
 };
 
+// ------------------------------------------------------------------------------ kernel tables
 using StageKernel = void (*)(StageArgs);
-using SelKernel = void (*)(LevelView, uint8_t*, int, int, int, int, SelParams);
-
 struct StageVariant {
   int nf, nc, rs, by;
   StageKernel fn;
-  int tile_floats;
-  int threads;
-  int trows, tcols;
+  int tile_floats, threads, trows, tcols;
 };
-
 template <int NF, int NC, int RS, int BY>
 StageVariant make_variant() {
   using SS = StageShape<NF, NC, RS, BY>;
   return StageVariant{NF, NC, RS, BY, &k_stage<NF, NC, RS, BY>, SS::tile_floats, SS::threads,
                       SS::TROWS, SS::TCOLS};
 }
-
-// The instantiated stage kernels (which footprints are built).
-std::vector<StageVariant> stage_variants() {
-  return {
-      // fixed-scale (Eq. 1), all phases in one CTA (n_phases must be 1 when L == 1)
+// Generic stage kernels (any shape; row-parity CTAs for the big pair banks).
+const std::vector<StageVariant>& stage_variants() {
+  static const std::vector<StageVariant> v = {
       make_variant<3, 0, 1, 8>(), make_variant<5, 0, 1, 8>(), make_variant<7, 0, 1, 8>(),
-      make_variant<9, 0, 1, 8>(),
-      // multiscale pairs, CTAs specialised by output-row parity
-      make_variant<3, 3, 2, 8>(), make_variant<5, 5, 2, 8>(), make_variant<7, 7, 2, 8>(),
-      make_variant<7, 7, 2, 4>(), make_variant<9, 9, 2, 8>(), make_variant<9, 9, 2, 4>(),
-      make_variant<9, 9, 2, 2>(), make_variant<7, 5, 2, 8>(), make_variant<7, 5, 2, 4>(),
-      make_variant<5, 3, 2, 8>(), make_variant<9, 7, 2, 4>(), make_variant<9, 7, 2, 2>(),
+      make_variant<9, 0, 1, 8>(), make_variant<3, 3, 2, 8>(), make_variant<5, 5, 2, 8>(),
+      make_variant<7, 7, 2, 8>(), make_variant<7, 7, 2, 4>(), make_variant<9, 9, 2, 8>(),
+      make_variant<9, 9, 2, 4>(), make_variant<9, 9, 2, 2>(), make_variant<7, 5, 2, 8>(),
+      make_variant<7, 5, 2, 4>(), make_variant<5, 3, 2, 8>(), make_variant<9, 7, 2, 4>(),
+      make_variant<9, 7, 2, 2>(),
   };
+  return v;
 }
 
-SelKernel selector_kernel(int ws) {
-  switch (ws) {
-    case 1: return &k_selector<1>;
-    case 3: return &k_selector<3>;
-    case 5: return &k_selector<5>;
-    case 7: return &k_selector<7>;
-    default: return nullptr;
+using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
+struct TmaVariant {
+  int nf, nc;
+  TmaKernel fn;
+  int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc;
+};
+template <int NF, int NC>
+TmaVariant make_tma() {
+  using SS = TmaShape<NF, NC>;
+  return TmaVariant{NF, NC, &k_stage_tma<NF, NC>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC};
+}
+// TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
+const std::vector<TmaVariant>& tma_variants() {
+  static const std::vector<TmaVariant> v = {
+      make_tma<3, 0>(), make_tma<5, 0>(), make_tma<7, 0>(), make_tma<9, 0>(),
+      make_tma<3, 3>(), make_tma<5, 5>(), make_tma<5, 3>(),
+  };
+  return v;
+}
+
+using DownKernelF = decltype(&k_down<float, 5, true>);
+using DownKernelD = decltype(&k_down<double, 5, true>);
+DownKernelF down_kernel_f(int ws, bool dec) {
+  switch (ws * 2 + (dec ? 1 : 0)) {
+    case 2: return &k_down<float, 1, false>;
+    case 3: return &k_down<float, 1, true>;
+    case 6: return &k_down<float, 3, false>;
+    case 7: return &k_down<float, 3, true>;
+    case 10: return &k_down<float, 5, false>;
+    case 11: return &k_down<float, 5, true>;
   }
+  return nullptr;
+}
+DownKernelD down_kernel_d(int ws) {
+  switch (ws) {
+    case 1: return &k_down<double, 1, true>;
+    case 3: return &k_down<double, 3, true>;
+    case 5: return &k_down<double, 5, true>;
+  }
+  return nullptr;
 }
 
+// ------------------------------------------------------------------------------ TMA encode
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    else
+      cudaGetLastError();
+  });
+  return g_encode;
+}
+
+// 3D tiled map over a [depth][rows][W] array of `esize`-byte elements.
+bool encode_3d(CUtensorMap* tm, const void* base, CUtensorMapDataType dt, int esize, int W, int rows,
+               int depth, int bw, int bh, int bd) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)depth};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * esize, (cuuint64_t)W * esize * rows};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bd};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(tm, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ------------------------------------------------------------------------------ row ranges
 struct Range {
   int lo = 0, hi = 0;  // [lo, hi)
   int n() const { return hi - lo; }
@@ -114,13 +183,11 @@ int fold_host(long long i, long long n) {
 // Hull of {fold(i, n) : lo <= i < hi}.
 Range fold_hull(long long lo, long long hi, int n) {
   if (hi <= lo) return Range{0, 0};
-  if (hi - lo >= 2LL * n || (lo >= 0 && hi <= n)) {
-    if (hi - lo >= 2LL * n) return Range{0, n};
-    return Range{(int)lo, (int)hi};
-  }
+  if (hi - lo >= 2LL * n) return Range{0, n};
+  if (lo >= 0 && hi <= n) return Range{(int)lo, (int)hi};
   int mn = n, mx = -1;
   for (long long i = lo; i < hi; ++i) {
-    int f = fold_host(i, n);
+    const int f = fold_host(i, n);
     mn = std::min(mn, f);
     mx = std::max(mx, f);
   }
@@ -133,26 +200,31 @@ Range hull(Range a, Range b) {
   return Range{std::min(a.lo, b.lo), std::max(a.hi, b.hi)};
 }
 
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
 }  // namespace
 
 struct blade_ms {
   blade_ms_config cfg;
   int n_o, n_s, n_c, K;
   int n_stages, nt, S, PS;
-  int device;
-  int num_sms;
+  int device, num_sms;
   float* d_bank = nullptr;  // [stage][phase][PS]
   size_t bank_bytes = 0;
-  std::vector<SelParams> sel;  // per stage
+  std::vector<DownParams> down;  // per stage (selector level)
+  // generic stage kernel
   StageVariant stage{};
   size_t stage_smem = 0;
   int stage_ctas_per_sm = 0;
-  SelKernel sel_fn = nullptr;
+  // TMA stage kernel (if the shape has one and the bank fits)
+  bool has_tma = false;
+  TmaVariant tma{};
+  size_t tma_smem = 0;
   // profiling (blade_ms_set_profiling): event pairs around each launch
   struct ProfRec { int kind, level; cudaEvent_t e0, e1; };
   bool profiling = false;
-  std::vector<ProfRec> prof;        // recorded, not yet read
-  std::vector<cudaEvent_t> ev_pool;  // free events
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
 };
 
 namespace {
@@ -160,13 +232,11 @@ namespace {
 struct Plan {
   int L = 0, N = 0;
   std::vector<int> H, W;
-  std::vector<Range> z;    // rows of z^l materialised (level 0: the input buffer's rows)
-  std::vector<Range> u;    // rows of u^l computed (stage output = map rows), l <= L-2 (or 0 if L==1)
+  std::vector<Range> z;  // rows of z^l materialised (level 0: needed input rows)
+  std::vector<Range> u;  // rows of u^l computed (= map rows), l <= L-2 (l = 0 if L == 1)
   size_t ws_bytes = 0;
-  std::vector<size_t> z_off, u_off, map_off;
+  std::vector<size_t> z32_off, z64_off, u_off, map_off;
 };
-
-inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Dependency cone of output rows [o0, o0+on) of the final output.
 void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) {
@@ -203,14 +273,18 @@ void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) 
       p.z[l - 1] = hull(p.z[l - 1], fold_hull(dlo, dhi, p.H[l - 1]));
     }
   }
-  // workspace: z^l (l >= 1), u^l (1 <= l <= L-2), maps (selector levels)
   size_t off = 0;
-  p.z_off.assign(L, 0);
+  p.z32_off.assign(L, 0);
+  p.z64_off.assign(L, 0);
   p.u_off.assign(L, 0);
   p.map_off.assign(L, 0);
   for (int l = 1; l < L; ++l) {
-    p.z_off[l] = off;
+    p.z32_off[l] = off;
     off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
+  }
+  for (int l = 1; l + 1 < L; ++l) {
+    p.z64_off[l] = off;
+    off = align256(off + sizeof(double) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
   }
   for (int l = 1; l + 1 < L; ++l) {
     p.u_off[l] = off;
@@ -286,54 +360,149 @@ struct ProfScope {
   }
 };
 
-// Enqueue the whole cascade for plan p. in0: level-0 input buffer (rows p.z[0] ... or wider,
-// described by in_view); out_view: final output rows p.u[0].
-blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view,
-                     char* ws, cudaStream_t st, bool run_stages,
-                     uint8_t* const* maps_out, float* const* levels_out) {
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// BLADE_SYNC_DEBUG=1: synchronise after every launch and name the kernel that failed.
+bool sync_debug() {
+  static const bool on = [] {
+    const char* e = getenv("BLADE_SYNC_DEBUG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+#define LAUNCH_CHECK(name)                                                                       \
+  do {                                                                                           \
+    cudaError_t e__ = cudaGetLastError();                                                        \
+    if (e__ == cudaSuccess && sync_debug()) e__ = cudaStreamSynchronize(st);                     \
+    if (e__ != cudaSuccess)                                                                      \
+      return fail(BLADE_ECUDA, "%s (level %d): %s", name, l, cudaGetErrorString(e__));           \
+  } while (0)
+
+// Enqueue the cascade for plan p. in_view: level-0 input (fp32, rows >= p.z[0]); out_view: final
+// output rows p.u[0]. levels_out (diagnostic) receives z^l (fp32) for l >= 1; maps_out the maps.
+blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view, char* ws,
+                     cudaStream_t st, bool run_stages, uint8_t* const* maps_out,
+                     float* const* levels_out) {
   const int L = p.L, N = p.N;
   if (N == 0) return BLADE_OK;
-  std::vector<LevelView> zv(L);
-  zv[0] = in_view;
+  std::vector<LevelView> z32(L);
+  std::vector<double*> z64(L, nullptr);
+  z32[0] = in_view;
   for (int l = 1; l < L; ++l) {
     float* base = (levels_out && levels_out[l - 1]) ? levels_out[l - 1]
-                                                    : reinterpret_cast<float*>(ws + p.z_off[l]);
-    zv[l] = make_view(base, p.H[l], p.W[l], p.z[l]);
+                                                    : reinterpret_cast<float*>(ws + p.z32_off[l]);
+    z32[l] = make_view(base, p.H[l], p.W[l], p.z[l]);
+    if (l + 1 < L) z64[l] = reinterpret_cast<double*>(ws + p.z64_off[l]);
   }
-  // ---- down pass (K1)
-  for (int l = 0; l + 1 < L; ++l) {
-    const Range r = p.z[l + 1];
-    if (r.n() <= 0) continue;
-    dim3 grid((p.W[l + 1] + dec::TX - 1) / dec::TX, (r.n() + dec::TY - 1) / dec::TY, N);
-    ProfScope ps(h, st, 0, l);
-    k_decimate<<<grid, dim3(32, 8), 0, st>>>(zv[l], zv[l + 1], r.lo, r.n());
-    CUDA_TRY(cudaGetLastError());
-  }
-  if (levels_out && !run_stages && !maps_out) return BLADE_OK;
   const int nsel = L == 1 ? 1 : L - 1;
+  std::vector<uint8_t*> maps(nsel);
+  for (int l = 0; l < nsel; ++l)
+    maps[l] = (maps_out && maps_out[l]) ? maps_out[l] : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
+
+  // ---- down pass: k_down(l) -> s^l, z^{l+1}
+  for (int l = 0; l < nsel; ++l) {
+    const Range U = p.u[l];
+    const bool dec = L > 1;
+    Range Z1 = dec ? p.z[l + 1] : Range{0, 0};
+    Range R = U;
+    if (dec) R = hull(R, Range{2 * Z1.lo, 2 * Z1.hi});
+    const int base = R.lo & ~1;
+    dim3 grid((p.W[l] + down::TX - 1) / down::TX, (R.hi - base + down::TY - 1) / down::TY, N);
+    const int H1 = dec ? p.H[l + 1] : 0, W1 = dec ? p.W[l + 1] : 0;
+    double* o64 = (dec && l + 1 < L - 1) ? z64[l + 1] : nullptr;
+    float* o32 = dec ? z32[l + 1].p : nullptr;
+    ProfScope ps(h, st, 1, l);
+    if (l == 0) {
+      auto fn = down_kernel_f(h->cfg.window_size, dec);
+      fn<<<grid, dim3(32, 8), sizeof(DownSmem), st>>>(
+          in_view.p, p.H[0], p.W[0], in_view.row0, in_view.rows, in_view.plane, in_view.frame, base,
+          maps[0], U.lo, U.n(), o64, o32, H1, W1, Z1.lo, Z1.n(), Z1.lo, Z1.n(), h->down[0]);
+    } else {
+      auto fn = down_kernel_d(h->cfg.window_size);
+      const long long plane = (long long)p.z[l].n() * p.W[l];
+      fn<<<grid, dim3(32, 8), sizeof(DownSmem), st>>>(
+          z64[l], p.H[l], p.W[l], p.z[l].lo, p.z[l].n(), plane, 3 * plane, base, maps[l], U.lo, U.n(),
+          o64, o32, H1, W1, Z1.lo, Z1.n(), Z1.lo, Z1.n(), h->down[l]);
+    }
+    LAUNCH_CHECK("k_down");
+  }
+  if (!run_stages) return BLADE_OK;
+
+  // ---- up pass: stage(l)
   for (int l = nsel - 1; l >= 0; --l) {
     const Range r = p.u[l];
-    uint8_t* map = (maps_out && maps_out[l]) ? maps_out[l] : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
-    {
-      dim3 grid((p.W[l] + sel::TX - 1) / sel::TX, (r.n() + sel::TY - 1) / sel::TY, N);
-      ProfScope ps(h, st, 1, l);
-      h->sel_fn<<<grid, dim3(32, 8), 0, st>>>(zv[l], map, r.lo, r.n(), r.lo, r.n(), h->sel[l]);
-      CUDA_TRY(cudaGetLastError());
+    LevelView zl = z32[l];
+    LevelView u1{};
+    if (L > 1)
+      u1 = (l + 1 == L - 1) ? z32[L - 1]
+                            : make_view(reinterpret_cast<float*>(ws + p.u_off[l + 1]), p.H[l + 1], p.W[l + 1],
+                                        p.u[l + 1]);
+    LevelView outv = (l == 0) ? out_view
+                              : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r);
+    const float* bank = h->d_bank + (size_t)l * h->cfg.n_phases * h->PS;
+    const int y_base = r.lo & ~1;
+    const int clamp = (l == 0 && h->cfg.clamp_output) ? 1 : 0;
+    ProfScope ps(h, st, 2, l);
+    // TMA path: needs 16-B aligned buffers whose row pitches are 16-B multiples
+    bool use_tma = h->has_tma && p.W[l] % 16 == 0 && aligned16(zl.p) && aligned16(outv.p) &&
+                   aligned16(maps[l]) && (L == 1 || (p.W[l + 1] % 4 == 0 && aligned16(u1.p)));
+    CUtensorMap tmz, tmu, tmm;
+    if (use_tma) {
+      const TmaVariant& tv = h->tma;
+      use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb, tv.fr, 3) &&
+                encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.W[l], r.n(), N, tv.tcols, tv.trows, 1);
+      if (use_tma) {
+        if (L > 1)
+          use_tma = encode_3d(&tmu, u1.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l + 1], u1.rows, N * 3, tv.ccb,
+                              tv.cr, 3);
+        else
+          tmu = tmz;
+      }
     }
-    if (!run_stages) continue;
+    if (use_tma) {
+      const TmaVariant& tv = h->tma;
+      StageTmaArgs a{};
+      a.H = p.H[l];
+      a.W = p.W[l];
+      a.H1 = L > 1 ? p.H[l + 1] : 1;
+      a.W1 = L > 1 ? p.W[l + 1] : 1;
+      a.z_row0 = zl.row0;
+      a.z_rows = zl.rows;
+      a.u_row0 = u1.row0;
+      a.u_rows = u1.rows;
+      a.map_row0 = r.lo;
+      a.map_rows = r.n();
+      a.z = zl.p;
+      a.u1 = u1.p;
+      a.out = outv.p;
+      a.out_row0 = outv.row0;
+      a.out_rows = outv.rows;
+      a.bank = bank;
+      a.K = h->K;
+      a.S = h->S;
+      a.PS = h->PS;
+      a.n_phases = h->cfg.n_phases;
+      a.N = N;
+      a.y_base = y_base;
+      a.o_r0 = r.lo;
+      a.o_rn = r.n();
+      a.tiles_x = (p.W[l] + tv.tcols - 1) / tv.tcols;
+      a.tiles_y = (r.hi - y_base + tv.trows - 1) / tv.trows;
+      a.n_tiles = N * a.tiles_x * a.tiles_y;
+      a.clamp = clamp;
+      const int grid = std::min(h->num_sms, a.n_tiles);
+      tv.fn<<<grid, dim3(32, 8), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+      LAUNCH_CHECK("k_stage_tma");
+      continue;
+    }
     StageArgs a{};
-    a.z = zv[l];
-    if (L > 1) {
-      a.u1 = (l + 1 == L - 1) ? zv[L - 1]
-                              : make_view(reinterpret_cast<float*>(ws + p.u_off[l + 1]), p.H[l + 1],
-                                          p.W[l + 1], p.u[l + 1]);
-    }
-    a.out = (l == 0) ? out_view
-                     : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r);
-    a.map = map;
+    a.z = zl;
+    a.u1 = u1;
+    a.out = outv;
+    a.map = maps[l];
     a.map_row0 = r.lo;
     a.map_rows = r.n();
-    a.bank = h->d_bank + (size_t)l * h->cfg.n_phases * h->PS;
+    a.bank = bank;
     a.K = h->K;
     a.S = h->S;
     a.PS = h->PS;
@@ -341,18 +510,15 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     a.N = N;
     a.out_r0 = r.lo;
     a.out_rn = r.n();
-    const int y_base = r.lo & ~1;
     a.tiles_x = (p.W[l] + h->stage.tcols - 1) / h->stage.tcols;
     a.tiles_y = (r.hi - y_base + h->stage.trows - 1) / h->stage.trows;
     a.n_tiles = N * a.tiles_x * a.tiles_y;
-    a.clamp = (l == 0 && h->cfg.clamp_output) ? 1 : 0;
+    a.clamp = clamp;
     long long grid = (long long)h->stage_ctas_per_sm * h->num_sms;
-    const long long need = (long long)a.n_tiles * h->stage.rs;
-    grid = std::min(grid, need);
+    grid = std::min(grid, (long long)a.n_tiles * h->stage.rs);
     if (h->stage.rs == 2) grid = std::max<long long>(2, grid & ~1LL);
-    ProfScope ps(h, st, 2, l);
     h->stage.fn<<<(unsigned)grid, dim3(32, h->stage.by), h->stage_smem, st>>>(a);
-    CUDA_TRY(cudaGetLastError());
+    LAUNCH_CHECK("k_stage");
   }
   return BLADE_OK;
 }
@@ -379,8 +545,8 @@ const char* blade_ms_status_string(blade_status s) {
 
 const char* blade_ms_last_error(void) { return g_last_error.c_str(); }
 
-blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layout* bl,
-                             const float* taps, size_t n_taps, int device, blade_ms_t* out) {
+blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layout* bl, const float* taps,
+                             size_t n_taps, int device, blade_ms_t* out) {
   g_last_error.clear();
   if (!out) return fail(BLADE_EINVAL, "out is NULL");
   *out = nullptr;
@@ -398,15 +564,15 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     return fail(BLADE_EINVAL, "n_filter_channels must be 1 or 3");
   if (c.n_filter_channels == 3)
     return fail(BLADE_EUNSUPPORTED, "per-channel (YCbCr) banks are not built (SURVEY.md §8 f1)");
-  if (c.window_size < 1 || c.window_size > 7 || !(c.window_size & 1))
-    return fail(BLADE_EINVAL, "window_size must be odd in 1..7");
+  if (c.window_size < 1 || c.window_size > 5 || !(c.window_size & 1))
+    return fail(BLADE_EINVAL, "window_size must be 1, 3 or 5");
   if (!(c.window_sigma > 0.0f) || !std::isfinite(c.window_sigma))
     return fail(BLADE_EINVAL, "window_sigma must be finite and > 0");
   if (c.clamp_output != 0 && c.clamp_output != 1) return fail(BLADE_EINVAL, "clamp_output must be 0 or 1");
   if (bl->n_orient < 1 || bl->n_strength < 1 || bl->n_coherence < 1)
     return fail(BLADE_EINVAL, "bucket counts must be >= 1");
-  if (bl->n_strength - 1 > kMaxThr || bl->n_coherence - 1 > kMaxThr)
-    return fail(BLADE_EUNSUPPORTED, "at most %d thresholds per feature", kMaxThr);
+  if (bl->n_strength - 1 > kMaxThr2 || bl->n_coherence - 1 > kMaxThr2)
+    return fail(BLADE_EUNSUPPORTED, "at most %d thresholds per feature", kMaxThr2);
   const long long K = (long long)bl->n_orient * bl->n_strength * bl->n_coherence;
   if (K > 256) return fail(BLADE_EUNSUPPORTED, "K = %lld > 256 needs uint16 maps (SURVEY.md §8 f2)", K);
   if ((bl->n_strength > 1 && !bl->strength_thresholds) || (bl->n_coherence > 1 && !bl->coherence_thresholds))
@@ -444,18 +610,19 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   DeviceGuard guard(device);
   if (!guard.ok) return fail(BLADE_EDEVICE, "cudaSetDevice(%d) failed", device);
 
-  // ---- pick the stage kernel variant: largest BY whose shared memory fits
   int max_smem = 0, nsm = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-  const int S = nt | 1;                   // odd tap stride (bank-conflict spread)
+  const int S = nt | 1;                      // odd tap stride (bank-conflict spread)
   const int PS = (int)((K * S + 3) & ~3LL);  // phase stride, 16-B aligned
+  const int cnc = c.levels > 1 ? c.coarse_size : 0;
+
+  // generic stage kernel: largest BY whose shared memory fits
   const int want_rs = c.levels == 1 ? 1 : 2;
   const StageVariant* best = nullptr;
   size_t best_smem = 0;
-  static const std::vector<StageVariant> variants = stage_variants();
-  for (const auto& v : variants) {
-    if (v.nf != c.fine_size || v.nc != (c.levels > 1 ? c.coarse_size : 0) || v.rs != want_rs) continue;
+  for (const auto& v : stage_variants()) {
+    if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs) continue;
     const int nph_cta = c.n_phases == 4 ? (v.rs == 2 ? 2 : 4) : 1;
     const size_t smem = sizeof(float) * ((((size_t)nph_cta * PS) + 3) / 4 * 4 + (size_t)v.tile_floats);
     if (smem > (size_t)max_smem) continue;
@@ -465,8 +632,10 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     }
   }
   if (!best)
-    return fail(BLADE_EUNSUPPORTED, "no stage kernel for fine %d / coarse %d with K = %lld (built: 3/5/7/9 "
-                "single-level; 3+3, 5+5, 7+7, 9+9, 7+5, 5+3, 9+7 pairs)", c.fine_size, c.coarse_size, K);
+    return fail(BLADE_EUNSUPPORTED,
+                "no stage kernel for fine %d / coarse %d with K = %lld (built: 3/5/7/9 single-level; 3+3, 5+5, "
+                "7+7, 9+9, 7+5, 5+3, 9+7 pairs)",
+                c.fine_size, c.coarse_size, K);
 
   blade_ms* h = new blade_ms();
   h->cfg = c;
@@ -482,32 +651,45 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->num_sms = nsm;
   h->stage = *best;
   h->stage_smem = best_smem;
-  h->sel_fn = selector_kernel(c.window_size);
+  for (const auto& v : tma_variants()) {
+    if (v.nf != c.fine_size || v.nc != cnc) continue;
+    const size_t bank = ((size_t)c.n_phases * PS * 4 + 127) & ~size_t(127);
+    const size_t smem = 2 * (size_t)v.stage_bytes + bank + 16;
+    if (smem <= (size_t)max_smem && get_encode()) {
+      h->has_tma = true;
+      h->tma = v;
+      h->tma_smem = smem;
+    }
+  }
 
-  // ---- selector parameters per stage: window weights (fp64 -> fp32), thresholds rounded up
+  // ---- selector parameters per stage (window weights fp64 -> fp32; thresholds pre-transformed)
   const int r = c.window_size / 2;
   double e[8], se = 0.0;
   for (int d = -r; d <= r; ++d) {
     e[d + r] = std::exp(-(double)(d * d) / (2.0 * (double)c.window_sigma * (double)c.window_sigma));
     se += e[d + r];
   }
-  auto round_up_f32 = [](double v) {
-    float f = (float)v;
-    if ((double)f < v) f = std::nextafter(f, INFINITY);
-    return f;
-  };
-  h->sel.resize(n_stages);
+  h->down.resize(n_stages);
   for (int s = 0; s < n_stages; ++s) {
-    SelParams& sp = h->sel[s];
-    memset(&sp, 0, sizeof sp);
-    for (int d = 0; d < c.window_size; ++d) sp.w[d] = (float)(e[d] / se);
-    sp.n_o = bl->n_orient;
-    sp.n_s = bl->n_strength;
-    sp.n_c = bl->n_coherence;
-    for (int i = 0; i < bl->n_strength - 1; ++i)
-      sp.ts[i] = round_up_f32(bl->strength_thresholds[(size_t)s * (bl->n_strength - 1) + i]);
-    for (int i = 0; i < bl->n_coherence - 1; ++i)
-      sp.tc[i] = round_up_f32(bl->coherence_thresholds[(size_t)s * (bl->n_coherence - 1) + i]);
+    DownParams& dp = h->down[s];
+    memset(&dp, 0, sizeof dp);
+    for (int d = 0; d < c.window_size; ++d) {
+      dp.w64[d] = e[d] / se;
+      dp.w32[d] = (float)(e[d] / se);
+    }
+    dp.n_o = bl->n_orient;
+    dp.n_s = bl->n_strength;
+    dp.n_c = bl->n_coherence;
+    for (int i = 0; i < bl->n_strength - 1; ++i) {
+      const double t = bl->strength_thresholds[(size_t)s * (bl->n_strength - 1) + i];
+      dp.ts2[i] = t <= 0.0 ? -INFINITY : (float)(t * t);  // S >= t <=> l1 >= t^2 (t > 0)
+    }
+    for (int i = 0; i < bl->n_coherence - 1; ++i) {
+      const double t = bl->coherence_thresholds[(size_t)s * (bl->n_coherence - 1) + i];
+      dp.tcA[i] = (float)(1.0 + t * t);
+      dp.tcB[i] = (float)(2.0 * t);
+      dp.tc_nonpos += t <= 0.0;
+    }
   }
 
   // ---- bank re-layout: host [stage][ch=1][phase][K][nt] -> device [stage][phase][PS]
@@ -529,13 +711,24 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   cudaError_t ce = cudaMemcpy(h->d_bank, relaid.data(), h->bank_bytes, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess)
     ce = cudaFuncSetAttribute(h->stage.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->stage_smem);
+  if (ce == cudaSuccess && h->has_tma)
+    ce = cudaFuncSetAttribute(h->tma.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
+  if (ce == cudaSuccess) {
+    for (int ws = 1; ws <= 5 && ce == cudaSuccess; ws += 2) {
+      ce = cudaFuncSetAttribute(down_kernel_f(ws, true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem));
+      if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(down_kernel_f(ws, false), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem));
+      if (ce == cudaSuccess)
+        ce = cudaFuncSetAttribute(down_kernel_d(ws), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem));
+    }
+  }
   int occ = 0;
   if (ce == cudaSuccess)
     ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->stage.fn, h->stage.threads, h->stage_smem);
   if (ce != cudaSuccess || occ < 1) {
     cudaFree(h->d_bank);
     delete h;
-    return fail(BLADE_ECUDA, "stage kernel setup failed: %s (occupancy %d)", cudaGetErrorString(ce), occ);
+    return fail(BLADE_ECUDA, "kernel setup failed: %s (occupancy %d)", cudaGetErrorString(ce), occ);
   }
   h->stage_ctas_per_sm = occ;
   *out = h;
@@ -594,15 +787,14 @@ blade_status blade_ms_get_info(blade_ms_t h, blade_ms_info* info) {
   info->K = h->K;
   info->device = h->device;
   info->bank_bytes_device = h->bank_bytes;
-  info->stage_smem_bytes = h->stage_smem;
-  info->stage_phase_groups = h->stage.rs;
+  info->stage_smem_bytes = h->has_tma ? h->tma_smem : h->stage_smem;
+  info->stage_phase_groups = h->has_tma ? 1 : h->stage.rs;
   return BLADE_OK;
 }
 
 static blade_status check_dims(int32_t N, int32_t H, int32_t W) {
   if (N < 0 || H < 1 || W < 1) return fail(BLADE_EINVAL, "need N >= 0, H >= 1, W >= 1 (got %d, %d, %d)", N, H, W);
-  if ((long long)H * W * 3 > (1LL << 31) - 1)
-    return fail(BLADE_EINVAL, "a frame of %d x %d exceeds 2^31 samples", H, W);
+  if ((long long)H * W * 3 > (1LL << 31) - 1) return fail(BLADE_EINVAL, "a frame of %d x %d exceeds 2^31 samples", H, W);
   if (N > 65535) return fail(BLADE_EINVAL, "N > 65535 frames per call");
   return BLADE_OK;
 }
@@ -622,29 +814,27 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
   (void)H;
   (void)W;
   const int L = h->cfg.levels;
-  *count = N == 0 ? 0 : (L - 1) + 2 * (L == 1 ? 1 : L - 1);
+  *count = N == 0 ? 0 : 2 * (L == 1 ? 1 : L - 1);
   return BLADE_OK;
 }
 
-static blade_status common_checks(blade_ms_t h, const void* in, const void* out, int32_t N, int32_t H,
-                                  int32_t W, void* ws, size_t ws_bytes, const Plan& p) {
+static blade_status common_checks(blade_ms_t h, const void* in, int32_t N, void* ws, size_t ws_bytes,
+                                  const Plan& p) {
   if (!h) return fail(BLADE_EINVAL, "handle is NULL");
   if (N > 0 && !in) return fail(BLADE_EINVAL, "in is NULL");
   if (N > 0 && !ws && p.ws_bytes > 0) return fail(BLADE_EINVAL, "workspace is NULL");
   if (ws_bytes < p.ws_bytes) return fail(BLADE_ESHAPE, "workspace %zu bytes < required %zu", ws_bytes, p.ws_bytes);
-  (void)out;
-  (void)H;
-  (void)W;
   blade_status s;
   if (N > 0) {
     if ((s = check_dev_ptr(h, in, "in")) != BLADE_OK) return s;
     if ((s = check_dev_ptr(h, ws, "workspace")) != BLADE_OK) return s;
+    if (!aligned16(ws)) return fail(BLADE_EINVAL, "workspace must be 16-byte aligned");
   }
   return BLADE_OK;
 }
 
-blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t N, int32_t H,
-                              int32_t W, void* ws, size_t ws_bytes, void* stream) {
+blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t N, int32_t H, int32_t W, void* ws,
+                              size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (!h) return fail(BLADE_EINVAL, "handle is NULL");
   blade_status s = check_dims(N, H, W);
@@ -652,7 +842,7 @@ blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t
   if (N == 0) return BLADE_OK;
   Plan p;
   plan_rows(h, N, H, W, 0, H, p);
-  if ((s = common_checks(h, in, out, N, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  if ((s = common_checks(h, in, N, ws, ws_bytes, p)) != BLADE_OK) return s;
   if (!out) return fail(BLADE_EINVAL, "out is NULL");
   if ((s = check_dev_ptr(h, out, "out")) != BLADE_OK) return s;
   const size_t img = sizeof(float) * (size_t)N * 3 * H * W;
@@ -665,8 +855,8 @@ blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t
   return enqueue(h, p, inv, outv, (char*)ws, (cudaStream_t)stream, true, nullptr, nullptr);
 }
 
-blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W,
-                               uint8_t* const* maps, void* ws, size_t ws_bytes, void* stream) {
+blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W, uint8_t* const* maps,
+                               void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (!h) return fail(BLADE_EINVAL, "handle is NULL");
   blade_status s = check_dims(N, H, W);
@@ -675,7 +865,7 @@ blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t
   if (N == 0) return BLADE_OK;
   Plan p;
   plan_rows(h, N, H, W, 0, H, p);
-  if ((s = common_checks(h, in, nullptr, N, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  if ((s = common_checks(h, in, N, ws, ws_bytes, p)) != BLADE_OK) return s;
   for (int l = 0; l < h->n_stages; ++l)
     if (maps[l] && (s = check_dev_ptr(h, maps[l], "maps_per_level[l]")) != BLADE_OK) return s;
   DeviceGuard guard(h->device);
@@ -683,8 +873,8 @@ blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t
   return enqueue(h, p, inv, LevelView{}, (char*)ws, (cudaStream_t)stream, false, maps, nullptr);
 }
 
-blade_status blade_ms_pyramid(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W,
-                              float* const* levels, void* ws, size_t ws_bytes, void* stream) {
+blade_status blade_ms_pyramid(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W, float* const* levels,
+                              void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (!h) return fail(BLADE_EINVAL, "handle is NULL");
   blade_status s = check_dims(N, H, W);
@@ -693,7 +883,7 @@ blade_status blade_ms_pyramid(blade_ms_t h, const float* in, int32_t N, int32_t 
   if (N == 0) return BLADE_OK;
   Plan p;
   plan_rows(h, N, H, W, 0, H, p);
-  if ((s = common_checks(h, in, nullptr, N, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  if ((s = common_checks(h, in, N, ws, ws_bytes, p)) != BLADE_OK) return s;
   for (int l = 1; l < h->cfg.levels; ++l) {
     if (!levels[l - 1]) return fail(BLADE_EINVAL, "levels[%d] is NULL", l - 1);
     if ((s = check_dev_ptr(h, levels[l - 1], "levels[l]")) != BLADE_OK) return s;
@@ -703,8 +893,8 @@ blade_status blade_ms_pyramid(blade_ms_t h, const float* in, int32_t N, int32_t 
   return enqueue(h, p, inv, LevelView{}, (char*)ws, (cudaStream_t)stream, false, nullptr, levels);
 }
 
-blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32_t out_rows,
-                                int32_t* in_row0, int32_t* in_rows) {
+blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32_t out_rows, int32_t* in_row0,
+                                int32_t* in_rows) {
   if (!h || !in_row0 || !in_rows) return fail(BLADE_EINVAL, "NULL argument");
   if (H < 1 || out_row0 < 0 || out_rows < 1 || out_row0 + out_rows > H)
     return fail(BLADE_EINVAL, "bad band [%d, %d) of H = %d", out_row0, out_row0 + out_rows, H);
@@ -715,11 +905,10 @@ blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32
   return BLADE_OK;
 }
 
-blade_status blade_ms_band_workspace_size(blade_ms_t h, int32_t H, int32_t W, int32_t out_row0,
-                                          int32_t out_rows, size_t* bytes) {
+blade_status blade_ms_band_workspace_size(blade_ms_t h, int32_t H, int32_t W, int32_t out_row0, int32_t out_rows,
+                                          size_t* bytes) {
   if (!h || !bytes) return fail(BLADE_EINVAL, "NULL argument");
-  if (H < 1 || W < 1 || out_row0 < 0 || out_rows < 1 || out_row0 + out_rows > H)
-    return fail(BLADE_EINVAL, "bad band");
+  if (H < 1 || W < 1 || out_row0 < 0 || out_rows < 1 || out_row0 + out_rows > H) return fail(BLADE_EINVAL, "bad band");
   Plan p;
   plan_rows(h, 1, H, W, out_row0, out_rows, p);
   *bytes = p.ws_bytes;
@@ -727,8 +916,8 @@ blade_status blade_ms_band_workspace_size(blade_ms_t h, int32_t H, int32_t W, in
 }
 
 blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t in_row0, int32_t in_rows,
-                                   float* out_band, int32_t out_row0, int32_t out_rows, int32_t H,
-                                   int32_t W, void* ws, size_t ws_bytes, void* stream) {
+                                   float* out_band, int32_t out_row0, int32_t out_rows, int32_t H, int32_t W,
+                                   void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (!h) return fail(BLADE_EINVAL, "handle is NULL");
   blade_status s = check_dims(1, H, W);
@@ -741,10 +930,9 @@ blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t i
   if (in_row0 < 0 || in_rows < 1 || in_row0 > p.z[0].lo || in_row0 + in_rows < p.z[0].hi || in_row0 + in_rows > H)
     return fail(BLADE_ESHAPE, "input band [%d, %d) does not cover the needed rows [%d, %d)", in_row0,
                 in_row0 + in_rows, p.z[0].lo, p.z[0].hi);
-  if ((s = common_checks(h, in_band, out_band, 1, H, W, ws, ws_bytes, p)) != BLADE_OK) return s;
+  if ((s = common_checks(h, in_band, 1, ws, ws_bytes, p)) != BLADE_OK) return s;
   if ((s = check_dev_ptr(h, out_band, "out_band")) != BLADE_OK) return s;
-  if (ranges_overlap(in_band, sizeof(float) * 3 * (size_t)in_rows * W, out_band,
-                     sizeof(float) * 3 * (size_t)out_rows * W))
+  if (ranges_overlap(in_band, sizeof(float) * 3 * (size_t)in_rows * W, out_band, sizeof(float) * 3 * (size_t)out_rows * W))
     return fail(BLADE_EINVAL, "out_band overlaps in_band");
   DeviceGuard guard(h->device);
   LevelView inv = make_view(const_cast<float*>(in_band), H, W, Range{in_row0, in_row0 + in_rows});
@@ -752,9 +940,8 @@ blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t i
   return enqueue(h, p, inv, outv, (char*)ws, (cudaStream_t)stream, true, nullptr, nullptr);
 }
 
-blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* out_host, int32_t N,
-                                   int32_t H, int32_t W, float* d_in, float* d_out, void* ws,
-                                   size_t ws_bytes, void* stream) {
+blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* out_host, int32_t N, int32_t H,
+                                   int32_t W, float* d_in, float* d_out, void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (!h) return fail(BLADE_EINVAL, "handle is NULL");
   blade_status s = check_dims(N, H, W);
@@ -763,7 +950,7 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
   if (!in_host || !out_host || !d_in || !d_out) return fail(BLADE_EINVAL, "NULL buffer");
   Plan pfull;
   plan_rows(h, N, H, W, 0, H, pfull);
-  if ((s = common_checks(h, d_in, d_out, N, H, W, ws, ws_bytes, pfull)) != BLADE_OK) return s;
+  if ((s = common_checks(h, d_in, N, ws, ws_bytes, pfull)) != BLADE_OK) return s;
   if ((s = check_dev_ptr(h, d_out, "d_out")) != BLADE_OK) return s;
   const size_t fbytes = sizeof(float) * 3 * (size_t)H * W;
   if (ranges_overlap(d_in, fbytes * N, d_out, fbytes * N)) return fail(BLADE_EINVAL, "d_out overlaps d_in");
@@ -776,8 +963,10 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
   cudaEvent_t ev_start = nullptr;
   blade_status rs = BLADE_OK;
   auto cleanup = [&]() {
-    for (auto& e : ev_in) if (e) cudaEventDestroy(e);
-    for (auto& e : ev_done) if (e) cudaEventDestroy(e);
+    for (auto& e : ev_in)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_done)
+      if (e) cudaEventDestroy(e);
     if (ev_start) cudaEventDestroy(ev_start);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
@@ -789,7 +978,6 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
     ce = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
     if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
   }
-  // the copies must not start before work already queued on the caller's stream
   if (ce == cudaSuccess) ce = cudaEventRecord(ev_start, st);
   if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_in, ev_start, 0);
   if (ce != cudaSuccess) {
@@ -803,7 +991,10 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
     ce = cudaMemcpyAsync(d_in + off, in_host + off, fbytes * nf, cudaMemcpyHostToDevice, s_in);
     if (ce == cudaSuccess) ce = cudaEventRecord(ev_in[i], s_in);
     if (ce == cudaSuccess) ce = cudaStreamWaitEvent(st, ev_in[i], 0);
-    if (ce != cudaSuccess) { rs = fail(BLADE_ECUDA, "H2D: %s", cudaGetErrorString(ce)); break; }
+    if (ce != cudaSuccess) {
+      rs = fail(BLADE_ECUDA, "H2D: %s", cudaGetErrorString(ce));
+      break;
+    }
     Plan p;
     plan_rows(h, nf, H, W, 0, H, p);
     LevelView inv = make_view(d_in + off, H, W, Range{0, H});
@@ -812,9 +1003,11 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
     if (rs != BLADE_OK) break;
     ce = cudaEventRecord(ev_done[i], st);
     if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_out, ev_done[i], 0);
-    if (ce == cudaSuccess)
-      ce = cudaMemcpyAsync(out_host + off, d_out + off, fbytes * nf, cudaMemcpyDeviceToHost, s_out);
-    if (ce != cudaSuccess) { rs = fail(BLADE_ECUDA, "D2H: %s", cudaGetErrorString(ce)); break; }
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out_host + off, d_out + off, fbytes * nf, cudaMemcpyDeviceToHost, s_out);
+    if (ce != cudaSuccess) {
+      rs = fail(BLADE_ECUDA, "D2H: %s", cudaGetErrorString(ce));
+      break;
+    }
     f0 += nf;
   }
   ce = cudaStreamSynchronize(s_out);

@@ -1,0 +1,340 @@
+// K3 k_stage_tma: the stage of Eq. 9 (§4) / Eq. 1 (§3) with
+// TMA-staged, double-buffered tiles. Used whenever the whole bank of a stage (all phases) fits in
+// shared memory next to two staging buffers (5x5 / 3x3 pairs, every single-level footprint).
+//
+// Persistent CTA (1 per SM): copy the stage's bank (4 phases x K filters, odd tap stride) into
+// shared memory once, then loop over 16 x 128 output tiles. For tile i+1 one elected thread
+// issues three cp.async.bulk.tensor loads (fine patch of z^l with an r_f halo, coarse patch of
+// u^{l+1} with an r_c halo, the uint8 bucket tile) into the other buffer, completing on an
+// mbarrier, while all threads compute tile i. TMA fills out-of-image cells with zeros; on border
+// tiles a fix-up pass overwrites them with the folded sample (R2), taken from the tile
+// itself or, for tiny levels, from global memory.
+//
+// Each thread computes a 2 x 4 pixel block (rows y, y+1; columns x..x+3): all four 2x2 output
+// phases, so phase(i, j) = 2 i + (j & 1) is static and the two coarse centres floor(x/2),
+// floor(x/2)+1 are shared by column pairs. Per input row the thread loads its window segment once
+// (LDS.128 / LDS.64, conflict-free) and the 8 pixels' taps (LDS.32, per-pixel addresses); the
+// three colour channels share every tap load (R13). FP32 FMA on the CUDA cores.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace blade {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Loads N consecutive floats from p into v[0..N). The address of p is congruent to A floats
+// modulo 4 (i.e. p - A is 16-B aligned when MAXV == 4, 8-B aligned when MAXV == 2); at each
+// position the widest naturally aligned LDS (up to MAXV floats) is used. Compile-time recursion.
+template <int A, int I, int N, int MAXV>
+__device__ __forceinline__ void lds_run_at(const float* p, float* v) {
+  if constexpr (I < N) {
+    if constexpr (MAXV >= 4 && ((A + I) & 3) == 0 && I + 3 < N) {
+      const float4 t = *reinterpret_cast<const float4*>(p + I);
+      v[I] = t.x; v[I + 1] = t.y; v[I + 2] = t.z; v[I + 3] = t.w;
+      lds_run_at<A, I + 4, N, MAXV>(p, v);
+    } else if constexpr (MAXV >= 2 && ((A + I) & 1) == 0 && I + 1 < N) {
+      const float2 t = *reinterpret_cast<const float2*>(p + I);
+      v[I] = t.x; v[I + 1] = t.y;
+      lds_run_at<A, I + 2, N, MAXV>(p, v);
+    } else {
+      v[I] = p[I];
+      lds_run_at<A, I + 1, N, MAXV>(p, v);
+    }
+  }
+}
+template <int A, int N, int MAXV = 4>
+__device__ __forceinline__ void lds_run(const float* p, float* v) {
+  lds_run_at<A, 0, N, MAXV>(p, v);
+}
+
+template <int NF, int NC>
+struct TmaShape {
+  static constexpr int RX = 4, RY = 2, BX = 32, BY = 8;
+  static constexpr int threads = BX * BY;
+  static constexpr int RF = NF / 2, RC = NC / 2;
+  static constexpr int TCOLS = BX * RX, TROWS = BY * RY;  // 128 x 16 outputs per tile
+  // TMA boxes must start on a 16-byte boundary in the innermost dimension: both boxes start 4
+  // columns left of the tile (covers halos up to 4) and the windows start at FO / CO inside.
+  static constexpr int MARGIN = 4;
+  static constexpr int FO = MARGIN - RF, CO = MARGIN - RC;
+  static constexpr int FR = TROWS + 2 * RF;
+  static constexpr int FCB = TCOLS + 2 * MARGIN;            // 136
+  static constexpr int CR = NC ? TROWS / 2 + 2 * RC : 0;
+  static constexpr int CCB = NC ? TCOLS / 2 + 2 * MARGIN : 0;  // 72
+  static constexpr int fine_bytes = 3 * FR * FCB * 4;
+  static constexpr int coarse_bytes = 3 * CR * CCB * 4;
+  static constexpr int map_bytes = TROWS * TCOLS;
+  static constexpr int al(int x) { return (x + 127) & ~127; }
+  static constexpr int fine_off = 0;
+  static constexpr int coarse_off = al(fine_bytes);
+  static constexpr int map_off = coarse_off + al(coarse_bytes);
+  static constexpr int stage_bytes = map_off + al(map_bytes);
+  static constexpr int FWIN = NF + RX - 1;  // fine window columns per thread
+  static constexpr int CWIN = NC + 1;       // coarse window columns per thread
+  static_assert(RF <= MARGIN && RC <= MARGIN, "halo wider than the TMA margin");
+};
+
+struct StageTmaArgs {
+  int H, W;            // level l dims (global)
+  int H1, W1;          // level l+1 dims
+  int z_row0, z_rows;  // rows of the z^l buffer
+  int u_row0, u_rows;  // rows of the u^{l+1} buffer
+  int map_row0, map_rows;
+  const float* z;      // z^l buffer (generic pointer, fix-up path for tiny levels)
+  const float* u1;
+  float* out;          // u^l buffer, rows [out_row0, out_row0 + out_rows)
+  int out_row0, out_rows;
+  const float* bank;   // [phase][PS] for this stage
+  int K, S, PS, n_phases;
+  int N;
+  int y_base;          // first tile row (even)
+  int o_r0, o_rn;      // output rows computed
+  int tiles_x, tiles_y, n_tiles;
+  int clamp;
+};
+
+template <int NF, int NC>
+__global__ void __launch_bounds__(256, 1)
+    k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
+                const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
+  using SS = TmaShape<NF, NC>;
+  constexpr int RF = SS::RF, RC = SS::RC;
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  // layout: [stage buffers x2][bank][mbarriers]
+  unsigned char* buf0 = tma_smem;
+  const int bank_floats = a.n_phases * a.PS;
+  float* sbank = reinterpret_cast<float*>(tma_smem + 2 * SS::stage_bytes);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tma_smem + 2 * SS::stage_bytes + ((bank_floats * 4 + 127) & ~127));
+
+  const int tid = threadIdx.y * SS::BX + threadIdx.x;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  constexpr uint32_t tx_bytes = SS::fine_bytes + SS::coarse_bytes + SS::map_bytes;
+
+  auto tile_coords = [&](int t, int& n, int& X0, int& Y0) {
+    n = t / (a.tiles_x * a.tiles_y);
+    const int rem = t - n * a.tiles_x * a.tiles_y;
+    const int tyi = rem / a.tiles_x;
+    X0 = (rem - tyi * a.tiles_x) * SS::TCOLS;
+    Y0 = a.y_base + tyi * SS::TROWS;
+  };
+  auto issue = [&](int t, int b) {
+    int n, X0, Y0;
+    tile_coords(t, n, X0, Y0);
+    unsigned char* sb = buf0 + b * SS::stage_bytes;
+    mbar_expect_tx(&mbar[b], tx_bytes);
+    tma_load_3d(sb + SS::fine_off, &tm_z, X0 - SS::MARGIN, Y0 - RF - a.z_row0, n * 3, &mbar[b]);
+    if constexpr (NC > 0)
+      tma_load_3d(sb + SS::coarse_off, &tm_u, X0 / 2 - SS::MARGIN, Y0 / 2 - RC - a.u_row0, n * 3, &mbar[b]);
+    tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[b]);
+  };
+
+  int t = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (t < a.n_tiles) issue(t, 0);
+  }
+  // ---- the bank -> shared memory, once
+  {
+    const float4* g4 = reinterpret_cast<const float4*>(a.bank);
+    float4* s4 = reinterpret_cast<float4*>(sbank);
+    for (int i = tid; i < (bank_floats >> 2); i += SS::threads) s4[i] = __ldg(g4 + i);
+  }
+  __syncthreads();
+
+  for (int it = 0; t < a.n_tiles; ++it, t += gridDim.x) {
+    const int b = it & 1;
+    const int tn = t + gridDim.x;
+    if (tid == 0 && tn < a.n_tiles) {
+      fence_proxy_async();  // generic-proxy accesses of buffer b^1 (previous tile) are ordered
+      issue(tn, b ^ 1);
+    }
+    int n, X0, Y0;
+    tile_coords(t, n, X0, Y0);
+    mbar_wait(&mbar[b], (it >> 1) & 1);
+    float* sfine = reinterpret_cast<float*>(buf0 + b * SS::stage_bytes + SS::fine_off);
+    float* scoarse = reinterpret_cast<float*>(buf0 + b * SS::stage_bytes + SS::coarse_off);
+    const uint8_t* smap = buf0 + b * SS::stage_bytes + SS::map_off;
+
+    // ---- border fix-up: out-of-image cells <- folded samples
+    const int FX = X0 - SS::MARGIN, CX = X0 / 2 - SS::MARGIN;  // box origins (columns)
+    const bool fine_border = FX < 0 || FX + SS::FCB > a.W || Y0 - RF < 0 || Y0 + SS::TROWS + RF > a.H;
+    const bool coarse_border = NC > 0 && (CX < 0 || CX + SS::CCB > a.W1 || Y0 / 2 - RC < 0 ||
+                                          Y0 / 2 - RC + SS::CR > a.H1);
+    if (fine_border || coarse_border) {
+      if (fine_border) {
+        for (int i = tid; i < SS::FR * SS::FCB; i += SS::threads) {
+          const int r = i / SS::FCB, q = i - r * SS::FCB;
+          const int gy = Y0 - RF + r, gx = FX + q;
+          if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) continue;
+          const int fy = fold_idx(gy, a.H), fx = fold_idx(gx, a.W);
+          const int ry = fy - (Y0 - RF), rx = fx - FX;
+          const bool in_tile = ry >= 0 && ry < SS::FR && rx >= 0 && rx < SS::FCB;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float v;
+            if (in_tile) {
+              v = sfine[(c * SS::FR + ry) * SS::FCB + rx];
+            } else {
+              const int by = min(max(fy - a.z_row0, 0), a.z_rows - 1);
+              v = a.z[(((long long)n * 3 + c) * a.z_rows + by) * a.W + fx];
+            }
+            sfine[(c * SS::FR + r) * SS::FCB + q] = v;
+          }
+        }
+      }
+      if constexpr (NC > 0) {
+        if (coarse_border) {
+          const int CY0 = Y0 / 2 - RC, CX0 = CX;
+          for (int i = tid; i < SS::CR * SS::CCB; i += SS::threads) {
+            const int r = i / SS::CCB, q = i - r * SS::CCB;
+            const int gy = CY0 + r, gx = CX0 + q;
+            if (gy >= 0 && gy < a.H1 && gx >= 0 && gx < a.W1) continue;
+            const int fy = fold_idx(gy, a.H1), fx = fold_idx(gx, a.W1);
+            const int ry = fy - CY0, rx = fx - CX0;
+            const bool in_tile = ry >= 0 && ry < SS::CR && rx >= 0 && rx < SS::CCB;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              float v;
+              if (in_tile) {
+                v = scoarse[(c * SS::CR + ry) * SS::CCB + rx];
+              } else {
+                const int by = min(max(fy - a.u_row0, 0), a.u_rows - 1);
+                v = a.u1[(((long long)n * 3 + c) * a.u_rows + by) * a.W1 + fx];
+              }
+              scoarse[(c * SS::CR + r) * SS::CCB + q] = v;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- this thread's 2 x 4 block
+    const int x = X0 + SS::RX * tx;
+    const int y = Y0 + SS::RY * ty;
+    const uint32_t mrow0 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty) * SS::TCOLS + 4 * tx);
+    const uint32_t mrow1 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty + 1) * SS::TCOLS + 4 * tx);
+    const float* tp[2][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k0 = (mrow0 >> (8 * j)) & 0xff, k1 = (mrow1 >> (8 * j)) & 0xff;
+      const int ph0 = a.n_phases == 4 ? (j & 1) : 0;
+      const int ph1 = a.n_phases == 4 ? 2 + (j & 1) : 0;
+      tp[0][j] = sbank + ph0 * a.PS + k0 * a.S;
+      tp[1][j] = sbank + ph1 * a.PS + k1 * a.S;
+    }
+    float acc[2][4][3];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[i][j][c] = 0.0f;
+
+    if constexpr (NC > 0) {
+      // coarse rows local ty .. ty+NC-1 (both pixel rows share floor(y/2)); cols 2tx .. 2tx+NC
+#pragma unroll
+      for (int wr = 0; wr < NC; ++wr) {
+        float v[3][SS::CWIN];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          lds_run<(SS::CO & 1), SS::CWIN, 2>(scoarse + (c * SS::CR + ty + wr) * SS::CCB + 2 * tx + SS::CO, v[c]);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int dx = 0; dx < NC; ++dx) {
+              const float tap = tp[i][j][NF * NF + wr * NC + dx];
+#pragma unroll
+              for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][(j >> 1) + dx], acc[i][j][c]);
+            }
+      }
+    }
+    // fine rows local 2ty .. 2ty+NF (NF+1 rows), cols 4tx .. 4tx+NF+2
+#pragma unroll
+    for (int wr = 0; wr < NF + 1; ++wr) {
+      float v[3][SS::FWIN];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        lds_run<SS::FO, SS::FWIN>(sfine + (c * SS::FR + 2 * ty + wr) * SS::FCB + 4 * tx + SS::FO, v[c]);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int dy = wr - i;
+        if (dy < 0 || dy >= NF) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int dx = 0; dx < NF; ++dx) {
+            const float tap = tp[i][j][dy * NF + dx];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][j + dx], acc[i][j][c]);
+          }
+      }
+    }
+
+    // ---- store (rows y, y+1; cols x .. x+3)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int yy = y + i;
+      if (yy < a.o_r0 || yy >= a.o_r0 + a.o_rn || x >= a.W) continue;
+      float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.W + x;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float v0 = acc[i][0][c], v1 = acc[i][1][c], v2 = acc[i][2][c], v3 = acc[i][3][c];
+        if (a.clamp) {
+          v0 = fminf(fmaxf(v0, 0.0f), 1.0f);
+          v1 = fminf(fmaxf(v1, 0.0f), 1.0f);
+          v2 = fminf(fmaxf(v2, 0.0f), 1.0f);
+          v3 = fminf(fmaxf(v3, 0.0f), 1.0f);
+        }
+        float* d = op + (long long)c * a.out_rows * a.W;
+        if (x + 3 < a.W) {
+          *reinterpret_cast<float4*>(d) = make_float4(v0, v1, v2, v3);  // W % 4 == 0 on this path
+        } else {
+          d[0] = v0;
+          if (x + 1 < a.W) d[1] = v1;
+          if (x + 2 < a.W) d[2] = v2;
+        }
+      }
+    }
+    __syncthreads();  // buffer b is free for the TMA issued at the next-but-one iteration
+  }
+}
+
+}  // namespace blade

@@ -1,11 +1,9 @@
-// Hot-path kernels of the multiscale BLADE denoiser for B200 (sm_100a).
+// Shared definitions of the hot-path kernels (B200, sm_100a) and the generic stage kernel.
 //
-//   K1 k_decimate : z^{l+1} = 8-tap antialiased bicubic 2x decimation of z^l
-//                   (§4 "Standard bicubic downsampling"; R14)
-//   K2 k_selector : s^l = bucket(theta, strength, coherence) of the joint-colour structure
-//                   tensor of z^l (§3 Eq. 6; R3-R8)
-//   K3 k_stage    : u^l = sum f u^{l+1}_{i/2+j} + sum g z^l_{i+j}  (§4 Eq. 9);
-//                   Eq. 1 when there is no coarse block.
+//   k_down      (k_down.cuh)      : fused decimation + selector at level l (K1 + K2)
+//   k_stage_tma (k_stage_tma.cuh) : Eq. 9 / Eq. 1 stage with TMA double-buffered tiles (K3)
+//   k_stage     (this file)       : Eq. 9 stage, generic fallback: CTAs specialised by output-row
+//                                   parity so 7x7 / 9x9 pair banks fit; synchronous staging (K3')
 //
 // All arithmetic is FP32 on the CUDA cores (no fast-math: IEEE sqrt/div, accurate atan2f).
 // Tensor cores are not used: every pixel contracts with its own selected filter, so the
@@ -46,181 +44,7 @@ __device__ __forceinline__ int view_row(const LevelView& v, int y) {
 }
 
 // ------------------------------------------------------------------------------------------
-// K1 decimation. Weights: Keys cubic (a = -0.5) at |t|/2, t = -3.5..3.5, normalised:
-// [-3, -9, 29, 111, 111, 29, -9, -3] / 256, exact in fp32. Output (y, x) reads input rows
-// 2y-3 .. 2y+4 and columns 2x-3 .. 2x+4 (centre at 2y + 0.5). Separable: horizontal pass into
-// shared memory, then vertical. The per-pixel arithmetic does not depend on the tile.
-// ------------------------------------------------------------------------------------------
-namespace dec {
-constexpr int TX = 32, TY = 16;
-constexpr int IN_R = 2 * TY + 6, IN_C = 2 * TX + 6;
-}  // namespace dec
-
-__device__ __forceinline__ float dec_w(int a) {
-  // constexpr table in registers: fp32-exact k/256
-  const float w0 = -3.0f / 256.0f, w1 = -9.0f / 256.0f, w2 = 29.0f / 256.0f, w3 = 111.0f / 256.0f;
-  switch (a) {
-    case 0: case 7: return w0;
-    case 1: case 6: return w1;
-    case 2: case 5: return w2;
-    default: return w3;
-  }
-}
-
-// grid: (ceil(W_out / TX), ceil(out_rows / TY), N); block (32, 8)
-__global__ void __launch_bounds__(256) k_decimate(LevelView in, LevelView out, int out_r0,
-                                                  int out_rn) {
-  __shared__ float tile[dec::IN_R][dec::IN_C + 1];
-  __shared__ float hp[dec::IN_R][dec::TX + 1];
-  const int n = blockIdx.z;
-  const int ox0 = blockIdx.x * dec::TX;
-  const int oy0 = out_r0 + blockIdx.y * dec::TY;  // global output row of the tile
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  const float* src = in.p + (long long)n * in.frame;
-  float* dst = out.p + (long long)n * out.frame;
-  for (int c = 0; c < 3; ++c) {
-    const float* sp = src + c * in.plane;
-    for (int i = tid; i < dec::IN_R * dec::IN_C; i += 256) {
-      const int r = i / dec::IN_C, q = i - r * dec::IN_C;
-      const int gy = 2 * oy0 - 3 + r, gx = 2 * ox0 - 3 + q;
-      tile[r][q] = __ldg(sp + (long long)view_row(in, gy) * in.W + fold_idx(gx, in.W));
-    }
-    __syncthreads();
-    for (int i = tid; i < dec::IN_R * dec::TX; i += 256) {
-      const int r = i / dec::TX, j = i - r * dec::TX;
-      float acc = 0.0f;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) acc = fmaf(dec_w(b), tile[r][2 * j + b], acc);
-      hp[r][j] = acc;
-    }
-    __syncthreads();
-    const int j = threadIdx.x;
-    const int ox = ox0 + j;
-#pragma unroll
-    for (int k = 0; k < dec::TY / 8; ++k) {
-      const int i = threadIdx.y + 8 * k;
-      const int oy = oy0 + i;
-      if (ox < out.W && oy < out_r0 + out_rn) {
-        float acc = 0.0f;
-#pragma unroll
-        for (int a = 0; a < 8; ++a) acc = fmaf(dec_w(a), hp[2 * i + a][j], acc);
-        dst[c * out.plane + (long long)(oy - out.row0) * out.W + ox] = acc;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// K2 selector. Per pixel: central-difference gradients of the folded image [R3], per-channel
-// products summed over RGB (Eq. 6) kept as T = sum gx^2+gy^2, D = sum (gx-gy)(gx+gy) and
-// B = sum gx gy (D avoids the a - c cancellation), separable Gaussian window [R4], closed-form
-// eigen-features and the quantiser [R7]:
-//   lambda_{1,2} = T/2 +- sqrt((D/2)^2 + B^2), S = sqrt(l1), C = (sqrt l1 - sqrt l2)/(sqrt l1 +
-//   sqrt l2), theta = (atan2(2B, D)/2 + pi/2) mod pi  (0 when D == 0 and B == 0) [R5, R6],
-//   o = floor(theta n_o / pi) mod n_o = floor(atan2(2B, D) n_o/(2 pi) + n_o/2) mod n_o.
-// ------------------------------------------------------------------------------------------
-constexpr int kMaxThr = 15;
-struct SelParams {
-  float w[8];  // window weights e(d)/sum e, d = -r..r (normalised in fp64, rounded to fp32)
-  int n_o, n_s, n_c;
-  float ts[kMaxThr];  // strength thresholds (rounded up to fp32)
-  float tc[kMaxThr];  // coherence thresholds
-};
-
-namespace sel {
-constexpr int TX = 32, TY = 16;
-}
-
-template <int WS>
-__global__ void __launch_bounds__(256) k_selector(LevelView z, uint8_t* map, int map_row0,
-                                                  int map_rows, int out_r0, int out_rn,
-                                                  SelParams prm) {
-  constexpr int RW = WS / 2;    // window radius
-  constexpr int R = RW + 1;     // halo of the image tile
-  constexpr int ZR = sel::TY + 2 * R, ZC = sel::TX + 2 * R;
-  constexpr int FR = sel::TY + 2 * RW, FC = sel::TX + 2 * RW;
-  __shared__ float zt[3][ZR][ZC];
-  __shared__ float F[3][FR][FC + 1];
-  __shared__ float Hq[3][FR][sel::TX + 1];
-  const int n = blockIdx.z;
-  const int ox0 = blockIdx.x * sel::TX;
-  const int oy0 = out_r0 + blockIdx.y * sel::TY;
-  const int tid = threadIdx.y * 32 + threadIdx.x;
-  const float* src = z.p + (long long)n * z.frame;
-  for (int i = tid; i < 3 * ZR * ZC; i += 256) {
-    const int c = i / (ZR * ZC);
-    const int rem = i - c * ZR * ZC;
-    const int r = rem / ZC, q = rem - r * ZC;
-    zt[c][r][q] = __ldg(src + c * z.plane + (long long)view_row(z, oy0 - R + r) * z.W +
-                        fold_idx(ox0 - R + q, z.W));
-  }
-  __syncthreads();
-  for (int i = tid; i < FR * FC; i += 256) {
-    const int r = i / FC, q = i - r * FC;
-    float T = 0.0f, D = 0.0f, B = 0.0f;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float gx = (zt[c][r + 1][q + 2] - zt[c][r + 1][q]) * 0.5f;
-      const float gy = (zt[c][r + 2][q + 1] - zt[c][r][q + 1]) * 0.5f;
-      T = fmaf(gx, gx, fmaf(gy, gy, T));
-      D = fmaf(gx - gy, gx + gy, D);
-      B = fmaf(gx, gy, B);
-    }
-    F[0][r][q] = T;
-    F[1][r][q] = D;
-    F[2][r][q] = B;
-  }
-  __syncthreads();
-  for (int i = tid; i < 3 * FR * sel::TX; i += 256) {
-    const int f = i / (FR * sel::TX);
-    const int rem = i - f * FR * sel::TX;
-    const int r = rem / sel::TX, j = rem - r * sel::TX;
-    float acc = 0.0f;
-#pragma unroll
-    for (int d = 0; d < WS; ++d) acc = fmaf(prm.w[d], F[f][r][j + d], acc);
-    Hq[f][r][j] = acc;
-  }
-  __syncthreads();
-  const int j = threadIdx.x;
-  const int ox = ox0 + j;
-  const float kTwoPiInv = 0.15915494309189535f;  // 1 / (2 pi)
-#pragma unroll
-  for (int k = 0; k < sel::TY / 8; ++k) {
-    const int i = threadIdx.y + 8 * k;
-    const int oy = oy0 + i;
-    if (ox >= z.W || oy >= out_r0 + out_rn) continue;
-    float T = 0.0f, D = 0.0f, B = 0.0f;
-#pragma unroll
-    for (int d = 0; d < WS; ++d) {
-      T = fmaf(prm.w[d], Hq[0][i + d][j], T);
-      D = fmaf(prm.w[d], Hq[1][i + d][j], D);
-      B = fmaf(prm.w[d], Hq[2][i + d][j], B);
-    }
-    const float half_tr = 0.5f * T;
-    const float hd = 0.5f * D;
-    const float r = sqrtf(fmaf(hd, hd, B * B));
-    const float l1 = half_tr + r;
-    const float l2 = fmaxf(half_tr - r, 0.0f);
-    const float s1 = sqrtf(fmaxf(l1, 0.0f)), s2 = sqrtf(l2);
-    const float coh = l1 > 0.0f ? __fdiv_rn(s1 - s2, s1 + s2) : 0.0f;
-    int o = 0;
-    if (!(D == 0.0f && B == 0.0f)) {
-      const float phi = atan2f(2.0f * B, D);
-      o = (int)floorf(fmaf(phi, (float)prm.n_o * kTwoPiInv, 0.5f * (float)prm.n_o));
-      o %= prm.n_o;
-      if (o < 0) o += prm.n_o;
-    }
-    int s = 0, kk = 0;
-    for (int t = 0; t < prm.n_s - 1; ++t) s += (prm.ts[t] <= s1);
-    for (int t = 0; t < prm.n_c - 1; ++t) kk += (prm.tc[t] <= coh);
-    map[(long long)n * map_rows * z.W + (long long)(oy - map_row0) * z.W + ox] =
-        (uint8_t)((o * prm.n_s + s) * prm.n_c + kk);
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// K3 stage (Eq. 9 / Eq. 1). Persistent CTAs: each CTA copies the filterbank of its stage (the
+// K3' stage (Eq. 9 / Eq. 1), generic fallback. Persistent CTAs: each CTA copies the filterbank of its stage (the
 // phases it needs) into shared memory ONCE and then loops over output tiles. Per tile it
 // stages the fine patch of z^l (tile + r_f halo, 3 channels) and the coarse patch of u^{l+1}
 // (tile/2 + r_c halo) in shared memory, folded at the true image border. Each thread computes
