@@ -126,20 +126,25 @@ def level_dims(H, W, L):
 
 
 def algorithmic_work(cfg, N):
-    """Algorithmic bytes / FLOPs per kernel launch."""
+    """Algorithmic HBM bytes / FP32 FLOPs per kernel launch for N frames.
+
+    k_down(l) ("selector" in the profile): reads z^l (12 B/px at l = 0, fp32; 24 B/px fp64 at
+    l >= 1), writes s^l (1 B/px) and z^{l+1} as fp64 + fp32 (fp64 omitted for the last level).
+    k_stage(l): reads z^l fp32 (12 B/px), u^{l+1} fp32 (12 B per coarse px), s^l (1 B/px), writes
+    u^l fp32 (12 B/px); FLOPs = 2 * 3 * (nf^2 + nc^2) per output pixel (one FMA = 2 FLOPs).
+    """
     d = level_dims(cfg.H, cfg.W, cfg.levels)
     L = cfg.levels
     nf2 = cfg.fine_size ** 2
     nc2 = cfg.coarse_size ** 2 if L > 1 else 0
     out = {}
-    for l in range(L - 1):  # K1: read z^l (12 B/px), write z^{l+1}
-        px, px1 = d[l][0] * d[l][1], d[l + 1][0] * d[l + 1][1]
-        out[("decimate", l)] = dict(bytes=N * 12 * (px + px1), flops=N * 3 * px1 * 2 * 16)
     nsel = 1 if L == 1 else L - 1
     for l in range(nsel):
         px = d[l][0] * d[l][1]
-        out[("selector", l)] = dict(bytes=N * (12 * px + px), flops=None)
         px1 = d[l + 1][0] * d[l + 1][1] if L > 1 else 0
+        rd = (12 if l == 0 else 24) * px
+        wr = px + (px1 * (12 + (24 if l + 1 < L - 1 else 0)) if L > 1 else 0)
+        out[("selector", l)] = dict(bytes=N * (rd + wr), flops=None)
         out[("stage", l)] = dict(bytes=N * (12 * px + 12 * px1 + px + 12 * px),
                                  flops=N * px * 3 * 2 * (nf2 + nc2))
     return out
@@ -147,29 +152,37 @@ def algorithmic_work(cfg, N):
 
 # ----------------------------------------------------------------------------- reference arm
 
-def oracle_sample_rate(cfg, target_s: float, rows_cap: int | None = None):
-    """Time the fp64 oracle on bounded samples of the workload: full-width row bands of
-    successive frames (each band treated as an image), until ~target_s of CPU time."""
+def oracle_sample_rate(cfg, target_s: float):
+    """Time the fp64 oracle (all host cores) on a bounded sample of the workload: whole frames of
+    the config (frame 0, 1, ...) until about target_s seconds have been spent (at least one
+    frame; if one frame would take longer than target_s, a full-width band of frame 0 treated
+    as an image)."""
     import oracle
     oracle.build()
+    taps = cfg.taps()
     W = cfg.W
-    # calibrate on a small band
     rows = min(cfg.H, 64)
-    z = cfg.frame(0, row0=0, rows=rows)
     sub = bs.Config(**{**cfg.__dict__, "H": rows})
+    z = cfg.frame(0, row0=0, rows=rows)
     t = time.perf_counter()
-    oracle.denoise_config(sub, z)
+    oracle.denoise_config(sub, z, taps)
     per_px = (time.perf_counter() - t) / (rows * W)
-    rows = int(min(cfg.H, max(16, target_s / max(per_px, 1e-12) / W)))
-    if rows_cap:
-        rows = min(rows, rows_cap)
-    sub = bs.Config(**{**cfg.__dict__, "H": rows})
-    z = cfg.frame(0, row0=0, rows=rows)
-    t = time.perf_counter()
-    oracle.denoise_config(sub, z)
-    dt = time.perf_counter() - t
-    mp = rows * W / 1e6
-    return mp / dt, dt, rows, oracle.max_threads()
+    if per_px * cfg.H * W > target_s:  # one frame is already too long: a band of frame 0
+        rows = int(min(cfg.H, max(16, target_s / per_px / W)))
+        sub = bs.Config(**{**cfg.__dict__, "H": rows})
+        z = cfg.frame(0, row0=0, rows=rows)
+        t = time.perf_counter()
+        oracle.denoise_config(sub, z, taps)
+        dt = time.perf_counter() - t
+        return rows * W / 1e6 / dt, dt, f"one {rows}x{W} full-width band of frame 0", oracle.max_threads()
+    n, dt = 0, 0.0
+    while dt < target_s and n < max(cfg.N, 1) * 4:
+        z = cfg.frame(n % max(cfg.N, 1))
+        t = time.perf_counter()
+        oracle.denoise_config(cfg, z, taps)
+        dt += time.perf_counter() - t
+        n += 1
+    return n * cfg.H * W / 1e6 / dt, dt, f"{n} full {cfg.H}x{W} frame(s)", oracle.max_threads()
 
 
 def run_reference(args):
@@ -340,21 +353,22 @@ def main():
                 "hbm_frac_of_measured": w["bytes"] / (dom_ms / 1e3) / 1e9 / hbm_peak}
     else:
         ach = w["bytes"] / (dom_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom[0], "achieved": ach, "peak": hbm_peak,
+        roof = {"bound": "hbm", "kernel": f"k_down level {dom[1]}", "achieved": ach, "peak": hbm_peak,
                 "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
                 "ms_per_launch": dom_ms}
     step_bytes = sum(v["bytes"] for v in work.values())
-    hbm_ach = step_bytes * world / (ms_per_step / 1e3) / 1e9 / world
-    breakdown = {f"{k[0]}{k[1]}": round(t, 4) for k, (t, c) in sorted(kern.items())}
+    hbm_ach = step_bytes / (ms_per_step / 1e3) / 1e9  # per GPU
+    names = {"selector": "k_down", "stage": "k_stage", "decimate": "k_decimate"}
+    breakdown = {f"{names.get(k[0], k[0])}{k[1]}": round(t, 4) for k, (t, c) in sorted(kern.items())}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            mps, dt, rows, cores = oracle_sample_rate(cfg, args.cpu_seconds)
+            mps, dt, what, cores = oracle_sample_rate(cfg, args.cpu_seconds)
             cpu = {"value": mps, "unit": "MP/s", "cores": cores, "kind": "oracle",
-                   "sample": f"one {rows}x{W} full-width band of a {cfg.name} frame, fp64 oracle "
-                             f"({dt:.1f} s)"}
+                   "sample": f"{what} of {cfg.name}, fp64 C oracle, OpenMP over rows "
+                             f"({dt:.1f} s of CPU time)"}
         except Exception as e:  # the baseline must never break the GPU line
             cpu = {"value": None, "unit": "MP/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {e}"}
