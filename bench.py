@@ -128,8 +128,9 @@ def level_dims(H, W, L):
 def algorithmic_work(cfg, N):
     """Algorithmic HBM bytes / FP32 FLOPs per kernel launch for N frames.
 
-    k_down(l) ("selector" in the profile): reads z^l (12 B/px at l = 0, fp32; 24 B/px fp64 at
-    l >= 1), writes s^l (1 B/px) and z^{l+1} as fp64 + fp32 (fp64 omitted for the last level).
+    k_down(l) ("selector" in the profile): reads z^l (12 B/px at l = 0, fp32; 24 B/px hi + lo
+    fp32 pair at l >= 1), writes s^l (1 B/px) and z^{l+1} as hi (+ lo unless l+1 is the
+    coarsest level), 12 (+12) B per level-(l+1) px.
     k_stage(l): reads z^l fp32 (12 B/px), u^{l+1} fp32 (12 B per coarse px), s^l (1 B/px), writes
     u^l fp32 (12 B/px); FLOPs = 2 * 3 * (nf^2 + nc^2) per output pixel (one FMA = 2 FLOPs).
     """
@@ -143,7 +144,7 @@ def algorithmic_work(cfg, N):
         px = d[l][0] * d[l][1]
         px1 = d[l + 1][0] * d[l + 1][1] if L > 1 else 0
         rd = (12 if l == 0 else 24) * px
-        wr = px + (px1 * (12 + (24 if l + 1 < L - 1 else 0)) if L > 1 else 0)
+        wr = px + (px1 * (12 + (12 if l + 1 < L - 1 else 0)) if L > 1 else 0)
         out[("selector", l)] = dict(bytes=N * (rd + wr), flops=None)
         out[("stage", l)] = dict(bytes=N * (12 * px + 12 * px1 + px + 12 * px),
                                  flops=N * px * 3 * 2 * (nf2 + nc2))

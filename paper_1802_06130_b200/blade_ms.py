@@ -57,7 +57,11 @@ EXPORTS = ["blade_ms_create", "blade_ms_workspace_size", "blade_ms_denoise", "bl
 
 
 def library_path() -> Path:
-    return _build.LIB
+    """The in-tree library; BLADE_MS_LIB=<path> selects another build of the same ABI
+    (kernel-variant experiments only; never a CPU path)."""
+    import os
+    alt = os.environ.get("BLADE_MS_LIB")
+    return Path(alt) if alt else _build.LIB
 
 
 def lib():
@@ -70,7 +74,7 @@ def lib():
     except Exception as e:  # no nvcc on this machine: use the shipped .so if present
         if not _build.LIB.exists():
             raise RuntimeError(f"libblade_ms.so is missing and could not be built: {e}") from e
-    L = ctypes.CDLL(str(_build.LIB))
+    L = ctypes.CDLL(str(library_path()))
     P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
     L.blade_ms_create.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(_Layout), P, sz,
                                   ctypes.c_int, ctypes.POINTER(P)]

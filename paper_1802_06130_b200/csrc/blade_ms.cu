@@ -11,7 +11,8 @@
 // are the band's dependency cone, so the same code serves both and bands are bit-identical.
 //
 // Data in HBM: z^0 = the caller's fp32 input; for l >= 1, z^l is kept in
-// fp64 (selector and decimation chain, l <= L-2) and fp32 (stage input); u^l fp32; s^l uint8.
+// an fp32 pair hi + lo (hi = stage input; hi + lo = the exact fp64 decimation, input of the next
+// selector and decimation, l <= L-2); u^l fp32; s^l uint8.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -115,27 +116,17 @@ const std::vector<TmaVariant>& tma_variants() {
   return v;
 }
 
-using DownKernelF = decltype(&k_down<float, 5, true>);
-using DownKernelD = decltype(&k_down<double, 5, true>);
-DownKernelF down_kernel_f(int ws, bool dec) {
-  switch (ws * 2 + (dec ? 1 : 0)) {
-    case 2: return &k_down<float, 1, false>;
-    case 3: return &k_down<float, 1, true>;
-    case 6: return &k_down<float, 3, false>;
-    case 7: return &k_down<float, 3, true>;
-    case 10: return &k_down<float, 5, false>;
-    case 11: return &k_down<float, 5, true>;
-  }
-  return nullptr;
+using DownKernel = void (*)(const DownArgs, const DownParams);
+template <bool FAST>
+DownKernel down_kernel_t(bool hilo, bool dec) {
+  if (hilo) return dec ? &k_down<true, true, FAST> : &k_down<true, false, FAST>;
+  return dec ? &k_down<false, true, FAST> : &k_down<false, false, FAST>;
 }
-DownKernelD down_kernel_d(int ws) {
-  switch (ws) {
-    case 1: return &k_down<double, 1, true>;
-    case 3: return &k_down<double, 3, true>;
-    case 5: return &k_down<double, 5, true>;
-  }
-  return nullptr;
+// FAST: the configs' layout (16 orientations, <= 3 strength and coherence bins)
+DownKernel down_kernel(bool hilo, bool dec, bool fast) {
+  return fast ? down_kernel_t<true>(hilo, dec) : down_kernel_t<false>(hilo, dec);
 }
+size_t down_smem(bool hilo) { return sizeof(float) * down::WARPS * down::RING * (hilo ? 6 : 3) * 64; }
 
 // ------------------------------------------------------------------------------ TMA encode
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -235,7 +226,7 @@ struct Plan {
   std::vector<Range> z;  // rows of z^l materialised (level 0: needed input rows)
   std::vector<Range> u;  // rows of u^l computed (= map rows), l <= L-2 (l = 0 if L == 1)
   size_t ws_bytes = 0;
-  std::vector<size_t> z32_off, z64_off, u_off, map_off;
+  std::vector<size_t> z32_off, zlo_off, u_off, map_off;
 };
 
 // Dependency cone of output rows [o0, o0+on) of the final output.
@@ -275,7 +266,7 @@ void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) 
   }
   size_t off = 0;
   p.z32_off.assign(L, 0);
-  p.z64_off.assign(L, 0);
+  p.zlo_off.assign(L, 0);
   p.u_off.assign(L, 0);
   p.map_off.assign(L, 0);
   for (int l = 1; l < L; ++l) {
@@ -283,8 +274,8 @@ void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) 
     off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
   }
   for (int l = 1; l + 1 < L; ++l) {
-    p.z64_off[l] = off;
-    off = align256(off + sizeof(double) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
+    p.zlo_off[l] = off;
+    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
   }
   for (int l = 1; l + 1 < L; ++l) {
     p.u_off[l] = off;
@@ -386,44 +377,62 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   const int L = p.L, N = p.N;
   if (N == 0) return BLADE_OK;
   std::vector<LevelView> z32(L);
-  std::vector<double*> z64(L, nullptr);
+  std::vector<float*> zlo(L, nullptr);
   z32[0] = in_view;
   for (int l = 1; l < L; ++l) {
     float* base = (levels_out && levels_out[l - 1]) ? levels_out[l - 1]
                                                     : reinterpret_cast<float*>(ws + p.z32_off[l]);
     z32[l] = make_view(base, p.H[l], p.W[l], p.z[l]);
-    if (l + 1 < L) z64[l] = reinterpret_cast<double*>(ws + p.z64_off[l]);
+    if (l + 1 < L) zlo[l] = reinterpret_cast<float*>(ws + p.zlo_off[l]);
   }
   const int nsel = L == 1 ? 1 : L - 1;
   std::vector<uint8_t*> maps(nsel);
   for (int l = 0; l < nsel; ++l)
     maps[l] = (maps_out && maps_out[l]) ? maps_out[l] : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
 
-  // ---- down pass: k_down(l) -> s^l, z^{l+1}
+  // ---- down pass: k_down(l) -> s^l, z^{l+1} (hi, and lo when level l+1 feeds a selector)
   for (int l = 0; l < nsel; ++l) {
     const Range U = p.u[l];
     const bool dec = L > 1;
     Range Z1 = dec ? p.z[l + 1] : Range{0, 0};
     Range R = U;
     if (dec) R = hull(R, Range{2 * Z1.lo, 2 * Z1.hi});
-    const int base = R.lo & ~1;
-    dim3 grid((p.W[l] + down::TX - 1) / down::TX, (R.hi - base + down::TY - 1) / down::TY, N);
-    const int H1 = dec ? p.H[l + 1] : 0, W1 = dec ? p.W[l + 1] : 0;
-    double* o64 = (dec && l + 1 < L - 1) ? z64[l + 1] : nullptr;
-    float* o32 = dec ? z32[l + 1].p : nullptr;
+    DownArgs da{};
+    da.zhi = l == 0 ? in_view.p : z32[l].p;
+    da.zlo = l == 0 ? nullptr : zlo[l];
+    da.H = p.H[l];
+    da.W = p.W[l];
+    da.in_row0 = l == 0 ? in_view.row0 : p.z[l].lo;
+    da.in_rows = l == 0 ? in_view.rows : p.z[l].n();
+    da.in_plane = (long long)da.in_rows * p.W[l];
+    da.in_frame = 3 * da.in_plane;
+    da.map = maps[l];
+    da.s_r0 = U.lo;
+    da.s_rn = U.n();
+    da.ohi = dec ? z32[l + 1].p : nullptr;
+    da.olo = (dec && l + 1 < L - 1) ? zlo[l + 1] : nullptr;
+    da.H1 = dec ? p.H[l + 1] : 1;
+    da.W1 = dec ? p.W[l + 1] : 1;
+    da.d_buf_row0 = Z1.lo;
+    da.d_buf_rows = Z1.n();
+    da.d_r0 = Z1.lo;
+    da.d_rn = Z1.n();
+    da.base = R.lo & ~1;
+    const int span = R.hi - da.base;
+    da.n_strips = (p.W[l] + down::STRIP - 1) / down::STRIP;
+    // band height: enough warps for ~4 waves of 16 resident warps per SM, 16..128 rows (even)
+    const long long col_tasks = (long long)N * da.n_strips;
+    const long long want_bands = std::max<long long>(1, (4LL * 16 * h->num_sms + col_tasks - 1) / col_tasks);
+    int RB = (int)std::min<long long>(128, std::max<long long>(16, (span + want_bands - 1) / want_bands));
+    RB = (RB + 1) & ~1;
+    da.RB = RB;
+    da.n_bands = (span + RB - 1) / RB;
+    da.n_tasks = (int)(col_tasks * da.n_bands);
     ProfScope ps(h, st, 1, l);
-    if (l == 0) {
-      auto fn = down_kernel_f(h->cfg.window_size, dec);
-      fn<<<grid, dim3(32, 8), sizeof(DownSmem), st>>>(
-          in_view.p, p.H[0], p.W[0], in_view.row0, in_view.rows, in_view.plane, in_view.frame, base,
-          maps[0], U.lo, U.n(), o64, o32, H1, W1, Z1.lo, Z1.n(), Z1.lo, Z1.n(), h->down[0]);
-    } else {
-      auto fn = down_kernel_d(h->cfg.window_size);
-      const long long plane = (long long)p.z[l].n() * p.W[l];
-      fn<<<grid, dim3(32, 8), sizeof(DownSmem), st>>>(
-          z64[l], p.H[l], p.W[l], p.z[l].lo, p.z[l].n(), plane, 3 * plane, base, maps[l], U.lo, U.n(),
-          o64, o32, H1, W1, Z1.lo, Z1.n(), Z1.lo, Z1.n(), h->down[l]);
-    }
+    const bool hilo = l > 0;
+    auto fn = down_kernel(hilo, dec, h->n_o == 16 && h->n_s <= 3 && h->n_c <= 3);
+    const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
+    fn<<<grid, 32 * down::WARPS, down_smem(hilo), st>>>(da, h->down[l]);
     LAUNCH_CHECK("k_down");
   }
   if (!run_stages) return BLADE_OK;
@@ -673,22 +682,30 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   for (int s = 0; s < n_stages; ++s) {
     DownParams& dp = h->down[s];
     memset(&dp, 0, sizeof dp);
-    for (int d = 0; d < c.window_size; ++d) {
-      dp.w64[d] = e[d] / se;
-      dp.w32[d] = (float)(e[d] / se);
-    }
+    for (int d = 0; d < c.window_size; ++d) dp.wp[d + 2 - r] = e[d] / se;  // offsets -r..r -> -2..2
     dp.n_o = bl->n_orient;
     dp.n_s = bl->n_strength;
     dp.n_c = bl->n_coherence;
+    for (int i = 0; i < kMaxThr2; ++i) dp.ts2[i] = dp.kc2[i] = INFINITY;
     for (int i = 0; i < bl->n_strength - 1; ++i) {
       const double t = bl->strength_thresholds[(size_t)s * (bl->n_strength - 1) + i];
       dp.ts2[i] = t <= 0.0 ? -INFINITY : (float)(t * t);  // S >= t <=> l1 >= t^2 (t > 0)
     }
+    int npos = 0;
     for (int i = 0; i < bl->n_coherence - 1; ++i) {
       const double t = bl->coherence_thresholds[(size_t)s * (bl->n_coherence - 1) + i];
-      dp.tcA[i] = (float)(1.0 + t * t);
-      dp.tcB[i] = (float)(2.0 * t);
-      dp.tc_nonpos += t <= 0.0;
+      if (t <= 0.0) {
+        dp.tc_nonpos += 1;
+      } else {
+        const double kap = 2.0 * t / (1.0 + t * t);  // C >= t <=> r >= kappa h
+        dp.kc2[npos++] = (float)(kap * kap);
+      }
+    }
+    dp.quad_edges = (bl->n_orient % 4 == 0 && bl->n_orient <= 64) ? 1 : 0;
+    for (int j = 1; dp.quad_edges && j < bl->n_orient / 4; ++j) {
+      const double al = 2.0 * M_PI * j / bl->n_orient;
+      dp.ecos[j - 1] = (float)std::cos(al);
+      dp.esin[j - 1] = (float)std::sin(al);
     }
   }
 
@@ -714,13 +731,11 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   if (ce == cudaSuccess && h->has_tma)
     ce = cudaFuncSetAttribute(h->tma.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
   if (ce == cudaSuccess) {
-    for (int ws = 1; ws <= 5 && ce == cudaSuccess; ws += 2) {
-      ce = cudaFuncSetAttribute(down_kernel_f(ws, true), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem));
-      if (ce == cudaSuccess)
-        ce = cudaFuncSetAttribute(down_kernel_f(ws, false), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem));
-      if (ce == cudaSuccess)
-        ce = cudaFuncSetAttribute(down_kernel_d(ws), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DownSmem));
-    }
+    for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl)
+      for (int dc = 0; dc < 2 && ce == cudaSuccess; ++dc)
+        for (int sm = 0; sm < 2 && ce == cudaSuccess; ++sm)
+          ce = cudaFuncSetAttribute(down_kernel(hl, dc, sm), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)down_smem(hl));
   }
   int occ = 0;
   if (ce == cudaSuccess)

@@ -1,13 +1,17 @@
 #!/bin/bash
-# One gpurun session: GPU parity tests, smoke, bench, ncu launch list (+ optional full capture).
+# One gpurun session: GPU parity tests, smoke, bench, ncu launch list, optional full captures.
+#   PYTEST=0 skips the tests; FULL="k_down:6 k_stage:12" captures (regex:skip) pairs.
 set -x
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 nvidia-smi > gpurun_out/nvsmi.txt 2>&1
+if [ "${PYTEST:-1}" = 1 ]; then
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_launch.log
-if [ -n "$FULL" ]; then
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage -s 12 -c 1 -o gpurun_out/stage_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_full.log 2>&1; echo "ncufull rc=$?" >> gpurun_out/ncu_full.log
 fi
+timeout 600 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 ${BENCH_ARGS} > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_launch.log
+for kv in ${FULL}; do
+  k=${kv%%:*}; s=${kv##*:}
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $s -c 1 -o gpurun_out/${k}_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 ${BENCH_ARGS} > gpurun_out/ncu_full_$k.log 2>&1; echo "ncufull rc=$?" >> gpurun_out/ncu_full_$k.log
+done
