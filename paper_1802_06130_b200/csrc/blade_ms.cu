@@ -97,14 +97,17 @@ const std::vector<StageVariant>& stage_variants() {
 
 using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
 struct TmaVariant {
-  int nf, nc;
+  int nf, nc, groups;
   TmaKernel fn;
   int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc;
 };
-template <int NF, int NC>
+#ifndef BLADE_TMA_GROUPS
+#define BLADE_TMA_GROUPS 2
+#endif
+template <int NF, int NC, int G = BLADE_TMA_GROUPS>
 TmaVariant make_tma() {
   using SS = TmaShape<NF, NC>;
-  return TmaVariant{NF, NC, &k_stage_tma<NF, NC>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
                     SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC};
 }
 // TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
@@ -499,8 +502,8 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       a.tiles_y = (r.hi - y_base + tv.trows - 1) / tv.trows;
       a.n_tiles = N * a.tiles_x * a.tiles_y;
       a.clamp = clamp;
-      const int grid = std::min(h->num_sms, a.n_tiles);
-      tv.fn<<<grid, dim3(32, 8), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+      const int grid = std::min(h->num_sms, (a.n_tiles + tv.groups - 1) / tv.groups);
+      tv.fn<<<grid, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
       LAUNCH_CHECK("k_stage_tma");
       continue;
     }

@@ -126,8 +126,12 @@ struct StageTmaArgs {
   int clamp;
 };
 
-template <int NF, int NC>
-__global__ void __launch_bounds__(256, 1)
+// G = 1: one 256-thread group, double-buffered tiles (TMA of tile i+1 overlaps tile i).
+// G = 2: two 256-thread groups (16 warps) share the bank; each group owns one tile buffer and works
+//        on every other tile, so one group computes while the other waits for its TMA (twice the
+//        resident warps for the same shared memory).
+template <int NF, int NC, int G>
+__global__ void __launch_bounds__(256 * G, 1)
     k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
   using SS = TmaShape<NF, NC>;
@@ -139,8 +143,15 @@ __global__ void __launch_bounds__(256, 1)
   float* sbank = reinterpret_cast<float*>(tma_smem + 2 * SS::stage_bytes);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tma_smem + 2 * SS::stage_bytes + ((bank_floats * 4 + 127) & ~127));
 
-  const int tid = threadIdx.y * SS::BX + threadIdx.x;
-  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int g = G == 2 ? (int)(threadIdx.y >> 3) : 0;  // thread group
+  const int tid = (threadIdx.y & 7) * SS::BX + threadIdx.x;  // thread index within the group
+  const int tx = threadIdx.x, ty = threadIdx.y & 7;
+  auto group_sync = [&]() {
+    if constexpr (G == 2)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(256) : "memory");
+    else
+      __syncthreads();
+  };
   constexpr uint32_t tx_bytes = SS::fine_bytes + SS::coarse_bytes + SS::map_bytes;
 
   auto tile_coords = [&](int t, int& n, int& X0, int& Y0) {
@@ -161,31 +172,34 @@ __global__ void __launch_bounds__(256, 1)
     tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[b]);
   };
 
-  int t = blockIdx.x;
-  if (tid == 0) {
+  const int ctid = threadIdx.y * SS::BX + threadIdx.x;
+  int t = blockIdx.x + g * gridDim.x;
+  const int tstride = G * gridDim.x;
+  if (ctid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (t < a.n_tiles) issue(t, 0);
   }
+  __syncthreads();
+  if (tid == 0 && t < a.n_tiles) issue(t, g);
   // ---- the bank -> shared memory, once
   {
     const float4* g4 = reinterpret_cast<const float4*>(a.bank);
     float4* s4 = reinterpret_cast<float4*>(sbank);
-    for (int i = tid; i < (bank_floats >> 2); i += SS::threads) s4[i] = __ldg(g4 + i);
+    for (int i = ctid; i < (bank_floats >> 2); i += SS::threads * G) s4[i] = __ldg(g4 + i);
   }
   __syncthreads();
 
-  for (int it = 0; t < a.n_tiles; ++it, t += gridDim.x) {
-    const int b = it & 1;
-    const int tn = t + gridDim.x;
-    if (tid == 0 && tn < a.n_tiles) {
+  for (int it = 0; t < a.n_tiles; ++it, t += tstride) {
+    const int b = G == 2 ? g : (it & 1);
+    const int tn = t + tstride;
+    if (G == 1 && tid == 0 && tn < a.n_tiles) {
       fence_proxy_async();  // generic-proxy accesses of buffer b^1 (previous tile) are ordered
       issue(tn, b ^ 1);
     }
     int n, X0, Y0;
     tile_coords(t, n, X0, Y0);
-    mbar_wait(&mbar[b], (it >> 1) & 1);
+    mbar_wait(&mbar[b], G == 2 ? (it & 1) : ((it >> 1) & 1));
     float* sfine = reinterpret_cast<float*>(buf0 + b * SS::stage_bytes + SS::fine_off);
     float* scoarse = reinterpret_cast<float*>(buf0 + b * SS::stage_bytes + SS::coarse_off);
     const uint8_t* smap = buf0 + b * SS::stage_bytes + SS::map_off;
@@ -241,7 +255,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
-      __syncthreads();
+      group_sync();
     }
 
     // ---- this thread's 2 x 4 block
@@ -333,7 +347,11 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-    __syncthreads();  // buffer b is free for the TMA issued at the next-but-one iteration
+    group_sync();  // buffer b is free for the next TMA into it
+    if (G == 2 && tid == 0 && tn < a.n_tiles) {
+      fence_proxy_async();
+      issue(tn, b);
+    }
   }
 }
 
