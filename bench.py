@@ -236,29 +236,57 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1802_06130_b200 import BladeMS
+    from paper_1802_06130_b200.shard import max_over_ranks, shard_for, units
     cfg = bs.load_config(args.config)
     if args.frames:
         cfg.N = args.frames
-    if cfg.N % world:
-        raise SystemExit(f"{cfg.name}: {cfg.N} frames do not split over {world} GPUs")
-    n_local = cfg.N // world
-    f0 = rank * n_local
+    shard = shard_for(cfg, rank, world)
     H, W = cfg.H, cfg.W
-
-    # ---- inputs: this rank's frames, generated on the host (seeded), copied once to HBM
-    x_host = torch.empty((n_local, 3, H, W), dtype=torch.float32).pin_memory()
-    xn = x_host.numpy()
-    for i in range(n_local):
-        bs.scene(cfg.seed, f0 + i, H, W, cfg.n_grat, cfg.n_disk, cfg.noise, cfg.p0, cfg.p1,
-                 out=xn[i])
-    x = x_host.to(dev, non_blocking=False)
-    out = torch.empty_like(x)
     h = BladeMS.from_config(cfg, device=local)
-    ws = h.workspace(n_local, H, W)
     stream = torch.cuda.current_stream(dev)
+    if shard.mode == "frames":
+        # ---- this rank's frames, generated on the host (seeded), copied once to HBM
+        n_local, f0 = shard.frames, shard.frame0
+        x_host = torch.empty((n_local, 3, H, W), dtype=torch.float32).pin_memory()
+        xn = x_host.numpy()
+        for i in range(n_local):
+            bs.scene(cfg.seed, f0 + i, H, W, cfg.n_grat, cfg.n_disk, cfg.noise, cfg.p0, cfg.p1,
+                     out=xn[i])
+        x = x_host.to(dev, non_blocking=False)
+        out = torch.empty_like(x)
+        ws = h.workspace(n_local, H, W)
 
-    def step():
-        h.denoise(x, out, ws, stream)
+        def step():
+            h.denoise(x, out, ws, stream)
+
+        def e2e_step():
+            h.denoise_host(x_host, out_host, d_in, out, ws, stream)
+        out_host = torch.empty_like(x_host).pin_memory()
+        d_in = torch.empty_like(x)
+        io_in = io_out = n_local * 3 * H * W * 4
+    else:
+        # ---- this rank's row band of the one image: input rows of its dependency cone
+        n_local = 1
+        x_host = torch.from_numpy(np.ascontiguousarray(
+            cfg.frame(0, row0=shard.in_row0, rows=shard.in_rows))).pin_memory()
+        x = x_host.to(dev)
+        out = torch.empty((3, shard.out_rows, W), dtype=torch.float32, device=dev)
+        ws = torch.empty(h.band_workspace_size(H, W, shard.out_row0, shard.out_rows),
+                         dtype=torch.uint8, device=dev)
+
+        def step():
+            h.denoise_rows(x, shard.in_row0, shard.out_row0, shard.out_rows, H, out, ws, stream)
+
+        out_host = torch.empty((3, shard.out_rows, W), dtype=torch.float32).pin_memory()
+        d_in = torch.empty_like(x)
+
+        def e2e_step():
+            d_in.copy_(x_host, non_blocking=True)
+            h.denoise_rows(d_in, shard.in_row0, shard.out_row0, shard.out_rows, H, out, ws, stream)
+            out_host.copy_(out, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        io_in = 3 * shard.in_rows * W * 4
+        io_out = 3 * shard.out_rows * W * 4
 
     def barrier():
         if world > 1:
@@ -285,12 +313,10 @@ def main():
     sampler.stop()
     clocks = sampler.summary(t0, t1)
     ms = e0.elapsed_time(e1)
-    t_max = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    ms_max = max_over_ranks(ms, dev)
     ms_per_step = ms_max / args.steps
-    total_px = cfg.N * H * W
+    total_px = cfg.N * H * W  # all ranks together (frames: the batch; bands: the whole image)
+    assert world > 1 or units(cfg, shard) == total_px
     value = total_px / 1e6 / (ms_per_step / 1e3)
 
     # ---- per-kernel breakdown: same steps again with events around every launch
@@ -302,26 +328,24 @@ def main():
     torch.cuda.synchronize(dev)
 
     # ---- end to end through the C ABI with host buffers (H2D + compute + D2H per step)
-    out_host = torch.empty_like(x_host).pin_memory()
-    d_in = torch.empty_like(x)
     e2e_ms = []
-    h.denoise_host(x_host, out_host, d_in, out, ws, stream)  # warm
+    e2e_step()  # warm
     for _ in range(max(args.e2e_steps, 1)):
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        h.denoise_host(x_host, out_host, d_in, out, ws, stream)
+        e2e_step()
         b.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms.append(a.elapsed_time(b))
-    e2e_t = torch.tensor([float(np.median(e2e_ms))], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_val = total_px / 1e6 / (float(e2e_t.item()) / 1e3)
-    io_bytes = n_local * 3 * H * W * 4
+    e2e_t = max_over_ranks(float(np.median(e2e_ms)), dev)
+    e2e_val = total_px / 1e6 / (e2e_t / 1e3)
 
     # ---- roofline of the dominant kernel
-    work = algorithmic_work(cfg, n_local)
+    if shard.mode == "frames":
+        work = algorithmic_work(cfg, n_local)
+    else:  # a band: the work model of an out_rows-row image (the halo rows are not counted)
+        work = algorithmic_work(bs.Config(**{**cfg.__dict__, "H": shard.out_rows}), 1)
     kern = {k: (t / c, c) for k, (t, c) in prof.items()}
     step_kernel_ms = sum(t for t, _ in prof.values()) / args.steps
     dom = max(prof, key=lambda k: prof[k][0])
@@ -383,7 +407,11 @@ def main():
             "config": {"workload": cfg.name, "desc": cfg.description, "frames": cfg.N,
                        "frames_per_gpu": n_local, "H": H, "W": W, "levels": cfg.levels,
                        "fine": cfg.fine_size, "coarse": cfg.coarse_size, "buckets": cfg.K,
-                       "parallelism": f"frames split over {world} GPU(s), no collective",
+                       "parallelism": (f"frames split over {world} GPU(s), no collective"
+                                       if shard.mode == "frames" else
+                                       f"row bands over {world} GPU(s) with recomputed halo "
+                                       f"(rank 0: out rows {shard.out_row0}+{shard.out_rows}, "
+                                       f"in rows {shard.in_row0}+{shard.in_rows}), no collective"),
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,
             "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
@@ -393,8 +421,8 @@ def main():
             "kernel_ms_per_step": breakdown,
             "kernel_sum_ms_per_step": step_kernel_ms,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_val, "unit": "MP/s", "h2d_bytes_per_step": io_bytes,
-                    "d2h_bytes_per_step": io_bytes, "ms_per_step": float(e2e_t.item())},
+            "e2e": {"value": e2e_val, "unit": "MP/s", "h2d_bytes_per_step": io_in,
+                    "d2h_bytes_per_step": io_out, "ms_per_step": e2e_t},
             "gpu_launches": args.steps * h.launch_count(n_local, H, W) * world,
             "clocks": clocks,
         }

@@ -134,6 +134,11 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
 blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32_t out_rows,
                                 int32_t* in_row0, int32_t* in_rows);
 
+/* The same halo query from a configuration alone (host-only, no device, no handle): used to plan
+ * the row bands of a multi-GPU split (BASELINE.json configs[4]) before any device is touched. */
+blade_status blade_ms_band_plan(const blade_ms_config* cfg, int32_t H, int32_t out_row0,
+                                int32_t out_rows, int32_t* in_row0, int32_t* in_rows);
+
 /* Workspace bytes for a band call (depends on the band's input extent). */
 blade_status blade_ms_band_workspace_size(blade_ms_t h, int32_t H, int32_t W, int32_t out_row0,
                                           int32_t out_rows, size_t* bytes);

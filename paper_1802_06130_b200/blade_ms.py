@@ -50,7 +50,7 @@ class _Info(ctypes.Structure):
 
 
 EXPORTS = ["blade_ms_create", "blade_ms_workspace_size", "blade_ms_denoise", "blade_ms_denoise_host",
-           "blade_ms_band_rows", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
+           "blade_ms_band_rows", "blade_ms_band_plan", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
            "blade_ms_selector", "blade_ms_pyramid", "blade_ms_get_info", "blade_ms_launch_count",
            "blade_ms_set_profiling", "blade_ms_profile_read",
            "blade_ms_destroy", "blade_ms_status_string", "blade_ms_last_error"]
@@ -82,6 +82,8 @@ def lib():
     L.blade_ms_denoise.argtypes = [P, P, P, i32, i32, i32, P, sz, P]
     L.blade_ms_denoise_host.argtypes = [P, P, P, i32, i32, i32, P, P, P, sz, P]
     L.blade_ms_band_rows.argtypes = [P, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.blade_ms_band_plan.argtypes = [ctypes.POINTER(_Config), i32, i32, i32, ctypes.POINTER(i32),
+                                     ctypes.POINTER(i32)]
     L.blade_ms_band_workspace_size.argtypes = [P, i32, i32, i32, i32, ctypes.POINTER(sz)]
     L.blade_ms_denoise_rows.argtypes = [P, P, i32, i32, P, i32, i32, i32, i32, P, sz, P]
     L.blade_ms_selector.argtypes = [P, P, i32, i32, i32, P, P, sz, P]
@@ -114,6 +116,17 @@ def _stream_ptr(stream) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
     return stream.cuda_stream
+
+
+def band_plan(levels: int, fine_size: int, coarse_size: int, window_size: int, H: int,
+              out_row0: int, out_rows: int) -> tuple[int, int]:
+    """blade_ms_band_plan: input rows (in_row0, in_rows) a row band needs (host only, no device)."""
+    cfg = _Config(levels, fine_size, coarse_size if levels > 1 else 0, 4 if levels > 1 else 1, 1,
+                  window_size, 1.5, 0)
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().blade_ms_band_plan(ctypes.byref(cfg), H, out_row0, out_rows, ctypes.byref(a),
+                                    ctypes.byref(b)))
+    return a.value, b.value
 
 
 class BladeMS:

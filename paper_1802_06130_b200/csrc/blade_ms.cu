@@ -233,8 +233,12 @@ struct Plan {
 };
 
 // Dependency cone of output rows [o0, o0+on) of the final output.
+void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int on, Plan& p);
 void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) {
-  const int L = h->cfg.levels;
+  plan_rows_cfg(h->cfg, N, H, W, o0, on, p);
+}
+void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int on, Plan& p) {
+  const int L = cfg.levels;
   p.L = L;
   p.N = N;
   p.H.assign(L, 0);
@@ -247,9 +251,9 @@ void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) 
   }
   p.z.assign(L, Range{});
   p.u.assign(L, Range{});
-  const int rf = h->cfg.fine_size / 2;
-  const int rc = h->cfg.coarse_size / 2;
-  const int ext = std::max(rf, h->cfg.window_size / 2 + 1);
+  const int rf = cfg.fine_size / 2;
+  const int rc = cfg.coarse_size / 2;
+  const int ext = std::max(rf, cfg.window_size / 2 + 1);
   p.u[0] = Range{o0, o0 + on};
   if (L == 1) {
     p.z[0] = fold_hull((long long)o0 - ext, (long long)o0 + on + ext, H);
@@ -918,6 +922,22 @@ blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32
     return fail(BLADE_EINVAL, "bad band [%d, %d) of H = %d", out_row0, out_row0 + out_rows, H);
   Plan p;
   plan_rows(h, 1, H, 1, out_row0, out_rows, p);
+  *in_row0 = p.z[0].lo;
+  *in_rows = p.z[0].n();
+  return BLADE_OK;
+}
+
+blade_status blade_ms_band_plan(const blade_ms_config* cfg, int32_t H, int32_t out_row0, int32_t out_rows,
+                                int32_t* in_row0, int32_t* in_rows) {
+  if (!cfg || !in_row0 || !in_rows) return fail(BLADE_EINVAL, "NULL argument");
+  if (cfg->levels < 1 || cfg->levels > 12 || cfg->fine_size < 1 || cfg->fine_size > 9 || !(cfg->fine_size & 1) ||
+      (cfg->levels > 1 && (cfg->coarse_size < 1 || cfg->coarse_size > 9 || !(cfg->coarse_size & 1))) ||
+      cfg->window_size < 1 || cfg->window_size > 5 || !(cfg->window_size & 1))
+    return fail(BLADE_EINVAL, "bad config");
+  if (H < 1 || out_row0 < 0 || out_rows < 1 || out_row0 + out_rows > H)
+    return fail(BLADE_EINVAL, "bad band [%d, %d) of H = %d", out_row0, out_row0 + out_rows, H);
+  Plan p;
+  plan_rows_cfg(*cfg, 1, H, 1, out_row0, out_rows, p);
   *in_row0 = p.z[0].lo;
   *in_rows = p.z[0].n();
   return BLADE_OK;

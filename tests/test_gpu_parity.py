@@ -204,3 +204,21 @@ def test_clamp_output_flag():
     raw = _handle(cfg).denoise(x)
     cl = _handle(cfg, clamp_output=True).denoise(x)
     assert torch.equal(cl, raw.clamp(0, 1))
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shard_bands_equal_full_image(world):
+    """The multi-GPU band split of bench.py (paper_1802_06130_b200.shard, configs[4] recipe at a
+    reduced size), run band by band on one device: bit-identical to the whole-image call."""
+    from paper_1802_06130_b200.shard import shard_for
+    cfg = _cfg_like("c4", 900, 260, 1)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    full = h.denoise(x)[0]
+    parts = []
+    for r in range(world):
+        s = shard_for(cfg, r, world)
+        assert s.mode == "bands"
+        band_in = x[0, :, s.in_row0:s.in_row0 + s.in_rows].contiguous()
+        parts.append(h.denoise_rows(band_in, s.in_row0, s.out_row0, s.out_rows, cfg.H))
+    assert torch.equal(torch.cat(parts, 1), full)
