@@ -99,7 +99,7 @@ using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
 struct TmaVariant {
   int nf, nc, groups;
   TmaKernel fn;
-  int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc;
+  int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc, S;
 };
 #ifndef BLADE_TMA_GROUPS
 #define BLADE_TMA_GROUPS 2
@@ -108,7 +108,7 @@ template <int NF, int NC, int G = BLADE_TMA_GROUPS>
 TmaVariant make_tma() {
   using SS = TmaShape<NF, NC>;
   return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC};
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S};
 }
 // TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
 const std::vector<TmaVariant>& tma_variants() {
@@ -201,9 +201,11 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 struct blade_ms {
   blade_ms_config cfg;
   int n_o, n_s, n_c, K;
-  int n_stages, nt, S, PS;
+  int n_stages, nt, S, PS;    // generic stage kernel bank: tap stride (odd), phase stride
+  int S_tma = 0, PS_tma = 0;  // TMA stage kernel bank (tma_tap_off layout)
   int device, num_sms;
-  float* d_bank = nullptr;  // [stage][phase][PS]
+  float* d_bank = nullptr;      // [stage][phase][PS], taps in ABI order per filter (k_stage)
+  float* d_bank_tma = nullptr;  // [stage][phase][PS_tma], tma_tap_off layout (k_stage_tma)
   size_t bank_bytes = 0;
   std::vector<DownParams> down;  // per stage (selector level)
   // generic stage kernel
@@ -493,10 +495,10 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       a.out = outv.p;
       a.out_row0 = outv.row0;
       a.out_rows = outv.rows;
-      a.bank = bank;
+      a.bank = h->d_bank_tma + (size_t)l * h->cfg.n_phases * h->PS_tma;
       a.K = h->K;
-      a.S = h->S;
-      a.PS = h->PS;
+      a.S = h->S_tma;
+      a.PS = h->PS_tma;
       a.n_phases = h->cfg.n_phases;
       a.N = N;
       a.y_base = y_base;
@@ -669,12 +671,15 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->stage_smem = best_smem;
   for (const auto& v : tma_variants()) {
     if (v.nf != c.fine_size || v.nc != cnc) continue;
-    const size_t bank = ((size_t)c.n_phases * PS * 4 + 127) & ~size_t(127);
+    const size_t tps = (size_t)K * v.S;  // phase stride of the TMA tap layout (multiple of 4)
+    const size_t bank = ((size_t)c.n_phases * tps * 4 + 127) & ~size_t(127);
     const size_t smem = 2 * (size_t)v.stage_bytes + bank + 16;
     if (smem <= (size_t)max_smem && get_encode()) {
       h->has_tma = true;
       h->tma = v;
       h->tma_smem = smem;
+      h->S_tma = v.S;
+      h->PS_tma = (int)tps;
     }
   }
 
@@ -717,22 +722,42 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   }
 
   // ---- bank re-layout: host [stage][ch=1][phase][K][nt] -> device [stage][phase][PS]
+  // generic kernel: [K][S] rows, taps in ABI order; TMA kernel: tma_tap_off layout
   const size_t dev_floats = (size_t)n_stages * c.n_phases * PS;
-  std::vector<float> relaid(dev_floats, 0.0f);
+  const size_t tma_floats = (size_t)n_stages * c.n_phases * h->PS_tma;
+  std::vector<float> relaid(dev_floats, 0.0f), relaid_tma(tma_floats, 0.0f);
   for (int s = 0; s < n_stages; ++s)
     for (int p = 0; p < c.n_phases; ++p)
       for (long long k = 0; k < K; ++k) {
         const float* src = taps + (((size_t)s * c.n_phases + p) * K + k) * nt;
         float* dst = relaid.data() + ((size_t)s * c.n_phases + p) * PS + (size_t)k * S;
         memcpy(dst, src, sizeof(float) * nt);
+        if (!h->has_tma) continue;
+        float* dt = relaid_tma.data() + ((size_t)s * c.n_phases + p) * h->PS_tma + (size_t)k * h->S_tma;
+        for (int dy = 0; dy < c.fine_size; ++dy)
+          for (int dx = 0; dx < c.fine_size; ++dx)
+            dt[tma_tap_off(c.fine_size, cnc, 0, dy, dx)] = src[dy * c.fine_size + dx];
+        for (int dy = 0; dy < cnc; ++dy)
+          for (int dx = 0; dx < cnc; ++dx)
+            dt[tma_tap_off(c.fine_size, cnc, 1, dy, dx)] = src[c.fine_size * c.fine_size + dy * cnc + dx];
       }
-  h->bank_bytes = sizeof(float) * dev_floats;
-  if (cudaMalloc(&h->d_bank, h->bank_bytes) != cudaSuccess) {
+  h->bank_bytes = sizeof(float) * (dev_floats + tma_floats);
+  if (cudaMalloc(&h->d_bank, sizeof(float) * dev_floats) != cudaSuccess ||
+      (h->has_tma && cudaMalloc(&h->d_bank_tma, sizeof(float) * tma_floats) != cudaSuccess)) {
     cudaGetLastError();
+    cudaFree(h->d_bank);
     delete h;
-    return fail(BLADE_ENOMEM, "cudaMalloc(%zu) for the bank failed", dev_floats * sizeof(float));
+    return fail(BLADE_ENOMEM, "cudaMalloc for the bank failed");
   }
-  cudaError_t ce = cudaMemcpy(h->d_bank, relaid.data(), h->bank_bytes, cudaMemcpyHostToDevice);
+  if (h->has_tma &&
+      cudaMemcpy(h->d_bank_tma, relaid_tma.data(), sizeof(float) * tma_floats, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(h->d_bank);
+    cudaFree(h->d_bank_tma);
+    delete h;
+    return fail(BLADE_ECUDA, "bank upload failed");
+  }
+  cudaError_t ce = cudaMemcpy(h->d_bank, relaid.data(), sizeof(float) * dev_floats, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess)
     ce = cudaFuncSetAttribute(h->stage.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->stage_smem);
   if (ce == cudaSuccess && h->has_tma)
@@ -749,6 +774,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->stage.fn, h->stage.threads, h->stage_smem);
   if (ce != cudaSuccess || occ < 1) {
     cudaFree(h->d_bank);
+    cudaFree(h->d_bank_tma);
     delete h;
     return fail(BLADE_ECUDA, "kernel setup failed: %s (occupancy %d)", cudaGetErrorString(ce), occ);
   }
@@ -795,6 +821,7 @@ blade_status blade_ms_destroy(blade_ms_t h) {
   }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
   cudaFree(h->d_bank);
+  cudaFree(h->d_bank_tma);
   delete h;
   return BLADE_OK;
 }

@@ -80,20 +80,56 @@ __device__ __forceinline__ void lds_run(const float* p, float* v) {
   lds_run_at<A, 0, N, MAXV>(p, v);
 }
 
+// Tap layout of one (phase, bucket) filter for this kernel (LDS.128-friendly): for every row of
+// the fine block (NF x NF) and then of the coarse block (NC x NC), the first 4 floor(n / 4) taps as
+// float4 chunks; after all chunks, the remaining n % 4 taps of every row. The filter stride S is
+// rounded up to a multiple of 4 floats with S / 4 odd (spreads the per-pixel 16-B tap loads over
+// the 8 bank groups). Used by the host re-layout (blade_ms_create) and, with compile-time
+// arguments, by the kernel.
+__host__ __device__ constexpr int tma_tap_off(int nf, int nc, int block, int dy, int dx) {
+  const int qf = nf / 4, qc = nc / 4, vec = 4 * (nf * qf + nc * qc);
+  if (block == 0)
+    return dx < 4 * qf ? 4 * (dy * qf + dx / 4) + dx % 4 : vec + dy * (nf % 4) + (dx - 4 * qf);
+  return dx < 4 * qc ? 4 * (nf * qf + dy * qc + dx / 4) + dx % 4
+                     : vec + nf * (nf % 4) + dy * (nc % 4) + (dx - 4 * qc);
+}
+__host__ __device__ constexpr int tma_tap_stride(int nf, int nc) {
+  const int r = (nf * nf + nc * nc + 3) & ~3;
+  return ((r / 4) & 1) ? r : r + 4;
+}
+
+// Loads the NB taps of row dy of `block` of the filter at tp (16-B aligned) into t[0..NB).
+template <int NF, int NC, int BLOCK>
+__device__ __forceinline__ void load_tap_row(const float* tp, int dy, float* t) {
+  constexpr int NB = BLOCK == 0 ? NF : NC;
+#pragma unroll
+  for (int q = 0; q < NB / 4; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(tp + tma_tap_off(NF, NC, BLOCK, dy, 4 * q));
+    t[4 * q] = v.x;
+    t[4 * q + 1] = v.y;
+    t[4 * q + 2] = v.z;
+    t[4 * q + 3] = v.w;
+  }
+#pragma unroll
+  for (int k = 4 * (NB / 4); k < NB; ++k) t[k] = tp[tma_tap_off(NF, NC, BLOCK, dy, k)];
+}
+
 template <int NF, int NC>
 struct TmaShape {
   static constexpr int RX = 4, RY = 2, BX = 32, BY = 8;
   static constexpr int threads = BX * BY;
   static constexpr int RF = NF / 2, RC = NC / 2;
   static constexpr int TCOLS = BX * RX, TROWS = BY * RY;  // 128 x 16 outputs per tile
-  // TMA boxes must start on a 16-byte boundary in the innermost dimension: both boxes start 4
-  // columns left of the tile (covers halos up to 4) and the windows start at FO / CO inside.
-  static constexpr int MARGIN = 4;
-  static constexpr int FO = MARGIN - RF, CO = MARGIN - RC;
+  // TMA box starts must be 16-B aligned in the innermost dimension (a box at column 2 faults with
+  // an illegal instruction: scripts/probes/tma_probe.cu), so both boxes start 4 columns left of
+  // the tile (covers halos up to 4) and the windows start at FO / CO inside.
+  static constexpr int FM = 4, CM = 4;
+  static constexpr int FO = FM - RF, CO = CM - RC;
   static constexpr int FR = TROWS + 2 * RF;
-  static constexpr int FCB = TCOLS + 2 * MARGIN;            // 136
+  static constexpr int FCB = TCOLS + 2 * FM;            // 136
   static constexpr int CR = NC ? TROWS / 2 + 2 * RC : 0;
-  static constexpr int CCB = NC ? TCOLS / 2 + 2 * MARGIN : 0;  // 72
+  static constexpr int CCB = NC ? TCOLS / 2 + 2 * CM : 0;  // 72
+  static_assert(RF <= FM && RC <= CM, "halo wider than the TMA margin");
   static constexpr int fine_bytes = 3 * FR * FCB * 4;
   static constexpr int coarse_bytes = 3 * CR * CCB * 4;
   static constexpr int map_bytes = TROWS * TCOLS;
@@ -104,7 +140,7 @@ struct TmaShape {
   static constexpr int stage_bytes = map_off + al(map_bytes);
   static constexpr int FWIN = NF + RX - 1;  // fine window columns per thread
   static constexpr int CWIN = NC + 1;       // coarse window columns per thread
-  static_assert(RF <= MARGIN && RC <= MARGIN, "halo wider than the TMA margin");
+  static constexpr int S = tma_tap_stride(NF, NC);
 };
 
 struct StageTmaArgs {
@@ -166,9 +202,9 @@ __global__ void __launch_bounds__(256 * G, 1)
     tile_coords(t, n, X0, Y0);
     unsigned char* sb = buf0 + b * SS::stage_bytes;
     mbar_expect_tx(&mbar[b], tx_bytes);
-    tma_load_3d(sb + SS::fine_off, &tm_z, X0 - SS::MARGIN, Y0 - RF - a.z_row0, n * 3, &mbar[b]);
+    tma_load_3d(sb + SS::fine_off, &tm_z, X0 - SS::FM, Y0 - RF - a.z_row0, n * 3, &mbar[b]);
     if constexpr (NC > 0)
-      tma_load_3d(sb + SS::coarse_off, &tm_u, X0 / 2 - SS::MARGIN, Y0 / 2 - RC - a.u_row0, n * 3, &mbar[b]);
+      tma_load_3d(sb + SS::coarse_off, &tm_u, X0 / 2 - SS::CM, Y0 / 2 - RC - a.u_row0, n * 3, &mbar[b]);
     tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[b]);
   };
 
@@ -205,7 +241,7 @@ __global__ void __launch_bounds__(256 * G, 1)
     const uint8_t* smap = buf0 + b * SS::stage_bytes + SS::map_off;
 
     // ---- border fix-up: out-of-image cells <- folded samples
-    const int FX = X0 - SS::MARGIN, CX = X0 / 2 - SS::MARGIN;  // box origins (columns)
+    const int FX = X0 - SS::FM, CX = X0 / 2 - SS::CM;  // box origins (columns)
     const bool fine_border = FX < 0 || FX + SS::FCB > a.W || Y0 - RF < 0 || Y0 + SS::TROWS + RF > a.H;
     const bool coarse_border = NC > 0 && (CX < 0 || CX + SS::CCB > a.W1 || Y0 / 2 - RC < 0 ||
                                           Y0 / 2 - RC + SS::CR > a.H1);
@@ -269,8 +305,8 @@ __global__ void __launch_bounds__(256 * G, 1)
       const int k0 = (mrow0 >> (8 * j)) & 0xff, k1 = (mrow1 >> (8 * j)) & 0xff;
       const int ph0 = a.n_phases == 4 ? (j & 1) : 0;
       const int ph1 = a.n_phases == 4 ? 2 + (j & 1) : 0;
-      tp[0][j] = sbank + ph0 * a.PS + k0 * a.S;
-      tp[1][j] = sbank + ph1 * a.PS + k1 * a.S;
+      tp[0][j] = sbank + ph0 * a.PS + k0 * SS::S;
+      tp[1][j] = sbank + ph1 * a.PS + k1 * SS::S;
     }
     float acc[2][4][3];
 #pragma unroll
@@ -291,13 +327,15 @@ __global__ void __launch_bounds__(256 * G, 1)
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
+          for (int j = 0; j < 4; ++j) {
+            float t[NC > 0 ? NC : 1];
+            load_tap_row<NF, NC, 1>(tp[i][j], wr, t);
 #pragma unroll
             for (int dx = 0; dx < NC; ++dx) {
-              const float tap = tp[i][j][NF * NF + wr * NC + dx];
 #pragma unroll
-              for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][(j >> 1) + dx], acc[i][j][c]);
+              for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][(j >> 1) + dx], acc[i][j][c]);
             }
+          }
       }
     }
     // fine rows local 2ty .. 2ty+NF (NF+1 rows), cols 4tx .. 4tx+NF+2
@@ -312,13 +350,15 @@ __global__ void __launch_bounds__(256 * G, 1)
         const int dy = wr - i;
         if (dy < 0 || dy >= NF) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j) {
+          float t[NF];
+          load_tap_row<NF, NC, 0>(tp[i][j], dy, t);
 #pragma unroll
           for (int dx = 0; dx < NF; ++dx) {
-            const float tap = tp[i][j][dy * NF + dx];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][j + dx], acc[i][j][c]);
+            for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][j + dx], acc[i][j][c]);
           }
+        }
       }
     }
 
