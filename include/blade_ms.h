@@ -134,6 +134,12 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
 blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32_t out_rows,
                                 int32_t* in_row0, int32_t* in_rows);
 
+/* Diagnostic (synchronous): after a blade_ms_denoise / _selector call of N x H x W frames with
+ * workspace ws has completed, counts[l] (l < n_stages) = the number of pixels of selector level l
+ * whose fp32 orientation bin was not certified and was recomputed in fp64 (DESIGN.md §6 H1). */
+blade_status blade_ms_fallback_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, const void* ws,
+                                     size_t ws_bytes, uint32_t* counts);
+
 /* The same halo query from a configuration alone (host-only, no device, no handle): used to plan
  * the row bands of a multi-GPU split (BASELINE.json configs[4]) before any device is touched. */
 blade_status blade_ms_band_plan(const blade_ms_config* cfg, int32_t H, int32_t out_row0,

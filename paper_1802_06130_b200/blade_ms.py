@@ -50,7 +50,7 @@ class _Info(ctypes.Structure):
 
 
 EXPORTS = ["blade_ms_create", "blade_ms_workspace_size", "blade_ms_denoise", "blade_ms_denoise_host",
-           "blade_ms_band_rows", "blade_ms_band_plan", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
+           "blade_ms_band_rows", "blade_ms_band_plan", "blade_ms_fallback_count", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
            "blade_ms_selector", "blade_ms_pyramid", "blade_ms_get_info", "blade_ms_launch_count",
            "blade_ms_set_profiling", "blade_ms_profile_read",
            "blade_ms_destroy", "blade_ms_status_string", "blade_ms_last_error"]
@@ -84,6 +84,7 @@ def lib():
     L.blade_ms_band_rows.argtypes = [P, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.blade_ms_band_plan.argtypes = [ctypes.POINTER(_Config), i32, i32, i32, ctypes.POINTER(i32),
                                      ctypes.POINTER(i32)]
+    L.blade_ms_fallback_count.argtypes = [P, i32, i32, i32, P, sz, P]
     L.blade_ms_band_workspace_size.argtypes = [P, i32, i32, i32, i32, ctypes.POINTER(sz)]
     L.blade_ms_denoise_rows.argtypes = [P, P, i32, i32, P, i32, i32, i32, i32, P, sz, P]
     L.blade_ms_selector.argtypes = [P, P, i32, i32, i32, P, P, sz, P]
@@ -189,6 +190,15 @@ class BladeMS:
         c = ctypes.c_int32()
         _check(lib().blade_ms_launch_count(self._h, N, H, W, ctypes.byref(c)))
         return c.value
+
+    def fallback_count(self, N: int, H: int, W: int, workspace: torch.Tensor) -> list[int]:
+        """Uncertified (fp64-recomputed) selector pixels per level of the last call that used
+        `workspace` (synchronises)."""
+        torch.cuda.synchronize(workspace.device)
+        c = np.zeros(16, np.uint32)
+        _check(lib().blade_ms_fallback_count(self._h, N, H, W, _ptr(workspace), workspace.numel(),
+                                             c.ctypes.data))
+        return [int(v) for v in c[:self.n_stages]]
 
     def set_profiling(self, enable: bool):
         _check(lib().blade_ms_set_profiling(self._h, int(enable)))

@@ -231,7 +231,9 @@ struct Plan {
   std::vector<Range> z;  // rows of z^l materialised (level 0: needed input rows)
   std::vector<Range> u;  // rows of u^l computed (= map rows), l <= L-2 (l = 0 if L == 1)
   size_t ws_bytes = 0;
-  std::vector<size_t> z32_off, zlo_off, u_off, map_off;
+  std::vector<size_t> z32_off, zlo_off, u_off, map_off, fb_off;
+  std::vector<unsigned int> fb_cap;
+  size_t fbcnt_off = 0;
 };
 
 // Dependency cone of output rows [o0, o0+on) of the final output.
@@ -295,6 +297,17 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
     p.map_off[l] = off;
     off = align256(off + (size_t)N * p.u[l].n() * p.W[l]);
   }
+  // uncertified-pixel lists of the fp32 selector (DESIGN.md §6 H1): 1/64 of each level's map
+  p.fb_off.assign(nsel, 0);
+  p.fb_cap.assign(nsel, 0);
+  for (int l = 0; l < nsel; ++l) {
+    const size_t px = (size_t)N * p.u[l].n() * p.W[l];
+    p.fb_cap[l] = (unsigned int)std::min<size_t>(std::max<size_t>(px / 64, 1024), 0x7fffffffu);
+    p.fb_off[l] = off;
+    off = align256(off + sizeof(unsigned long long) * p.fb_cap[l]);
+  }
+  p.fbcnt_off = off;
+  off = align256(off + sizeof(unsigned int) * 16);
   p.ws_bytes = std::max<size_t>(off, 256);
 }
 
@@ -399,7 +412,10 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   for (int l = 0; l < nsel; ++l)
     maps[l] = (maps_out && maps_out[l]) ? maps_out[l] : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
 
-  // ---- down pass: k_down(l) -> s^l, z^{l+1} (hi, and lo when level l+1 feeds a selector)
+  // ---- down pass: k_down(l) -> s^l, z^{l+1} (hi, and lo when level l+1 feeds a selector);
+  //      k_down_fixup(l) recomputes the (rare) pixels whose fp32 orientation is uncertified
+  unsigned int* fb_cnt = reinterpret_cast<unsigned int*>(ws + p.fbcnt_off);
+  CUDA_TRY(cudaMemsetAsync(fb_cnt, 0, sizeof(unsigned int) * nsel, st));
   for (int l = 0; l < nsel; ++l) {
     const Range U = p.u[l];
     const bool dec = L > 1;
@@ -437,12 +453,21 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.RB = RB;
     da.n_bands = (span + RB - 1) / RB;
     da.n_tasks = (int)(col_tasks * da.n_bands);
+    da.fb_list = reinterpret_cast<unsigned long long*>(ws + p.fb_off[l]);
+    da.fb_count = fb_cnt + l;
+    da.fb_cap = p.fb_cap[l];
+    da.N = N;
     ProfScope ps(h, st, 1, l);
     const bool hilo = l > 0;
-    auto fn = down_kernel(hilo, dec, h->n_o == 16 && h->n_s <= 3 && h->n_c <= 3);
+    const bool fast = h->n_o == 16 && h->n_s <= 3 && h->n_c <= 3;
+    auto fn = down_kernel(hilo, dec, fast);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     fn<<<grid, 32 * down::WARPS, down_smem(hilo), st>>>(da, h->down[l]);
     LAUNCH_CHECK("k_down");
+    auto fx = hilo ? (fast ? &k_down_fixup<true, true> : &k_down_fixup<true, false>)
+                   : (fast ? &k_down_fixup<false, true> : &k_down_fixup<false, false>);
+    fx<<<4 * h->num_sms, 128, 0, st>>>(da, h->down[l]);
+    LAUNCH_CHECK("k_down_fixup");
   }
   if (!run_stages) return BLADE_OK;
 
@@ -863,7 +888,7 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
   (void)H;
   (void)W;
   const int L = h->cfg.levels;
-  *count = N == 0 ? 0 : 2 * (L == 1 ? 1 : L - 1);
+  *count = N == 0 ? 0 : 3 * (L == 1 ? 1 : L - 1);  // k_down + k_down_fixup + k_stage per stage level
   return BLADE_OK;
 }
 
@@ -951,6 +976,19 @@ blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32
   plan_rows(h, 1, H, 1, out_row0, out_rows, p);
   *in_row0 = p.z[0].lo;
   *in_rows = p.z[0].n();
+  return BLADE_OK;
+}
+
+blade_status blade_ms_fallback_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, const void* ws,
+                                     size_t ws_bytes, uint32_t* counts) {
+  if (!h || !ws || !counts) return fail(BLADE_EINVAL, "NULL argument");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  Plan p;
+  plan_rows(h, N, H, W, 0, H, p);
+  if (ws_bytes < p.ws_bytes) return fail(BLADE_ESHAPE, "workspace too small");
+  DeviceGuard guard(h->device);
+  CUDA_TRY(cudaMemcpy(counts, (const char*)ws + p.fbcnt_off, sizeof(uint32_t) * h->n_stages, cudaMemcpyDeviceToHost));
   return BLADE_OK;
 }
 

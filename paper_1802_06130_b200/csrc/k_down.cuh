@@ -61,6 +61,10 @@ struct DownArgs {
   float* olo;        // z^{l+1} lo (nullptr: not needed, l + 1 is the coarsest level)
   int H1, W1, d_buf_row0, d_buf_rows, d_r0, d_rn;
   int base, RB, n_strips, n_bands, n_tasks;
+  unsigned long long* fb_list;  // uncertified map entries (flat index into map), capacity fb_cap
+  unsigned int* fb_count;       // zeroed before the launch; may exceed fb_cap (overflow)
+  unsigned int fb_cap;
+  int N;                        // frames of the launch
 };
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
@@ -147,6 +151,125 @@ __device__ __forceinline__ int bucket_of(double a, double b, double c, const Dow
   return (o * prm.n_s + s) * prm.n_c + k;
 }
 
+// ---- fp32 selector with a certificate (DESIGN.md §6 H1)
+//
+// The window sums a = sum w gx^2, b = sum w gx gy, c = sum w gy^2 (unscaled gradients 2g, fp32 from
+// exact fp32 inputs or from the hi/lo pyramid) carry absolute errors |da|, |dc| <= ~11 u T and
+// |db| <= ~8 u T (T = a + c, u = 2^-24: every product and weight is rounded once, all sums of
+// a and c have positive terms, |gx gy| <= (gx^2 + gy^2) / 2). So X = c - a and Y = -2b, whose angle
+// psi decides the orientation bin, are each off by <= 16 u T, and every sign test below (the
+// quadrant signs of X, Y and the cross products with the bin edges, |v| <= T) is off by at most
+// 32 u T. A test whose |value| exceeds kCert T = 64 u T therefore has the sign of the exact test;
+// a pixel with any closer test is recomputed in fp64 (abc_fp64). Strength and coherence are
+// well-conditioned: their fp32 errors (~1e-6 relative) stay far inside the 1e-5 parity window.
+constexpr float kCert = 64.0f * 5.9604644775390625e-8f;
+
+template <bool FAST>
+__device__ __forceinline__ int bucket32(float a, float b, float c, const DownParams& prm, bool& safe) {
+  constexpr int MAXT = FAST ? 2 : kMaxThr2;
+  const float T = a + c;
+  const float Df = a - c;
+  const float h = 0.125f * T;                                    // unscaled x4 -> T/2
+  const float q = 0.0625f * fmaf(0.25f * Df, Df, b * b);         // r^2
+  const float bound = kCert * T;
+  int o = 0;
+  if (!(Df == 0.0f && b == 0.0f)) {
+    const float X = -Df, Y = -2.0f * b;
+    float mn = fminf(fabsf(X), fabsf(Y));
+    if (FAST || prm.quad_edges) {
+      int qd;
+      float xr, yr;
+      if (X > 0.0f && Y >= 0.0f) { qd = 0; xr = X; yr = Y; }
+      else if (X <= 0.0f && Y > 0.0f) { qd = 1; xr = Y; yr = -X; }
+      else if (X < 0.0f && Y <= 0.0f) { qd = 2; xr = -X; yr = -Y; }
+      else { qd = 3; xr = -Y; yr = X; }
+      if constexpr (FAST) {
+        constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f;  // pi/8
+        constexpr float c2 = 0.70710678118654752f;                              // pi/4
+        const float e1 = fmaf(c1, yr, -s1 * xr), e2 = fmaf(c2, yr, -c2 * xr), e3 = fmaf(s1, yr, -c1 * xr);
+        o = 4 * qd + (e1 >= 0.0f) + (e2 >= 0.0f) + (e3 >= 0.0f);
+        mn = fminf(mn, fminf(fabsf(e1), fminf(fabsf(e2), fabsf(e3))));
+      } else {
+        const int m = prm.n_o >> 2;
+        o = qd * m;
+        for (int j = 0; j < m - 1; ++j) {
+          const float e = fmaf(prm.ecos[j], yr, -prm.esin[j] * xr);
+          o += (e >= 0.0f);
+          mn = fminf(mn, fabsf(e));
+        }
+      }
+    } else {
+      // generic n_o: atan2f (~2 ulp) and the distance to the nearest edge in psi
+      const float kTwoPiInv = 0.15915494309189535f;
+      const float phi = atan2f(-Y, -X);  // = atan2(2b, a - c)
+      const float f = fmaf(phi, (float)prm.n_o * kTwoPiInv, 0.5f * (float)prm.n_o);
+      o = (int)floorf(f);
+      const float fr = f - floorf(f);
+      const float dist = fminf(fr, 1.0f - fr) * 6.283185307179586f / (float)prm.n_o;  // radians in psi
+      mn = fminf(mn, (dist - 2e-6f) * sqrtf(fmaf(X, X, Y * Y)));
+      o %= prm.n_o;
+      if (o < 0) o += prm.n_o;
+    }
+    safe = mn > bound;
+  } else {
+    safe = !(T > 0.0f);  // all gradients exactly zero => theta = 0 exactly [R5]
+  }
+  int s = 0;
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    if (!FAST && t >= prm.n_s - 1) break;
+    const float d = prm.ts2[t] - h;
+    s += (d <= 0.0f) || (q >= d * d);
+  }
+  int k = prm.tc_nonpos;
+  if (h > 0.0f) {
+    const float h2 = h * h;
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      if (!FAST && t >= prm.n_c - 1) break;
+      k += (q >= prm.kc2[t] * h2);
+    }
+  }
+  return (o * prm.n_s + s) * prm.n_c + k;
+}
+
+// fp64 recomputation of (a, b, c) at one pixel (unscaled gradients, fp64 sums, the exact fp64
+// level from hi + lo). Unused by the fix-up kernel (which spreads the window over a warp); kept as
+// the plain single-thread reference of the same sums.
+template <bool HILO>
+__device__ __forceinline__ void abc_fp64(const DownArgs& a, const DownParams& prm, int n, int xp, int yp,
+                                      double& A, double& B, double& C) {
+  auto Z = [&](int c, int y, int x) -> double {
+    int br = fold_idx(y, a.H) - a.in_row0;
+    br = min(max(br, 0), a.in_rows - 1);
+    const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.W + fold_idx(x, a.W);
+    double v = (double)a.zhi[o];
+    if constexpr (HILO) v += (double)a.zlo[o];
+    return v;
+  };
+  A = B = C = 0.0;
+  for (int dy = -2; dy <= 2; ++dy) {
+    double ra = 0.0, rb = 0.0, rc = 0.0;
+    for (int dx = -2; dx <= 2; ++dx) {
+      const int y = yp + dy, x = xp + dx;
+      double pa = 0.0, pb = 0.0, pc = 0.0;
+      for (int c = 0; c < 3; ++c) {
+        const double gx = Z(c, y, x + 1) - Z(c, y, x - 1);
+        const double gy = Z(c, y + 1, x) - Z(c, y - 1, x);
+        pa = fma(gx, gx, pa);
+        pb = fma(gx, gy, pb);
+        pc = fma(gy, gy, pc);
+      }
+      ra = fma(prm.wp[dx + 2], pa, ra);
+      rb = fma(prm.wp[dx + 2], pb, rb);
+      rc = fma(prm.wp[dx + 2], pc, rc);
+    }
+    A = fma(prm.wp[dy + 2], ra, A);
+    B = fma(prm.wp[dy + 2], rb, B);
+    C = fma(prm.wp[dy + 2], rc, C);
+  }
+}
+
 // grid: ceil(n_tasks / WARPS) CTAs of 32 * WARPS threads; task = (frame, band, strip), strip fastest.
 template <bool HILO, bool DEC, bool FAST>
 __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, const DownParams prm) {
@@ -173,6 +296,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
   // one 8-byte copy when the two columns are adjacent in memory and 8-B aligned (interior, W even)
   const bool pair8 = fx1 == fx0 + 1 && ((fx0 | a.W | (int)(a.in_plane & 1)) & 1) == 0 &&
                      ((reinterpret_cast<uintptr_t>(a.zhi) | reinterpret_cast<uintptr_t>(HILO ? a.zlo : a.zhi)) & 7) == 0;
+  const bool all_pair8 = __all_sync(0xffffffffu, pair8);
 
   auto issue = [&](int i) {
     const int r = Yb - 3 + i;
@@ -180,20 +304,20 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
     br = min(max(br, 0), a.in_rows - 1);
     float* dst = ring + (i % RING) * NP * 64;
     const long long ro = (long long)br * a.W;
+    if (all_pair8) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float* s = hbase + c * a.in_plane + ro;
-      if (pair8) {
-        cp_async8(dst + c * 64, s + fx0);
-      } else {
+      for (int c = 0; c < 3; ++c) {
+        cp_async8(dst + c * 64, hbase + c * a.in_plane + ro + fx0);
+        if constexpr (HILO) cp_async8(dst + (3 + c) * 64, lbase + c * a.in_plane + ro + fx0);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float* s = hbase + c * a.in_plane + ro;
         cp_async4(dst + c * 64, s + fx0);
         cp_async4(dst + c * 64 + 1, s + fx1);
-      }
-      if constexpr (HILO) {
-        const float* sl = lbase + c * a.in_plane + ro;
-        if (pair8) {
-          cp_async8(dst + (3 + c) * 64, sl + fx0);
-        } else {
+        if constexpr (HILO) {
+          const float* sl = lbase + c * a.in_plane + ro;
           cp_async4(dst + (3 + c) * 64, sl + fx0);
           cp_async4(dst + (3 + c) * 64 + 1, sl + fx1);
         }
@@ -206,24 +330,25 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
     cp_async_commit();
   }
 
-  const double w0 = prm.wp[0], w1 = prm.wp[1], w2 = prm.wp[2], w3 = prm.wp[3], w4 = prm.wp[4];
+  const float w0 = (float)prm.wp[0], w1 = (float)prm.wp[1], w2 = (float)prm.wp[2];  // symmetric
   constexpr double dw0 = -3.0 / 256.0, dw1 = -9.0 / 256.0, dw2 = 29.0 / 256.0, dw3 = 111.0 / 256.0;
 
-  double zm[3][2], zc[3][2];  // own columns of rows c-1, c (c = r-1 is the product row)
-  double cL1[3], cR2[3];      // row c at columns x-1 and x+2
-  double vA[4][2], vB[4][2], vC[4][2];  // pending window rows y = c-1 .. c+2 (after the shift)
-  double dacc[4][3];          // pending decimated rows (4) x channels
+  // fp32 gradient rows (own columns of rows c-1, c; row c at columns x-1, x+2); hi and lo parts
+  float hm[3][2], hc[3][2], hL[3], hR[3];
+  float lm[3][2], lc[3][2], lL[3], lR[3];
+  float vA[4][2], vB[4][2], vC[4][2];  // pending window rows y = c-1 .. c+2 (after the shift)
+  double dacc[4][3];                   // pending decimated rows (4) x channels
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) vA[k][j] = vB[k][j] = vC[k][j] = 0.0;
+    for (int j = 0; j < 2; ++j) vA[k][j] = vB[k][j] = vC[k][j] = 0.0f;
 #pragma unroll
     for (int c = 0; c < 3; ++c) dacc[k][c] = 0.0;
   }
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    zm[c][0] = zm[c][1] = zc[c][0] = zc[c][1] = 0.0;
-    cL1[c] = cR2[c] = 0.0;
+    hm[c][0] = hm[c][1] = hc[c][0] = hc[c][1] = hL[c] = hR[c] = 0.0f;
+    lm[c][0] = lm[c][1] = lc[c][0] = lc[c][1] = lL[c] = lR[c] = 0.0f;
   }
 
   uint8_t* mapf = a.map + (long long)n * a.s_rn * a.W;
@@ -236,59 +361,60 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
     cp_async_commit();
     cp_async_wait<RING - 1>();
     const float* src = ring + (i % RING) * NP * 64;
-    double zn[3][2];
+    float hn[3][2], ln[3][2], nL[3], nR[3], nlL[3], nlR[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const float2 h2 = *reinterpret_cast<const float2*>(src + c * 64);
+      hn[c][0] = h2.x;
+      hn[c][1] = h2.y;
       if constexpr (HILO) {
         const float2 l2 = *reinterpret_cast<const float2*>(src + (3 + c) * 64);
-        zn[c][0] = (double)h2.x + (double)l2.x;
-        zn[c][1] = (double)h2.y + (double)l2.y;
+        ln[c][0] = l2.x;
+        ln[c][1] = l2.y;
       } else {
-        zn[c][0] = (double)h2.x;
-        zn[c][1] = (double)h2.y;
+        ln[c][0] = ln[c][1] = 0.0f;
       }
-    }
-    // horizontal neighbours of row r (x-1, x+2 for the next gradient row; x-3..x+4 for decimation)
-    double nL1[3], nR2[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      nL1[c] = shfl_up_d(zn[c][1], 1);
-      nR2[c] = shfl_dn_d(zn[c][0], 1);
+      // columns x-1 and x+2 of row r (fp32 parts): gradients of the next product row
+      nL[c] = __shfl_up_sync(0xffffffffu, hn[c][1], 1);
+      nR[c] = __shfl_down_sync(0xffffffffu, hn[c][0], 1);
+      if constexpr (HILO) {
+        nlL[c] = __shfl_up_sync(0xffffffffu, ln[c][1], 1);
+        nlR[c] = __shfl_down_sync(0xffffffffu, ln[c][0], 1);
+      } else {
+        nlL[c] = nlR[c] = 0.0f;
+      }
     }
     const int r = Yb - 3 + i;
 
     if constexpr (DEC) {
-      // ---- decimation: horizontal 8 taps at column Xd of row r, then the vertical ring
+      // ---- decimation (fp64): horizontal 8 taps at column Xd of row r, then the vertical ring
       const bool odd_r = (i & 1) == 0;  // Yb even => r = Yb - 3 + i is odd for even i
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double zL2 = shfl_up_d(zn[c][0], 1);   // x-2
-        const double zL3 = shfl_up_d(zn[c][1], 2);   // x-3
-        const double zR3 = shfl_dn_d(zn[c][1], 1);   // x+3
-        const double zR4 = shfl_dn_d(zn[c][0], 2);   // x+4
-        double hp = dw0 * zL3;
-        hp = fma(dw1, zL2, hp);
-        hp = fma(dw2, nL1[c], hp);
-        hp = fma(dw3, zn[c][0], hp);
-        hp = fma(dw3, zn[c][1], hp);
-        hp = fma(dw2, nR2[c], hp);
-        hp = fma(dw1, zR3, hp);
-        hp = fma(dw0, zR4, hp);
-        // pending rows Y' = Yb/2 + m - 3 + k (k = 0..3); weight index 6-2k (odd r) / 7-2k (even r)
+        const double z0 = (double)hn[c][0] + (double)ln[c][0];
+        const double z1 = (double)hn[c][1] + (double)ln[c][1];
+        const double zL1 = (double)nL[c] + (double)nlL[c];
+        const double zR2 = (double)nR[c] + (double)nlR[c];
+        const double zL2 = shfl_up_d(z0, 1);   // x-2
+        const double zL3 = shfl_up_d(z1, 2);   // x-3
+        const double zR3 = shfl_dn_d(z1, 1);   // x+3
+        const double zR4 = shfl_dn_d(z0, 2);   // x+4
+        double hp = dw0 * (zL3 + zR4);
+        hp = fma(dw1, zL2 + zR3, hp);
+        hp = fma(dw2, zL1 + zR2, hp);
+        hp = fma(dw3, z0 + z1, hp);
         if (odd_r) {
-          dacc[0][c] = fma(dw1, hp, dacc[0][c]);  // w[6] = w[1]
-          dacc[1][c] = fma(dw3, hp, dacc[1][c]);  // w[4] = w[3]
+          dacc[0][c] = fma(dw1, hp, dacc[0][c]);  // w[6]
+          dacc[1][c] = fma(dw3, hp, dacc[1][c]);  // w[4]
           dacc[2][c] = fma(dw2, hp, dacc[2][c]);  // w[2]
           dacc[3][c] = fma(dw0, hp, dacc[3][c]);  // w[0]
         } else {
-          dacc[0][c] = fma(dw0, hp, dacc[0][c]);  // w[7] = w[0]
-          dacc[1][c] = fma(dw2, hp, dacc[1][c]);  // w[5] = w[2]
+          dacc[0][c] = fma(dw0, hp, dacc[0][c]);  // w[7]
+          dacc[1][c] = fma(dw2, hp, dacc[1][c]);  // w[5]
           dacc[2][c] = fma(dw3, hp, dacc[2][c]);  // w[3]
           dacc[3][c] = fma(dw1, hp, dacc[3][c]);  // w[1]
         }
       }
-      // NB: w = [-3, -9, 29, 111, 111, 29, -9, -3] / 256 is symmetric: w[6] = w[1] = dw1 ...
       if (!odd_r) {
         const int Yd = (r - 4) / 2;  // completed row (r even)
         if (out_lane && Yd >= a.d_r0 && Yd < a.d_r0 + a.d_rn && Xd < a.W1 && i >= 7) {
@@ -312,58 +438,138 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
     }
 
     if (i >= 2) {
-      // ---- products at row c = r - 1 for columns x, x+1 (unscaled gradients 2g)
-      double A0 = 0.0, B0 = 0.0, C0 = 0.0, A1 = 0.0, B1 = 0.0, C1 = 0.0;
+      // ---- fp32 products at row c = r - 1 for columns x, x+1 (unscaled gradients 2g; at l >= 1
+      //      (hi1 - hi0) + (lo1 - lo0), relative error ~2u of the exact fp64-level difference)
+      float A0 = 0.0f, B0 = 0.0f, C0 = 0.0f, A1 = 0.0f, B1 = 0.0f, C1 = 0.0f;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double gx0 = zc[c][1] - cL1[c], gx1 = cR2[c] - zc[c][0];
-        const double gy0 = zn[c][0] - zm[c][0], gy1 = zn[c][1] - zm[c][1];
-        A0 = fma(gx0, gx0, A0);
-        B0 = fma(gx0, gy0, B0);
-        C0 = fma(gy0, gy0, C0);
-        A1 = fma(gx1, gx1, A1);
-        B1 = fma(gx1, gy1, B1);
-        C1 = fma(gy1, gy1, C1);
+        float gx0 = hc[c][1] - hL[c], gx1 = hR[c] - hc[c][0];
+        float gy0 = hn[c][0] - hm[c][0], gy1 = hn[c][1] - hm[c][1];
+        if constexpr (HILO) {
+          gx0 += lc[c][1] - lL[c];
+          gx1 += lR[c] - lc[c][0];
+          gy0 += ln[c][0] - lm[c][0];
+          gy1 += ln[c][1] - lm[c][1];
+        }
+        A0 = fmaf(gx0, gx0, A0);
+        B0 = fmaf(gx0, gy0, B0);
+        C0 = fmaf(gy0, gy0, C0);
+        A1 = fmaf(gx1, gx1, A1);
+        B1 = fmaf(gx1, gy1, B1);
+        C1 = fmaf(gy1, gy1, C1);
       }
-      // ---- horizontal window: products at x-2, x-1 (lane-1) and x+2, x+3 (lane+1)
-      const double Am2 = shfl_up_d(A0, 1), Am1 = shfl_up_d(A1, 1), Ap2 = shfl_dn_d(A0, 1), Ap3 = shfl_dn_d(A1, 1);
-      const double Bm2 = shfl_up_d(B0, 1), Bm1 = shfl_up_d(B1, 1), Bp2 = shfl_dn_d(B0, 1), Bp3 = shfl_dn_d(B1, 1);
-      const double Cm2 = shfl_up_d(C0, 1), Cm1 = shfl_up_d(C1, 1), Cp2 = shfl_dn_d(C0, 1), Cp3 = shfl_dn_d(C1, 1);
-      double hA0 = w0 * Am2, hB0 = w0 * Bm2, hC0 = w0 * Cm2;
-      hA0 = fma(w1, Am1, hA0); hB0 = fma(w1, Bm1, hB0); hC0 = fma(w1, Cm1, hC0);
-      hA0 = fma(w2, A0, hA0);  hB0 = fma(w2, B0, hB0);  hC0 = fma(w2, C0, hC0);
-      hA0 = fma(w3, A1, hA0);  hB0 = fma(w3, B1, hB0);  hC0 = fma(w3, C1, hC0);
-      hA0 = fma(w4, Ap2, hA0); hB0 = fma(w4, Bp2, hB0); hC0 = fma(w4, Cp2, hC0);
-      double hA1 = w0 * Am1, hB1 = w0 * Bm1, hC1 = w0 * Cm1;
-      hA1 = fma(w1, A0, hA1);  hB1 = fma(w1, B0, hB1);  hC1 = fma(w1, C0, hC1);
-      hA1 = fma(w2, A1, hA1);  hB1 = fma(w2, B1, hB1);  hC1 = fma(w2, C1, hC1);
-      hA1 = fma(w3, Ap2, hA1); hB1 = fma(w3, Bp2, hB1); hC1 = fma(w3, Cp2, hC1);
-      hA1 = fma(w4, Ap3, hA1); hB1 = fma(w4, Bp3, hB1); hC1 = fma(w4, Cp3, hC1);
+      // ---- horizontal window: products at x-2, x-1 (lane-1) and x+2, x+3 (lane+1); w symmetric
+      const float Am2 = __shfl_up_sync(0xffffffffu, A0, 1), Am1 = __shfl_up_sync(0xffffffffu, A1, 1);
+      const float Ap2 = __shfl_down_sync(0xffffffffu, A0, 1), Ap3 = __shfl_down_sync(0xffffffffu, A1, 1);
+      const float Bm2 = __shfl_up_sync(0xffffffffu, B0, 1), Bm1 = __shfl_up_sync(0xffffffffu, B1, 1);
+      const float Bp2 = __shfl_down_sync(0xffffffffu, B0, 1), Bp3 = __shfl_down_sync(0xffffffffu, B1, 1);
+      const float Cm2 = __shfl_up_sync(0xffffffffu, C0, 1), Cm1 = __shfl_up_sync(0xffffffffu, C1, 1);
+      const float Cp2 = __shfl_down_sync(0xffffffffu, C0, 1), Cp3 = __shfl_down_sync(0xffffffffu, C1, 1);
+      const float hA[2] = {fmaf(w0, Am2 + Ap2, fmaf(w1, Am1 + A1, w2 * A0)), fmaf(w0, Am1 + Ap3, fmaf(w1, A0 + Ap2, w2 * A1))};
+      const float hB[2] = {fmaf(w0, Bm2 + Bp2, fmaf(w1, Bm1 + B1, w2 * B0)), fmaf(w0, Bm1 + Bp3, fmaf(w1, B0 + Bp2, w2 * B1))};
+      const float hC[2] = {fmaf(w0, Cm2 + Cp2, fmaf(w1, Cm1 + C1, w2 * C0)), fmaf(w0, Cm1 + Cp3, fmaf(w1, C0 + Cp2, w2 * C1))};
       // ---- vertical window: pending rows y = c-2 .. c+2 get weight w[c - y + 2]
-      const double hA[2] = {hA0, hA1}, hB[2] = {hB0, hB1}, hC[2] = {hC0, hC1};
       const int y = r - 3;  // = c - 2: completes now
       const bool emit = i >= 6 && out_lane && y >= a.s_r0 && y < a.s_r0 + a.s_rn;
+      int bk[2];
+      bool need_fb = false;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const double fa = fma(w4, hA[j], vA[0][j]), fb = fma(w4, hB[j], vB[0][j]), fc = fma(w4, hC[j], vC[0][j]);
-        if (emit && x + j < a.W)
-          mapf[(long long)(y - a.s_r0) * a.W + x + j] = (uint8_t)bucket_of<FAST>(fa, fb, fc, prm);
-        vA[0][j] = fma(w3, hA[j], vA[1][j]); vB[0][j] = fma(w3, hB[j], vB[1][j]); vC[0][j] = fma(w3, hC[j], vC[1][j]);
-        vA[1][j] = fma(w2, hA[j], vA[2][j]); vB[1][j] = fma(w2, hB[j], vB[2][j]); vC[1][j] = fma(w2, hC[j], vC[2][j]);
-        vA[2][j] = fma(w1, hA[j], vA[3][j]); vB[2][j] = fma(w1, hB[j], vB[3][j]); vC[2][j] = fma(w1, hC[j], vC[3][j]);
-        vA[3][j] = w0 * hA[j];               vB[3][j] = w0 * hB[j];               vC[3][j] = w0 * hC[j];
+        const float fa = fmaf(w0, hA[j], vA[0][j]), fb = fmaf(w0, hB[j], vB[0][j]), fc = fmaf(w0, hC[j], vC[0][j]);
+        bool safe = true;
+        bk[j] = bucket32<FAST>(fa, fb, fc, prm, safe);
+        need_fb |= emit && x + j < a.W && !safe;
+        (void)safe;
+        vA[0][j] = fmaf(w1, hA[j], vA[1][j]); vB[0][j] = fmaf(w1, hB[j], vB[1][j]); vC[0][j] = fmaf(w1, hC[j], vC[1][j]);
+        vA[1][j] = fmaf(w2, hA[j], vA[2][j]); vB[1][j] = fmaf(w2, hB[j], vB[2][j]); vC[1][j] = fmaf(w2, hC[j], vC[2][j]);
+        vA[2][j] = fmaf(w1, hA[j], vA[3][j]); vB[2][j] = fmaf(w1, hB[j], vB[3][j]); vC[2][j] = fmaf(w1, hC[j], vC[3][j]);
+        vA[3][j] = w0 * hA[j];                vB[3][j] = w0 * hB[j];                vC[3][j] = w0 * hC[j];
+      }
+      if (need_fb) {  // rare: queue the uncertified pixel(s) for the fp64 fix-up kernel
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (x + j >= a.W) continue;
+          const unsigned int slot = atomicAdd(a.fb_count, 1u);
+          if (slot < a.fb_cap)
+            a.fb_list[slot] = ((unsigned long long)n * a.s_rn + (unsigned long long)(y - a.s_r0)) * a.W + x + j;
+        }
+      }
+      if (emit) {
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          if (x + j < a.W) mapf[(long long)(y - a.s_r0) * a.W + x + j] = (uint8_t)bk[j];
       }
     }
     // ---- rotate the gradient rows
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      zm[c][0] = zc[c][0];
-      zm[c][1] = zc[c][1];
-      zc[c][0] = zn[c][0];
-      zc[c][1] = zn[c][1];
-      cL1[c] = nL1[c];
-      cR2[c] = nR2[c];
+      hm[c][0] = hc[c][0];
+      hm[c][1] = hc[c][1];
+      hc[c][0] = hn[c][0];
+      hc[c][1] = hn[c][1];
+      hL[c] = nL[c];
+      hR[c] = nR[c];
+      lm[c][0] = lc[c][0];
+      lm[c][1] = lc[c][1];
+      lc[c][0] = ln[c][0];
+      lc[c][1] = ln[c][1];
+      lL[c] = nlL[c];
+      lR[c] = nlR[c];
     }
+  }
+}
+
+// Fix-up of the uncertified pixels of one k_down launch: fp64 (a, b, c) and the bucket rule in
+// fp64-derived fp32 as the fp64 selector. If the list overflowed (pathological inputs with many
+// exactly isotropic tensors), every map entry of the launch is recomputed.
+template <bool HILO, bool FAST>
+__global__ void __launch_bounds__(128) k_down_fixup(const DownArgs a, const DownParams prm) {
+  // one warp per pixel: lane t < 25 evaluates the gradient products at window offset
+  // (t / 5 - 2, t % 5 - 2) in fp64, the weighted products are summed over the warp (fp64)
+  const unsigned int cnt = *a.fb_count;
+  const bool all = cnt > a.fb_cap;
+  const unsigned long long per_frame = (unsigned long long)a.s_rn * a.W;
+  const unsigned long long items = all ? (unsigned long long)a.N * per_frame : (unsigned long long)cnt;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < items;
+       i += warps) {
+    const unsigned long long e = all ? i : a.fb_list[i];
+    const int n = (int)(e / per_frame);
+    const unsigned long long r = e - (unsigned long long)n * per_frame;
+    const int y = a.s_r0 + (int)(r / a.W), xx = (int)(r % a.W);
+    double pa = 0.0, pb = 0.0, pc = 0.0;
+    if (lane < 25) {
+      const int dy = lane / 5 - 2, dx = lane % 5 - 2;
+      auto Z = [&](int c, int yy, int xq) -> double {
+        int br = fold_idx(yy, a.H) - a.in_row0;
+        br = min(max(br, 0), a.in_rows - 1);
+        const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.W + fold_idx(xq, a.W);
+        double v = (double)a.zhi[o];
+        if constexpr (HILO) v += (double)a.zlo[o];
+        return v;
+      };
+      const int yy = y + dy, xq = xx + dx;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double gx = Z(c, yy, xq + 1) - Z(c, yy, xq - 1);
+        const double gy = Z(c, yy + 1, xq) - Z(c, yy - 1, xq);
+        pa = fma(gx, gx, pa);
+        pb = fma(gx, gy, pb);
+        pc = fma(gy, gy, pc);
+      }
+      const double wgt = prm.wp[dy + 2] * prm.wp[dx + 2];
+      pa *= wgt;
+      pb *= wgt;
+      pc *= wgt;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      pa += __shfl_xor_sync(0xffffffffu, pa, o);
+      pb += __shfl_xor_sync(0xffffffffu, pb, o);
+      pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    }
+    if (lane == 0) a.map[e] = (uint8_t)bucket_of<FAST>(pa, pb, pc, prm);
   }
 }
 

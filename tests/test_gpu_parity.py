@@ -222,3 +222,20 @@ def test_shard_bands_equal_full_image(world):
         band_in = x[0, :, s.in_row0:s.in_row0 + s.in_rows].contiguous()
         parts.append(h.denoise_rows(band_in, s.in_row0, s.out_row0, s.out_rows, cfg.H))
     assert torch.equal(torch.cat(parts, 1), full)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3"])
+def test_fp32_selector_fallback_is_rare(name):
+    """The fp32 selector recomputes uncertified pixels in fp64 (DESIGN.md §6 H1); on the configs'
+    scenes that must stay rare (it is a correctness net, not the path)."""
+    cfg = bs.load_config(name)
+    N = min(cfg.N, 2)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch(N=N)).cuda()
+    ws = h.workspace(N, cfg.H, cfg.W)
+    h.selector(x, workspace=ws)
+    counts = h.fallback_count(N, cfg.H, cfg.W, ws)
+    dims = h.level_dims(cfg.H, cfg.W)
+    rates = [c / (N * dims[l][0] * dims[l][1]) for l, c in enumerate(counts)]
+    print(f"{name}: fallback counts {counts} rates {rates}")
+    assert all(r < 2e-3 for r in rates), rates
