@@ -125,7 +125,7 @@ DownKernel down_kernel_t(bool hilo, bool dec) {
   if (hilo) return dec ? &k_down<true, true, FAST> : &k_down<true, false, FAST>;
   return dec ? &k_down<false, true, FAST> : &k_down<false, false, FAST>;
 }
-// FAST: the configs' layout (16 orientations, <= 3 strength and coherence bins)
+// FAST: the configs' bucket layout (16 orientations x 3 strength x 3 coherence bins)
 DownKernel down_kernel(bool hilo, bool dec, bool fast) {
   return fast ? down_kernel_t<true>(hilo, dec) : down_kernel_t<false>(hilo, dec);
 }
@@ -459,7 +459,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.N = N;
     ProfScope ps(h, st, 1, l);
     const bool hilo = l > 0;
-    const bool fast = h->n_o == 16 && h->n_s <= 3 && h->n_c <= 3;
+    const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
     auto fn = down_kernel(hilo, dec, fast);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     fn<<<grid, 32 * down::WARPS, down_smem(hilo), st>>>(da, h->down[l]);

@@ -172,24 +172,33 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
   const float h = 0.125f * T;                                    // unscaled x4 -> T/2
   const float q = 0.0625f * fmaf(0.25f * Df, Df, b * b);         // r^2
   const float bound = kCert * T;
-  int o = 0;
-  if (!(Df == 0.0f && b == 0.0f)) {
-    const float X = -Df, Y = -2.0f * b;
-    float mn = fminf(fabsf(X), fabsf(Y));
-    if (FAST || prm.quad_edges) {
-      int qd;
-      float xr, yr;
-      if (X > 0.0f && Y >= 0.0f) { qd = 0; xr = X; yr = Y; }
-      else if (X <= 0.0f && Y > 0.0f) { qd = 1; xr = Y; yr = -X; }
-      else if (X < 0.0f && Y <= 0.0f) { qd = 2; xr = -X; yr = -Y; }
-      else { qd = 3; xr = -Y; yr = X; }
-      if constexpr (FAST) {
-        constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f;  // pi/8
-        constexpr float c2 = 0.70710678118654752f;                              // pi/4
-        const float e1 = fmaf(c1, yr, -s1 * xr), e2 = fmaf(c2, yr, -c2 * xr), e3 = fmaf(s1, yr, -c1 * xr);
-        o = 4 * qd + (e1 >= 0.0f) + (e2 >= 0.0f) + (e3 >= 0.0f);
-        mn = fminf(mn, fminf(fabsf(e1), fminf(fabsf(e2), fabsf(e3))));
-      } else {
+  const float X = -Df, Y = -2.0f * b;
+  const bool zero = Df == 0.0f && b == 0.0f;
+  int o;
+  float mn;
+  if constexpr (FAST) {
+    // branch-free: rotate (X, Y) by pi into the upper half plane, then by -pi/2 into quadrant 0
+    const bool lower = Y < 0.0f || (Y == 0.0f && X < 0.0f);
+    const float X1 = lower ? -X : X, Y1 = lower ? -Y : Y;
+    const bool left = X1 <= 0.0f;
+    const float xr = left ? Y1 : X1, yr = left ? -X1 : Y1;
+    constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f;  // pi/8
+    constexpr float c2 = 0.70710678118654752f;                              // pi/4
+    const float e1 = fmaf(c1, yr, -s1 * xr), e2 = fmaf(c2, yr, -c2 * xr), e3 = fmaf(s1, yr, -c1 * xr);
+    o = (lower ? 8 : 0) + (left ? 4 : 0) + (e1 >= 0.0f) + (e2 >= 0.0f) + (e3 >= 0.0f);
+    mn = fminf(fminf(fabsf(X), fabsf(Y)), fminf(fabsf(e1), fminf(fabsf(e2), fabsf(e3))));
+    o = zero ? 0 : o;
+  } else {
+    o = 0;
+    mn = fminf(fabsf(X), fabsf(Y));
+    if (!zero) {
+      if (prm.quad_edges) {
+        int qd;
+        float xr, yr;
+        if (X > 0.0f && Y >= 0.0f) { qd = 0; xr = X; yr = Y; }
+        else if (X <= 0.0f && Y > 0.0f) { qd = 1; xr = Y; yr = -X; }
+        else if (X < 0.0f && Y <= 0.0f) { qd = 2; xr = -X; yr = -Y; }
+        else { qd = 3; xr = -Y; yr = X; }
         const int m = prm.n_o >> 2;
         o = qd * m;
         for (int j = 0; j < m - 1; ++j) {
@@ -197,23 +206,22 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
           o += (e >= 0.0f);
           mn = fminf(mn, fabsf(e));
         }
+      } else {
+        // generic n_o: atan2f (~2 ulp) and the distance to the nearest edge in psi
+        const float kTwoPiInv = 0.15915494309189535f;
+        const float phi = atan2f(-Y, -X);  // = atan2(2b, a - c)
+        const float f = fmaf(phi, (float)prm.n_o * kTwoPiInv, 0.5f * (float)prm.n_o);
+        o = (int)floorf(f);
+        const float fr = f - floorf(f);
+        const float dist = fminf(fr, 1.0f - fr) * 6.283185307179586f / (float)prm.n_o;  // radians in psi
+        mn = fminf(mn, (dist - 2e-6f) * sqrtf(fmaf(X, X, Y * Y)));
+        o %= prm.n_o;
+        if (o < 0) o += prm.n_o;
       }
-    } else {
-      // generic n_o: atan2f (~2 ulp) and the distance to the nearest edge in psi
-      const float kTwoPiInv = 0.15915494309189535f;
-      const float phi = atan2f(-Y, -X);  // = atan2(2b, a - c)
-      const float f = fmaf(phi, (float)prm.n_o * kTwoPiInv, 0.5f * (float)prm.n_o);
-      o = (int)floorf(f);
-      const float fr = f - floorf(f);
-      const float dist = fminf(fr, 1.0f - fr) * 6.283185307179586f / (float)prm.n_o;  // radians in psi
-      mn = fminf(mn, (dist - 2e-6f) * sqrtf(fmaf(X, X, Y * Y)));
-      o %= prm.n_o;
-      if (o < 0) o += prm.n_o;
     }
-    safe = mn > bound;
-  } else {
-    safe = !(T > 0.0f);  // all gradients exactly zero => theta = 0 exactly [R5]
   }
+  // certified iff every sign test clears the error bound; exact zero gradients => theta = 0 [R5]
+  safe = zero ? !(T > 0.0f) : (mn > bound);
   int s = 0;
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) {
@@ -221,15 +229,15 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
     const float d = prm.ts2[t] - h;
     s += (d <= 0.0f) || (q >= d * d);
   }
-  int k = prm.tc_nonpos;
-  if (h > 0.0f) {
-    const float h2 = h * h;
+  const float h2 = h * h;
+  int k = 0;
 #pragma unroll
-    for (int t = 0; t < MAXT; ++t) {
-      if (!FAST && t >= prm.n_c - 1) break;
-      k += (q >= prm.kc2[t] * h2);
-    }
+  for (int t = 0; t < MAXT; ++t) {
+    if (!FAST && t >= prm.n_c - 1) break;
+    k += (q >= prm.kc2[t] * h2);
   }
+  k = prm.tc_nonpos + (h > 0.0f ? k : 0);  // C = 0 when l1 = 0 [R6]
+  if constexpr (FAST) return (o * 3 + s) * 3 + k;  // FAST layout: 16 x 3 x 3
   return (o * prm.n_s + s) * prm.n_c + k;
 }
 
@@ -354,6 +362,8 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
   uint8_t* mapf = a.map + (long long)n * a.s_rn * a.W;
   const long long oframe = (long long)n * 3 * a.d_buf_rows * a.W1;
   const int Xd = x >> 1;  // decimated column (x even)
+  // 2-byte map stores when every map row starts 2-B aligned (x is even)
+  const bool map16 = ((a.W | (int)(reinterpret_cast<uintptr_t>(a.map) & 1)) & 1) == 0;
 
 #pragma unroll 2
   for (int i = 0; i < nrows; ++i) {
@@ -494,10 +504,14 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
             a.fb_list[slot] = ((unsigned long long)n * a.s_rn + (unsigned long long)(y - a.s_r0)) * a.W + x + j;
         }
       }
-      if (emit) {
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (x + j < a.W) mapf[(long long)(y - a.s_r0) * a.W + x + j] = (uint8_t)bk[j];
+      if (emit && x < a.W) {
+        uint8_t* mrow = mapf + (long long)(y - a.s_r0) * a.W + x;
+        if (map16 && x + 1 < a.W)
+          *reinterpret_cast<uint16_t*>(mrow) = (uint16_t)(bk[0] | (bk[1] << 8));
+        else {
+          mrow[0] = (uint8_t)bk[0];
+          if (x + 1 < a.W) mrow[1] = (uint8_t)bk[1];
+        }
       }
     }
     // ---- rotate the gradient rows
