@@ -239,3 +239,25 @@ def test_fp32_selector_fallback_is_rare(name):
     rates = [c / (N * dims[l][0] * dims[l][1]) for l, c in enumerate(counts)]
     print(f"{name}: fallback counts {counts} rates {rates}")
     assert all(r < 2e-3 for r in rates), rates
+
+
+@pytest.mark.parametrize("name,H,W,N", [("c0", 64, 64, 1), ("c1", 67, 129, 2), ("c3", 130, 259, 2),
+                                        ("c4", 77, 190, 1), ("c2", 5, 1, 1)])
+def test_no_writes_outside_buffers(name, H, W, N):
+    """Canary bytes after the output and after the workspace stay untouched (out-of-bounds writes
+    into caller memory are otherwise silent)."""
+    cfg = _cfg_like(name, H, W, N)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    n_out = x.numel()
+    out_buf = torch.full((n_out + 4096,), 7.25, dtype=torch.float32, device="cuda")
+    out = out_buf[:n_out].view_as(x)
+    ws_n = h.workspace_size(N, H, W)
+    ws_buf = torch.full((ws_n + 65536,), 0xA5, dtype=torch.uint8, device="cuda")
+    h.denoise(x, out, ws_buf[:ws_n])
+    torch.cuda.synchronize()
+    assert bool((out_buf[n_out:] == 7.25).all())
+    assert bool((ws_buf[ws_n:] == 0xA5).all())
+    maps = h.selector(x, workspace=ws_buf[:ws_n])
+    torch.cuda.synchronize()
+    assert bool((ws_buf[ws_n:] == 0xA5).all())
