@@ -29,6 +29,7 @@
 
 #include "../../include/blade_ms.h"
 #include "k_down.cuh"
+#include "k_stage_ph.cuh"
 #include "k_stage_tma.cuh"
 #include "kernels.cuh"
 
@@ -100,6 +101,7 @@ struct TmaVariant {
   int nf, nc, groups;
   TmaKernel fn;
   int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc, S;
+  bool phase_split;  // k_stage_ph: CTAs specialised by output phase, one phase's bank each
 };
 #ifndef BLADE_TMA_GROUPS
 #define BLADE_TMA_GROUPS 2
@@ -108,7 +110,20 @@ template <int NF, int NC, int G = BLADE_TMA_GROUPS>
 TmaVariant make_tma() {
   using SS = TmaShape<NF, NC>;
   return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S};
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false};
+}
+template <int NF, int NC>
+TmaVariant make_ph() {
+  using SS = PhShape<NF, NC>;
+  return TmaVariant{NF, NC, 2, &k_stage_ph<NF, NC>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, true};
+}
+// Phase-split TMA stage kernels: pair banks whose four phases do not fit one CTA.
+const std::vector<TmaVariant>& ph_variants() {
+  static const std::vector<TmaVariant> v = {
+      make_ph<7, 7>(), make_ph<9, 9>(), make_ph<7, 5>(), make_ph<9, 7>(), make_ph<5, 7>(), make_ph<7, 9>(),
+  };
+  return v;
 }
 // TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
 const std::vector<TmaVariant>& tma_variants() {
@@ -533,8 +548,13 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       a.tiles_y = (r.hi - y_base + tv.trows - 1) / tv.trows;
       a.n_tiles = N * a.tiles_x * a.tiles_y;
       a.clamp = clamp;
-      const int grid = std::min(h->num_sms, (a.n_tiles + tv.groups - 1) / tv.groups);
-      tv.fn<<<grid, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+      if (tv.phase_split) {  // 4 phase-CTAs per tile group, 2 workers (groups) per CTA
+        const int per_phase = std::max(1, std::min(h->num_sms / 4, (a.n_tiles + 1) / 2));
+        tv.fn<<<4 * per_phase, dim3(32, 8), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+      } else {
+        const int grid = std::min(h->num_sms, (a.n_tiles + tv.groups - 1) / tv.groups);
+        tv.fn<<<grid, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+      }
       LAUNCH_CHECK("k_stage_tma");
       continue;
     }
@@ -705,6 +725,20 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
       h->tma_smem = smem;
       h->S_tma = v.S;
       h->PS_tma = (int)tps;
+    }
+  }
+  if (!h->has_tma && c.levels > 1 && c.n_phases == 4) {
+    for (const auto& v : ph_variants()) {
+      if (v.nf != c.fine_size || v.nc != cnc) continue;
+      const size_t tps = (size_t)K * v.S;
+      const size_t smem = 2 * (size_t)v.stage_bytes + ((tps * 4 + 127) & ~size_t(127)) + 16;
+      if (smem <= (size_t)max_smem && get_encode()) {
+        h->has_tma = true;
+        h->tma = v;
+        h->tma_smem = smem;
+        h->S_tma = v.S;
+        h->PS_tma = (int)tps;
+      }
     }
   }
 

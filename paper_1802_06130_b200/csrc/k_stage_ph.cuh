@@ -1,0 +1,267 @@
+// K3'' k_stage_ph: the stage of Eq. 9 (§4) for pair banks too large to keep all
+// four phases in one CTA's shared memory (7x7 + 7x7: 226 KB, 9x9 + 9x9: 373 KB for 4 x 144 filters;
+// BASELINE.json configs[2], configs[4]).
+//
+// CTAs are specialised by output phase p = 2 (y mod 2) + (x mod 2) (R9): a CTA keeps the
+// 144 filters of its phase (58 / 94 KB, tma_tap_off layout) and computes only the pixels of that
+// phase, so every thread block is a 2 x 2 block of the phase's sub-lattice (image pixels 2 apart).
+// Two 128-thread groups per CTA each own one TMA tile buffer (fine patch of z^l, coarse patch of
+// u^{l+1}, bucket tile of a 16 x 128 image tile) on an mbarrier and alternate tiles, so one
+// group computes while the other's TMA is in flight. The four phase-CTAs of a tile read the same
+// patches (L2 hits). Border cells are fixed up by the fold (R2) as in k_stage_tma.
+// FP32 FMA on the CUDA cores; taps shared by R, G, B (R13); LDS.128 tap rows.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "k_stage_tma.cuh"
+
+namespace blade {
+
+template <int NF, int NC>
+struct PhShape {
+  static constexpr int BX = 32, BY = 4;             // threads per group
+  static constexpr int threads = BX * BY;           // 128
+  static constexpr int RF = NF / 2, RC = NC / 2;
+  static constexpr int SUBR = 2 * BY, SUBC = 2 * BX;  // phase sub-lattice tile 8 x 64 (2 x 2 per thread)
+  static constexpr int TROWS = 2 * SUBR, TCOLS = 2 * SUBC;  // image tile 16 x 128
+  static constexpr int FM = 4, CM = 4;              // 16-B aligned TMA box starts (column margins)
+  static constexpr int FR = TROWS - 1 + 2 * RF;     // fine rows Y0 + py - RF .. Y0 + py + TROWS - 2 + RF
+  static constexpr int FCB = TCOLS + 2 * FM;        // 136: columns X0 - 4 .. X0 + 131
+  static constexpr int CR = SUBR + 2 * RC;          // coarse rows Y0/2 - RC .. Y0/2 + SUBR - 1 + RC
+  static constexpr int CCB = SUBC + 2 * CM;         // 72
+  static constexpr int FW = 2 * RF + 3;             // fine window columns per thread
+  static constexpr int CW = 2 * RC + 2;             // coarse window columns per thread
+  static constexpr int fine_bytes = 3 * FR * FCB * 4;
+  static constexpr int coarse_bytes = 3 * CR * CCB * 4;
+  static constexpr int map_bytes = TROWS * TCOLS;
+  static constexpr int al(int x) { return (x + 127) & ~127; }
+  static constexpr int fine_off = 0;
+  static constexpr int coarse_off = al(fine_bytes);
+  static constexpr int map_off = coarse_off + al(coarse_bytes);
+  static constexpr int stage_bytes = map_off + al(map_bytes);
+  static constexpr int S = tma_tap_stride(NF, NC);
+  static_assert(RF <= FM && RC <= CM, "halo wider than the TMA margin");
+};
+
+// One tile of phase (py, PX) by one 128-thread group: fix-up of border cells, then the 2 x 2
+// sub-lattice block of each thread.
+template <int NF, int NC, int PX>
+__device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, int Y0, int py, float* sfine,
+                                       float* scoarse, const uint8_t* smap, const float* sbank, int tid,
+                                       int tx, int ty, int g) {
+  using SS = PhShape<NF, NC>;
+  constexpr int RF = SS::RF, RC = SS::RC;
+  auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(SS::threads) : "memory"); };
+  const int FY = Y0 + py - RF, FX = X0 - SS::FM;          // fine box origin
+  const int CY = Y0 / 2 - RC, CX = X0 / 2 - SS::CM;       // coarse box origin
+  const bool fine_border = FX < 0 || FX + SS::FCB > a.W || FY < 0 || FY + SS::FR > a.H;
+  const bool coarse_border = CX < 0 || CX + SS::CCB > a.W1 || CY < 0 || CY + SS::CR > a.H1;
+  if (fine_border || coarse_border) {
+    if (fine_border) {
+      for (int i = tid; i < SS::FR * SS::FCB; i += SS::threads) {
+        const int r = i / SS::FCB, q = i - r * SS::FCB;
+        const int gy = FY + r, gx = FX + q;
+        if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) continue;
+        const int fy = fold_idx(gy, a.H), fx = fold_idx(gx, a.W);
+        const int ry = fy - FY, rx = fx - FX;
+        const bool in_tile = ry >= 0 && ry < SS::FR && rx >= 0 && rx < SS::FCB;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          float v;
+          if (in_tile) {
+            v = sfine[(c * SS::FR + ry) * SS::FCB + rx];
+          } else {
+            const int by = min(max(fy - a.z_row0, 0), a.z_rows - 1);
+            v = a.z[(((long long)n * 3 + c) * a.z_rows + by) * a.W + fx];
+          }
+          sfine[(c * SS::FR + r) * SS::FCB + q] = v;
+        }
+      }
+    }
+    if (coarse_border) {
+      for (int i = tid; i < SS::CR * SS::CCB; i += SS::threads) {
+        const int r = i / SS::CCB, q = i - r * SS::CCB;
+        const int gy = CY + r, gx = CX + q;
+        if (gy >= 0 && gy < a.H1 && gx >= 0 && gx < a.W1) continue;
+        const int fy = fold_idx(gy, a.H1), fx = fold_idx(gx, a.W1);
+        const int ry = fy - CY, rx = fx - CX;
+        const bool in_tile = ry >= 0 && ry < SS::CR && rx >= 0 && rx < SS::CCB;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          float v;
+          if (in_tile) {
+            v = scoarse[(c * SS::CR + ry) * SS::CCB + rx];
+          } else {
+            const int by = min(max(fy - a.u_row0, 0), a.u_rows - 1);
+            v = a.u1[(((long long)n * 3 + c) * a.u_rows + by) * a.W1 + fx];
+          }
+          scoarse[(c * SS::CR + r) * SS::CCB + q] = v;
+        }
+      }
+    }
+    group_sync();
+  }
+
+  // ---- this thread's 2 x 2 sub-lattice block: image pixels (Y0 + py + 4 ty + 2 i, X0 + PX + 4 tx + 2 j)
+  const float* tp[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = smap[(py + 4 * ty + 2 * i) * SS::TCOLS + PX + 4 * tx + 2 * j];
+      tp[i][j] = sbank + k * SS::S;
+    }
+  float acc[2][2][3];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[i][j][c] = 0.0f;
+
+  // coarse: pixel (i, j) has centre (Y0/2 + 2ty + i, X0/2 + 2tx + j); window rows 2ty + i + dy,
+  // columns (box) 2tx + j + dx + CM - RC
+  constexpr int CO = SS::CM - RC;
+#pragma unroll
+  for (int wr = 0; wr < NC + 1; ++wr) {
+    float v[3][SS::CW];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      lds_run<(CO & 1), SS::CW, 2>(scoarse + (c * SS::CR + 2 * ty + wr) * SS::CCB + 2 * tx + CO, v[c]);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int dy = wr - i;
+      if (dy < 0 || dy >= NC) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float t[NC];
+        load_tap_row<NF, NC, 1>(tp[i][j], dy, t);
+#pragma unroll
+        for (int dx = 0; dx < NC; ++dx)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][j + dx], acc[i][j][c]);
+      }
+    }
+  }
+  // fine: pixel (i, j) window rows 4ty + 2i + dy (box rows from Y0 + py - RF), columns (box)
+  // PX + 4tx + 2j + dx + FM - RF
+  constexpr int FO = PX + SS::FM - RF;
+#pragma unroll
+  for (int wr = 0; wr < NF + 2; ++wr) {
+    float v[3][SS::FW];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      lds_run<(FO & 3), SS::FW>(sfine + (c * SS::FR + 4 * ty + wr) * SS::FCB + 4 * tx + FO, v[c]);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int dy = wr - 2 * i;
+      if (dy < 0 || dy >= NF) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float t[NF];
+        load_tap_row<NF, NC, 0>(tp[i][j], dy, t);
+#pragma unroll
+        for (int dx = 0; dx < NF; ++dx)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][2 * j + dx], acc[i][j][c]);
+      }
+    }
+  }
+
+  // ---- store
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int yy = Y0 + py + 4 * ty + 2 * i;
+    if (yy < a.o_r0 || yy >= a.o_r0 + a.o_rn) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int xx = X0 + PX + 4 * tx + 2 * j;
+      if (xx >= a.W) continue;
+      float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.W + xx;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float v = acc[i][j][c];
+        if (a.clamp) v = fminf(fmaxf(v, 0.0f), 1.0f);
+        op[(long long)c * a.out_rows * a.W] = v;
+      }
+    }
+  }
+}
+
+// grid: 4 * m CTAs (CTA b serves phase b % 4), 256 threads = 2 groups of 128; n_tiles counts the
+// 16 x 128 image tiles; each phase's 2m workers stride over them.
+template <int NF, int NC>
+__global__ void __launch_bounds__(256, 1)
+    k_stage_ph(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
+               const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
+  using SS = PhShape<NF, NC>;
+  constexpr int RF = SS::RF, RC = SS::RC;
+  extern __shared__ __align__(128) unsigned char ph_smem[];
+  unsigned char* buf0 = ph_smem;
+  float* sbank = reinterpret_cast<float*>(ph_smem + 2 * SS::stage_bytes);
+  const int bank_floats = a.K * SS::S;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(ph_smem + 2 * SS::stage_bytes + ((bank_floats * 4 + 127) & ~127));
+
+  const int p = blockIdx.x & 3, py = p >> 1, px = p & 1;
+  const int g = threadIdx.y >> 2;                          // group (0, 1)
+  const int tx = threadIdx.x, ty = threadIdx.y & 3;
+  const int tid = ty * SS::BX + tx;                        // within the group
+  const int ctid = threadIdx.y * SS::BX + threadIdx.x;
+  const int cpp = gridDim.x >> 2;                          // CTAs per phase
+  const int workers = 2 * cpp;
+  constexpr uint32_t tx_bytes = SS::fine_bytes + SS::coarse_bytes + SS::map_bytes;
+
+  auto tile_coords = [&](int t, int& n, int& X0, int& Y0) {
+    n = t / (a.tiles_x * a.tiles_y);
+    const int rem = t - n * a.tiles_x * a.tiles_y;
+    const int tyi = rem / a.tiles_x;
+    X0 = (rem - tyi * a.tiles_x) * SS::TCOLS;
+    Y0 = a.y_base + tyi * SS::TROWS;
+  };
+  auto issue = [&](int t) {
+    int n, X0, Y0;
+    tile_coords(t, n, X0, Y0);
+    unsigned char* sb = buf0 + g * SS::stage_bytes;
+    mbar_expect_tx(&mbar[g], tx_bytes);
+    tma_load_3d(sb + SS::fine_off, &tm_z, X0 - SS::FM, Y0 + py - RF - a.z_row0, n * 3, &mbar[g]);
+    tma_load_3d(sb + SS::coarse_off, &tm_u, X0 / 2 - SS::CM, Y0 / 2 - RC - a.u_row0, n * 3, &mbar[g]);
+    tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[g]);
+  };
+
+  int t = (blockIdx.x >> 2) * 2 + g;
+  if (ctid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0 && t < a.n_tiles) issue(t);
+  {
+    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)p * a.PS);
+    float4* s4 = reinterpret_cast<float4*>(sbank);
+    for (int i = ctid; i < (bank_floats >> 2); i += 2 * SS::threads) s4[i] = __ldg(g4 + i);
+  }
+  __syncthreads();
+
+  for (int it = 0; t < a.n_tiles; ++it, t += workers) {
+    int n, X0, Y0;
+    tile_coords(t, n, X0, Y0);
+    mbar_wait(&mbar[g], it & 1);
+    float* sfine = reinterpret_cast<float*>(buf0 + g * SS::stage_bytes + SS::fine_off);
+    float* scoarse = reinterpret_cast<float*>(buf0 + g * SS::stage_bytes + SS::coarse_off);
+    const uint8_t* smap = buf0 + g * SS::stage_bytes + SS::map_off;
+    if (px)
+      ph_tile<NF, NC, 1>(a, n, X0, Y0, py, sfine, scoarse, smap, sbank, tid, tx, ty, g);
+    else
+      ph_tile<NF, NC, 0>(a, n, X0, Y0, py, sfine, scoarse, smap, sbank, tid, tx, ty, g);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(SS::threads) : "memory");  // buffer free
+    if (tid == 0 && t + workers < a.n_tiles) {
+      fence_proxy_async();
+      issue(t + workers);
+    }
+  }
+}
+
+}  // namespace blade
