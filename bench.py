@@ -209,7 +209,7 @@ def run_reference(args):
     sample = (f"one {rows}x{cfg.W} full-width band of a {cfg.name} frame per step "
               f"(treated as an image), fp64 oracle, OpenMP over rows")
     line = {"impl": "reference", "metric": "megapixels/sec full multiscale denoise",
-            "value": val, "unit": "MP/s", "n_gpus": 0, "steps": args.steps,
+            "value": val, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "desc": cfg.description, "frames": cfg.N,

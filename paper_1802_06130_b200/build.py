@@ -17,8 +17,9 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 INCLUDE = PKG.parent / "include"
 LIB = PKG / "libblade_ms.so"
-SOURCES = [CSRC / "blade_ms.cu"]
-DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [INCLUDE / "blade_ms.h"]
+SOURCES = [CSRC / "blade_ms.cu", CSRC / "tab_down.cu", CSRC / "tab_stage.cu", CSRC / "tab_tma.cu",
+           CSRC / "tab_ph.cu"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [INCLUDE / "blade_ms.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -36,17 +37,31 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
-        return LIB
-    tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
-    cmd = [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-I", str(INCLUDE), "-o", str(tmp), *map(str, SOURCES)]
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          out: Path | None = None) -> Path:
+    """Compile every translation unit in parallel (nvcc -c), then link the shared library."""
+    from concurrent.futures import ThreadPoolExecutor
+    lib = out or LIB
+    if out is None and not force and not needs_build():
+        return lib
+    objdir = PKG.parent / "build" / ("obj" if out is None else f"obj_{lib.stem}")
+    objdir.mkdir(parents=True, exist_ok=True)
+    flags = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-I", str(INCLUDE),
+             *(extra or [])]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+        flags.append("-Xptxas=-v")
+
+    def compile_one(src: Path) -> Path:
+        obj = objdir / (src.stem + ".o")
+        subprocess.check_call([nvcc(), *flags, "-c", "-o", str(obj), str(src)])
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    tmp = lib.with_suffix(f".so.tmp{os.getpid()}")
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs)])
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -32,6 +32,7 @@
 #include "k_stage_ph.cuh"
 #include "k_stage_tma.cuh"
 #include "kernels.cuh"
+#include "tables.h"
 
 using namespace blade;
 
@@ -71,79 +72,8 @@ struct DeviceGuard {
 };
 
 // ------------------------------------------------------------------------------ kernel tables
-using StageKernel = void (*)(StageArgs);
-struct StageVariant {
-  int nf, nc, rs, by;
-  StageKernel fn;
-  int tile_floats, threads, trows, tcols;
-};
-template <int NF, int NC, int RS, int BY>
-StageVariant make_variant() {
-  using SS = StageShape<NF, NC, RS, BY>;
-  return StageVariant{NF, NC, RS, BY, &k_stage<NF, NC, RS, BY>, SS::tile_floats, SS::threads,
-                      SS::TROWS, SS::TCOLS};
-}
-// Generic stage kernels (any shape; row-parity CTAs for the big pair banks).
-const std::vector<StageVariant>& stage_variants() {
-  static const std::vector<StageVariant> v = {
-      make_variant<3, 0, 1, 8>(), make_variant<5, 0, 1, 8>(), make_variant<7, 0, 1, 8>(),
-      make_variant<9, 0, 1, 8>(), make_variant<3, 3, 2, 8>(), make_variant<5, 5, 2, 8>(),
-      make_variant<7, 7, 2, 8>(), make_variant<7, 7, 2, 4>(), make_variant<9, 9, 2, 8>(),
-      make_variant<9, 9, 2, 4>(), make_variant<9, 9, 2, 2>(), make_variant<7, 5, 2, 8>(),
-      make_variant<7, 5, 2, 4>(), make_variant<5, 3, 2, 8>(), make_variant<9, 7, 2, 4>(),
-      make_variant<9, 7, 2, 2>(),
-  };
-  return v;
-}
-
-using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
-struct TmaVariant {
-  int nf, nc, groups;
-  TmaKernel fn;
-  int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc, S;
-  bool phase_split;  // k_stage_ph: CTAs specialised by output phase, one phase's bank each
-};
-#ifndef BLADE_TMA_GROUPS
-#define BLADE_TMA_GROUPS 2
-#endif
-template <int NF, int NC, int G = BLADE_TMA_GROUPS>
-TmaVariant make_tma() {
-  using SS = TmaShape<NF, NC>;
-  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false};
-}
-template <int NF, int NC>
-TmaVariant make_ph() {
-  using SS = PhShape<NF, NC>;
-  return TmaVariant{NF, NC, 2, &k_stage_ph<NF, NC>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, true};
-}
-// Phase-split TMA stage kernels: pair banks whose four phases do not fit one CTA.
-const std::vector<TmaVariant>& ph_variants() {
-  static const std::vector<TmaVariant> v = {
-      make_ph<7, 7>(), make_ph<9, 9>(), make_ph<7, 5>(), make_ph<9, 7>(), make_ph<5, 7>(), make_ph<7, 9>(),
-  };
-  return v;
-}
-// TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
-const std::vector<TmaVariant>& tma_variants() {
-  static const std::vector<TmaVariant> v = {
-      make_tma<3, 0>(), make_tma<5, 0>(), make_tma<7, 0>(), make_tma<9, 0>(),
-      make_tma<3, 3>(), make_tma<5, 5>(), make_tma<5, 3>(),
-  };
-  return v;
-}
-
-using DownKernel = void (*)(const DownArgs, const DownParams);
-template <bool FAST>
-DownKernel down_kernel_t(bool hilo, bool dec) {
-  if (hilo) return dec ? &k_down<true, true, FAST> : &k_down<true, false, FAST>;
-  return dec ? &k_down<false, true, FAST> : &k_down<false, false, FAST>;
-}
-// FAST: the configs' bucket layout (16 orientations x 3 strength x 3 coherence bins)
-DownKernel down_kernel(bool hilo, bool dec, bool fast) {
-  return fast ? down_kernel_t<true>(hilo, dec) : down_kernel_t<false>(hilo, dec);
-}
+// (instantiated in their own translation units, tab_*.cu, compiled in parallel; tables.h)
+using namespace blade::tables;
 size_t down_smem(bool hilo) { return sizeof(float) * down::WARPS * down::RING * (hilo ? 6 : 3) * 64; }
 
 // ------------------------------------------------------------------------------ TMA encode
@@ -479,8 +409,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     fn<<<grid, 32 * down::WARPS, down_smem(hilo), st>>>(da, h->down[l]);
     LAUNCH_CHECK("k_down");
-    auto fx = hilo ? (fast ? &k_down_fixup<true, true> : &k_down_fixup<true, false>)
-                   : (fast ? &k_down_fixup<false, true> : &k_down_fixup<false, false>);
+    auto fx = fixup_kernel(hilo, fast);
     fx<<<4 * h->num_sms, 128, 0, st>>>(da, h->down[l]);
     LAUNCH_CHECK("k_down_fixup");
   }
@@ -1094,7 +1023,7 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
   DeviceGuard guard(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   // chunked frame pipeline: H2D (chunk i+1) || compute (chunk i) || D2H (chunk i-1)
-  const int nchunks = std::min<int>(N, 8);
+  const int nchunks = std::min<int>(N, 16);
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in(nchunks, nullptr), ev_done(nchunks, nullptr);
   cudaEvent_t ev_start = nullptr;

@@ -1,0 +1,24 @@
+// Generic k_stage instantiations (tables.h).
+#include "tables.h"
+
+namespace blade {
+namespace tables {
+template <int NF, int NC, int RS, int BY>
+static StageVariant make_variant() {
+  using SS = StageShape<NF, NC, RS, BY>;
+  return StageVariant{NF, NC, RS, BY, &k_stage<NF, NC, RS, BY>, SS::tile_floats, SS::threads,
+                      SS::TROWS, SS::TCOLS};
+}
+const std::vector<StageVariant>& stage_variants() {
+  static const std::vector<StageVariant> v = {
+      make_variant<3, 0, 1, 8>(), make_variant<5, 0, 1, 8>(), make_variant<7, 0, 1, 8>(),
+      make_variant<9, 0, 1, 8>(), make_variant<3, 3, 2, 8>(), make_variant<5, 5, 2, 8>(),
+      make_variant<7, 7, 2, 8>(), make_variant<7, 7, 2, 4>(), make_variant<9, 9, 2, 8>(),
+      make_variant<9, 9, 2, 4>(), make_variant<9, 9, 2, 2>(), make_variant<7, 5, 2, 8>(),
+      make_variant<7, 5, 2, 4>(), make_variant<5, 3, 2, 8>(), make_variant<9, 7, 2, 4>(),
+      make_variant<9, 7, 2, 2>(),
+  };
+  return v;
+}
+}  // namespace tables
+}  // namespace blade

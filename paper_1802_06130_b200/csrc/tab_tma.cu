@@ -1,0 +1,23 @@
+// k_stage_tma instantiations (tables.h).
+#include "tables.h"
+
+#ifndef BLADE_TMA_GROUPS
+#define BLADE_TMA_GROUPS 2
+#endif
+namespace blade {
+namespace tables {
+template <int NF, int NC, int G = BLADE_TMA_GROUPS>
+static TmaVariant make_tma() {
+  using SS = TmaShape<NF, NC>;
+  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false};
+}
+const std::vector<TmaVariant>& tma_variants() {
+  static const std::vector<TmaVariant> v = {
+      make_tma<3, 0>(), make_tma<5, 0>(), make_tma<7, 0>(), make_tma<9, 0>(),
+      make_tma<3, 3>(), make_tma<5, 5>(), make_tma<5, 3>(),
+  };
+  return v;
+}
+}  // namespace tables
+}  // namespace blade

@@ -1,0 +1,43 @@
+// Kernel tables: every kernel instantiation the host orchestrator (blade_ms.cu) can launch,
+// defined in its own translation unit (tab_down.cu, tab_stage.cu, tab_tma.cu, tab_ph.cu) so the
+// library builds in parallel. Launches go through the typed __global__ function pointers.
+#pragma once
+#include <cuda.h>
+#include <vector>
+
+#include "k_down.cuh"
+#include "k_stage_ph.cuh"
+#include "k_stage_tma.cuh"
+#include "kernels.cuh"
+
+namespace blade {
+namespace tables {
+
+using StageKernel = void (*)(StageArgs);
+struct StageVariant {
+  int nf, nc, rs, by;
+  StageKernel fn;
+  int tile_floats, threads, trows, tcols;
+};
+// Generic stage kernels (any shape; row-parity CTAs for the big pair banks).
+const std::vector<StageVariant>& stage_variants();
+
+using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
+struct TmaVariant {
+  int nf, nc, groups;
+  TmaKernel fn;
+  int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc, S;
+  bool phase_split;  // k_stage_ph: CTAs specialised by output phase, one phase's bank each
+};
+// TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
+const std::vector<TmaVariant>& tma_variants();
+// Phase-split TMA stage kernels: pair banks whose four phases do not fit one CTA.
+const std::vector<TmaVariant>& ph_variants();
+
+using DownKernel = void (*)(const DownArgs, const DownParams);
+// FAST: the configs' bucket layout (16 orientations x 3 strength x 3 coherence bins)
+DownKernel down_kernel(bool hilo, bool dec, bool fast);
+DownKernel fixup_kernel(bool hilo, bool fast);
+
+}  // namespace tables
+}  // namespace blade
