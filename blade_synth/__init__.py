@@ -149,12 +149,14 @@ class Config:
                   self.n_disk, self.noise, self.p0, self.p1, out=out[i])
         return out
 
-    def taps(self, redraw_below: float = 4.0) -> np.ndarray:
-        """All stages: float32 [n_stages, 1 (filter channel), n_phases, K, nf^2 + nc^2]."""
+    def taps(self, redraw_below: float = 4.0, channels: int = 1) -> np.ndarray:
+        """All stages: float32 [n_stages, channels, n_phases, K, nf^2 + nc^2]. channels = 3 draws
+        independent per-channel (Y, Cb, Cr) banks (NEXT f1): channel c of stage s uses the bank
+        stream of stage index s + 1000 c; channel 0 equals the single-channel bank."""
         nc = self.coarse_size if self.levels > 1 else 0
-        st = [bank(self.seed, s, self.n_phases, self.K, self.fine_size, nc, redraw_below)[0]
-              for s in range(self.n_stages)]
-        return np.stack(st)[:, None]
+        st = [[bank(self.seed, s + 1000 * c, self.n_phases, self.K, self.fine_size, nc,
+                    redraw_below)[0] for c in range(channels)] for s in range(self.n_stages)]
+        return np.stack([np.stack(ch) for ch in st])
 
     def thresholds(self) -> tuple[np.ndarray, np.ndarray]:
         ts = np.asarray(self.strength_thresholds, dtype=np.float64).reshape(self.n_stages,

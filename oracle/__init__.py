@@ -9,6 +9,8 @@ imports it.
 
 Parity status per function (pins in tests/test_oracle_*.py):
   fold, decimate, tensor, eigen, quantize, selector, stage, denoise: pinned.
+  rgb_to_ycc, ycc_to_rgb, denoise_ycc (per-channel YCbCr banks, NEXT f1): pinned
+  (tests/test_oracle_ycc.py).
   Thresholds and scene generator are inputs, not results (parity unpinned by
   nature; they are produced by blade_synth and scripts/fit_thresholds.py).
 """
@@ -200,6 +202,57 @@ def denoise(z, L: int, nf: int, nc: int, n_phases: int, n_o: int, n_s: int, n_c:
     if rc:
         raise RuntimeError(f"oracle_denoise failed ({rc})")
     return out
+
+
+# ---------------------------------------------------------------- per-channel YCbCr path (NEXT f1)
+# PAPER.md:198-202 (§3 footnote 1): "images are converted to YCbCr (ITU-R BT.601). We train filters
+# separately on Y, Cb, and Cr while using the same filter selector s(.)". Full-range BT.601 with the
+# constants of SPEC.md:61 on the [0, 1] scale (offset 128/255; R25); the selector runs on
+# the noisy RGB levels (R26); the pyramid is decimated in RGB.
+YCC_OFFSET = 128.0 / 255.0
+
+
+def rgb_to_ycc(z) -> np.ndarray:
+    """(3,H,W) RGB -> YCbCr: Y = .299R + .587G + .114B, Cb = o + .564(B - Y), Cr = o + .713(R - Y)."""
+    z = _f64(z)
+    R, G, B = z
+    Y = 0.299 * R + 0.587 * G + 0.114 * B
+    return np.stack([Y, YCC_OFFSET + 0.564 * (B - Y), YCC_OFFSET + 0.713 * (R - Y)])
+
+
+def ycc_to_rgb(y) -> np.ndarray:
+    """Exact algebraic inverse of rgb_to_ycc."""
+    y = _f64(y)
+    Y, Cb, Cr = y
+    R = Y + (Cr - YCC_OFFSET) / 0.713
+    B = Y + (Cb - YCC_OFFSET) / 0.564
+    G = (Y - 0.299 * R - 0.114 * B) / 0.587
+    return np.stack([R, G, B])
+
+
+def denoise_ycc(z, L: int, nf: int, nc: int, n_phases: int, n_o: int, n_s: int, n_c: int, ts, tc,
+                taps, window_size: int = 5, window_sigma: float = 1.5) -> np.ndarray:
+    """Cascade with per-channel (Y, Cb, Cr) banks and the shared RGB selector, for ONE frame
+    (3, H, W) RGB -> (3, H, W) RGB fp64. taps: [n_stages, 3, n_phases, K, nt]."""
+    z = _f64(z)
+    taps = _f64(taps)
+    assert taps.ndim == 5 and taps.shape[1] == 3
+    ts, tc = _f64(ts), _f64(tc)
+    lv = pyramid(z, L)
+    nsel = 1 if L == 1 else L - 1
+    buckets = [selector(lv[l], n_o, n_s, n_c, ts[l], tc[l], window_size, window_sigma)
+               for l in range(nsel)]
+    ycc = [rgb_to_ycc(v) for v in lv]
+    if L == 1:
+        out = np.concatenate([stage(ycc[0][c:c + 1], None, buckets[0], taps[0, c], n_phases, nf, 0)
+                              for c in range(3)])
+    else:
+        u = ycc[L - 1]
+        for l in range(L - 2, -1, -1):
+            u = np.concatenate([stage(ycc[l][c:c + 1], u[c:c + 1], buckets[l], taps[l, c],
+                                      n_phases, nf, nc) for c in range(3)])
+        out = u
+    return ycc_to_rgb(out)
 
 
 def denoise_config(cfg, z, taps=None) -> np.ndarray:
