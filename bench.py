@@ -47,6 +47,8 @@ def parse():
                     help="override the frame count (profiling only; not a bench line)")
     ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ycc", action="store_true",
+                    help="per-channel Y/Cb/Cr banks (NEXT row f1) instead of one bank for R,G,B")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the oracle sample (cpu_baseline)")
@@ -256,7 +258,7 @@ def main():
         cfg.N = args.frames
     shard = shard_for(cfg, rank, world)
     H, W = cfg.H, cfg.W
-    h = BladeMS.from_config(cfg, device=local)
+    h = BladeMS.from_config(cfg, taps=cfg.taps(channels=3 if args.ycc else 1), device=local)
     stream = torch.cuda.current_stream(dev)
     if shard.mode == "frames":
         # ---- this rank's frames, generated on the host (seeded), copied once to HBM
@@ -432,6 +434,7 @@ def main():
             "config": {"workload": cfg.name, "desc": cfg.description, "frames": cfg.N,
                        "frames_per_gpu": n_local, "H": H, "W": W, "levels": cfg.levels,
                        "fine": cfg.fine_size, "coarse": cfg.coarse_size, "buckets": cfg.K,
+                       "filter_channels": "Y,Cb,Cr (f1)" if args.ycc else "shared R,G,B",
                        "parallelism": (f"frames split over {world} GPU(s), no collective"
                                        if shard.mode == "frames" else
                                        f"row bands over {world} GPU(s) with recomputed halo "

@@ -157,12 +157,14 @@ class BladeMS:
 
     @classmethod
     def from_config(cls, cfg, taps=None, device: int = 0, clamp_output: bool = False):
-        """Build from any object with the attributes of blade_synth.Config."""
+        """Build from any object with the attributes of blade_synth.Config; taps of shape
+        [n_stages, 3, n_phases, K, nt] select per-channel YCbCr banks (n_filter_channels = 3)."""
         ts, tc = cfg.thresholds()
         taps = cfg.taps() if taps is None else taps
+        nch = int(np.asarray(taps).shape[1]) if np.asarray(taps).ndim == 5 else 1
         return cls(cfg.levels, cfg.fine_size, cfg.coarse_size if cfg.levels > 1 else 0,
                    cfg.n_phases, cfg.n_orient, cfg.n_strength, cfg.n_coherence, ts, tc, taps,
-                   cfg.window_size, cfg.window_sigma, clamp_output, device)
+                   cfg.window_size, cfg.window_sigma, clamp_output, device, n_filter_channels=nch)
 
     # -------------------------------------------------------------------------------- queries
     def close(self):

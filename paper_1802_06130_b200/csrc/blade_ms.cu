@@ -426,7 +426,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
                                         p.u[l + 1]);
     LevelView outv = (l == 0) ? out_view
                               : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r);
-    const float* bank = h->d_bank + (size_t)l * h->cfg.n_phases * h->PS;
+    const float* bank = h->d_bank + (size_t)l * h->cfg.n_filter_channels * h->cfg.n_phases * h->PS;
     const int y_base = r.lo & ~1;
     const int clamp = (l == 0 && h->cfg.clamp_output) ? 1 : 0;
     ProfScope ps(h, st, 2, l);
@@ -506,11 +506,23 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     a.tiles_y = (r.hi - y_base + h->stage.trows - 1) / h->stage.trows;
     a.n_tiles = N * a.tiles_x * a.tiles_y;
     a.clamp = clamp;
+    // CTAs come in sets of rs (row parity) x 3 (channel, CH3) specialisations
+    const long long set = (long long)h->stage.rs * (h->stage.ch3 ? 3 : 1);
     long long grid = (long long)h->stage_ctas_per_sm * h->num_sms;
-    grid = std::min(grid, (long long)a.n_tiles * h->stage.rs);
-    if (h->stage.rs == 2) grid = std::max<long long>(2, grid & ~1LL);
+    grid = std::min(grid, (long long)a.n_tiles * set);
+    grid = std::max<long long>(set, grid / set * set);
+    a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
+    if (h->stage.ch3) a.clamp = 0;  // clamped after the colour conversion
     h->stage.fn<<<(unsigned)grid, dim3(32, h->stage.by), h->stage_smem, st>>>(a);
     LAUNCH_CHECK("k_stage");
+    if (h->stage.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
+      const long long per_frame = (long long)r.n() * p.W[0];
+      const long long total = (long long)N * per_frame;
+      const unsigned g2 = (unsigned)std::min<long long>((total + 255) / 256, 8LL * h->num_sms);
+      k_ycc_to_rgb<><<<g2, 256, 0, st>>>(outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane, outv.frame,
+                                       per_frame, N, h->cfg.clamp_output);
+      LAUNCH_CHECK("k_ycc_to_rgb");
+    }
   }
   return BLADE_OK;
 }
@@ -554,8 +566,6 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   if (c.levels == 1 && c.n_phases != 1) return fail(BLADE_EINVAL, "n_phases must be 1 when levels == 1");
   if (c.n_filter_channels != 1 && c.n_filter_channels != 3)
     return fail(BLADE_EINVAL, "n_filter_channels must be 1 or 3");
-  if (c.n_filter_channels == 3)
-    return fail(BLADE_EUNSUPPORTED, "per-channel (YCbCr) banks are not built (SURVEY.md §8 f1)");
   if (c.window_size < 1 || c.window_size > 5 || !(c.window_size & 1))
     return fail(BLADE_EINVAL, "window_size must be 1, 3 or 5");
   if (!(c.window_sigma > 0.0f) || !std::isfinite(c.window_sigma))
@@ -613,8 +623,9 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   const int want_rs = c.levels == 1 ? 1 : 2;
   const StageVariant* best = nullptr;
   size_t best_smem = 0;
+  const bool ch3 = c.n_filter_channels == 3;
   for (const auto& v : stage_variants()) {
-    if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs) continue;
+    if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs || v.ch3 != ch3) continue;
     const int nph_cta = c.n_phases == 4 ? (v.rs == 2 ? 2 : 4) : 1;
     const size_t smem = sizeof(float) * ((((size_t)nph_cta * PS) + 3) / 4 * 4 + (size_t)v.tile_floats);
     if (smem > (size_t)max_smem) continue;
@@ -644,7 +655,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->stage = *best;
   h->stage_smem = best_smem;
   for (const auto& v : tma_variants()) {
-    if (v.nf != c.fine_size || v.nc != cnc) continue;
+    if (ch3 || v.nf != c.fine_size || v.nc != cnc) continue;
     const size_t tps = (size_t)K * v.S;  // phase stride of the TMA tap layout (multiple of 4)
     const size_t bank = ((size_t)c.n_phases * tps * 4 + 127) & ~size_t(127);
     const size_t smem = 2 * (size_t)v.stage_bytes + bank + 16;
@@ -656,7 +667,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
       h->PS_tma = (int)tps;
     }
   }
-  if (!h->has_tma && c.levels > 1 && c.n_phases == 4) {
+  if (!h->has_tma && !ch3 && c.levels > 1 && c.n_phases == 4) {
     for (const auto& v : ph_variants()) {
       if (v.nf != c.fine_size || v.nc != cnc) continue;
       const size_t tps = (size_t)K * v.S;
@@ -709,16 +720,18 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     }
   }
 
-  // ---- bank re-layout: host [stage][ch=1][phase][K][nt] -> device [stage][phase][PS]
-  // generic kernel: [K][S] rows, taps in ABI order; TMA kernel: tma_tap_off layout
-  const size_t dev_floats = (size_t)n_stages * c.n_phases * PS;
+  // ---- bank re-layout: host [stage][ch][phase][K][nt] -> device [stage][ch][phase][PS]
+  // generic kernel: [K][S] rows, taps in ABI order; TMA kernel (one channel): tma_tap_off layout
+  const int nch = c.n_filter_channels;
+  const size_t dev_floats = (size_t)n_stages * nch * c.n_phases * PS;
   const size_t tma_floats = (size_t)n_stages * c.n_phases * h->PS_tma;
   std::vector<float> relaid(dev_floats, 0.0f), relaid_tma(tma_floats, 0.0f);
   for (int s = 0; s < n_stages; ++s)
+    for (int ch = 0; ch < nch; ++ch)
     for (int p = 0; p < c.n_phases; ++p)
       for (long long k = 0; k < K; ++k) {
-        const float* src = taps + (((size_t)s * c.n_phases + p) * K + k) * nt;
-        float* dst = relaid.data() + ((size_t)s * c.n_phases + p) * PS + (size_t)k * S;
+        const float* src = taps + ((((size_t)s * nch + ch) * c.n_phases + p) * K + k) * nt;
+        float* dst = relaid.data() + (((size_t)s * nch + ch) * c.n_phases + p) * PS + (size_t)k * S;
         memcpy(dst, src, sizeof(float) * nt);
         if (!h->has_tma) continue;
         float* dt = relaid_tma.data() + ((size_t)s * c.n_phases + p) * h->PS_tma + (size_t)k * h->S_tma;
@@ -851,7 +864,8 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
   (void)H;
   (void)W;
   const int L = h->cfg.levels;
-  *count = N == 0 ? 0 : 3 * (L == 1 ? 1 : L - 1);  // k_down + k_down_fixup + k_stage per stage level
+  // k_down + k_down_fixup + k_stage per stage level (+ the YCbCr -> RGB conversion with per-channel banks)
+  *count = N == 0 ? 0 : 3 * (L == 1 ? 1 : L - 1) + (h->cfg.n_filter_channels == 3 ? 1 : 0);
   return BLADE_OK;
 }
 

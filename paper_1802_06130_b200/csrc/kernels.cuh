@@ -68,9 +68,19 @@ struct StageArgs {
   int out_r0, out_rn;  // global output rows
   int tiles_x, tiles_y, n_tiles;
   int clamp;           // clamp output to [0, 1]
+  int u_rgb;           // CH3: the coarse input is RGB (z^{L-1}) rather than YCbCr planes
 };
 
-template <int NF, int NC, int RS, int BY>
+// Full-range BT.601 on the [0, 1] scale (R25), channel ch of (R, G, B).
+__device__ __forceinline__ float rgb_to_ycc_ch(int ch, float R, float G, float B) {
+  const float Y = fmaf(0.299f, R, fmaf(0.587f, G, 0.114f * B));
+  const float kO = 128.0f / 255.0f;
+  if (ch == 0) return Y;
+  if (ch == 1) return fmaf(0.564f, B - Y, kO);
+  return fmaf(0.713f, R - Y, kO);
+}
+
+template <int NF, int NC, int RS, int BY, bool CH3 = false>
 struct StageShape {
   static constexpr int BX = 32;
   static constexpr int RF = NF / 2, RC = NC / 2;
@@ -83,35 +93,43 @@ struct StageShape {
   static constexpr int CC = NC ? BX + 2 * RC : 0;
   static constexpr int CCP = NC ? CC + 1 : 0;
   static constexpr int NPH_CTA = RS == 2 ? 2 : 4;  // phases a CTA holds when n_phases == 4
-  static constexpr int tile_floats = 3 * FR * FCP + 3 * CR * CCP;
+  static constexpr int PL = CH3 ? 1 : 3;            // staged planes (CH3: the CTA's channel only)
+  static constexpr int tile_floats = PL * FR * FCP + PL * CR * CCP;
   static constexpr int threads = BX * BY;
 };
 
-template <int NF, int NC, int RS, int BY>
+// CH3 (per-channel YCbCr banks, NEXT f1): CTAs are also specialised by channel c (Y, Cb, Cr); the
+// fine patch (RGB z^l) is converted to channel c while staged, the coarse patch too when it is
+// z^{L-1} (RGB), else it is plane c of the YCbCr u^{l+1}; the output is plane c of a YCbCr u^l
+// (level 0 is converted back to RGB by k_ycc_to_rgb).
+template <int NF, int NC, int RS, int BY, bool CH3>
 __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
-  using SS = StageShape<NF, NC, RS, BY>;
+  using SS = StageShape<NF, NC, RS, BY, CH3>;
+  constexpr int PL = SS::PL;
   constexpr int RF = SS::RF, RC = SS::RC;
   extern __shared__ __align__(16) float smem[];
   const int nph_cta = a.n_phases == 4 ? SS::NPH_CTA : 1;
   const int bank_floats = nph_cta * a.PS;
   float* sbank = smem;
   float* sfine = smem + ((bank_floats + 3) & ~3);
-  float* scoarse = sfine + 3 * SS::FR * SS::FCP;
+  float* scoarse = sfine + PL * SS::FR * SS::FCP;
 
   const int par = RS == 2 ? (int)(blockIdx.x & 1) : 0;  // output-row parity of this CTA
-  const int group = RS == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int ngroups = RS == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int rest = RS == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int chn = CH3 ? rest % 3 : 0;                    // filter channel of this CTA
+  const int group = CH3 ? rest / 3 : rest;
+  const int ngroups = (int)gridDim.x / (RS * (CH3 ? 3 : 1));
   const int tid = threadIdx.y * SS::BX + threadIdx.x;
 
   // ---- filterbank -> shared memory, once per CTA
   {
     const int ph0 = (a.n_phases == 4 && RS == 2) ? 2 * par : 0;
-    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)ph0 * a.PS);
+    const long long boff = (long long)(chn * a.n_phases + ph0) * a.PS;
+    const float4* g4 = reinterpret_cast<const float4*>(a.bank + boff);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     const int n4 = bank_floats >> 2;
     for (int i = tid; i < n4; i += SS::threads) s4[i] = __ldg(g4 + i);
-    for (int i = (n4 << 2) + tid; i < bank_floats; i += SS::threads)
-      sbank[i] = __ldg(a.bank + (long long)ph0 * a.PS + i);
+    for (int i = (n4 << 2) + tid; i < bank_floats; i += SS::threads) sbank[i] = __ldg(a.bank + boff + i);
   }
 
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -131,9 +149,14 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
       for (int i = tid; i < SS::FR * SS::FC; i += SS::threads) {
         const int r = i / SS::FC, q = i - r * SS::FC;
         const long long ro = (long long)view_row(a.z, Y0 - RF + r) * a.z.W + fold_idx(X0 - RF + q, a.z.W);
+        if constexpr (CH3) {
+          sfine[r * SS::FCP + q] =
+              rgb_to_ycc_ch(chn, __ldg(zp + ro), __ldg(zp + a.z.plane + ro), __ldg(zp + 2 * a.z.plane + ro));
+        } else {
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          sfine[(c * SS::FR + r) * SS::FCP + q] = __ldg(zp + c * a.z.plane + ro);
+          for (int c = 0; c < 3; ++c)
+            sfine[(c * SS::FR + r) * SS::FCP + q] = __ldg(zp + c * a.z.plane + ro);
+        }
       }
     }
     if constexpr (NC > 0) {
@@ -142,9 +165,15 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
       for (int i = tid; i < SS::CR * SS::CC; i += SS::threads) {
         const int r = i / SS::CC, q = i - r * SS::CC;
         const long long ro = (long long)view_row(a.u1, CY0 + r) * a.u1.W + fold_idx(CX0 + q, a.u1.W);
+        if constexpr (CH3) {
+          scoarse[r * SS::CCP + q] =
+              a.u_rgb ? rgb_to_ycc_ch(chn, __ldg(up + ro), __ldg(up + a.u1.plane + ro), __ldg(up + 2 * a.u1.plane + ro))
+                      : __ldg(up + chn * a.u1.plane + ro);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          scoarse[(c * SS::CR + r) * SS::CCP + q] = __ldg(up + c * a.u1.plane + ro);
+          for (int c = 0; c < 3; ++c)
+            scoarse[(c * SS::CR + r) * SS::CCP + q] = __ldg(up + c * a.u1.plane + ro);
+        }
       }
     }
     __syncthreads();
@@ -171,13 +200,13 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
         tp[i][j] = sbank + ps * a.PS + k * a.S;
       }
 
-    float acc[2][2][3];
+    float acc[2][2][PL];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[i][j][c] = 0.0f;
+        for (int c = 0; c < PL; ++c) acc[i][j][c] = 0.0f;
 
     // coarse term first (matches nothing in particular; any order is a valid fp32 sum)
     if constexpr (NC > 0) {
@@ -186,9 +215,9 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
 #pragma unroll
       for (int wr = 0; wr < NC + (RS == 2 ? 1 : 0); ++wr) {
         const int crow = (ly >> 1) + wr;  // local coarse row
-        float v[3][NC];
+        float v[PL][NC];
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < PL; ++c)
 #pragma unroll
           for (int q = 0; q < NC; ++q) v[c][q] = scoarse[(c * SS::CR + crow) * SS::CCP + cx + q];
 #pragma unroll
@@ -201,7 +230,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
             for (int dx = 0; dx < NC; ++dx) {
               const float tap = tp[i][j][NF * NF + dy * NC + dx];
 #pragma unroll
-              for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][dx], acc[i][j][c]);
+              for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(tap, v[c][dx], acc[i][j][c]);
             }
         }
       }
@@ -210,9 +239,9 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
 #pragma unroll
     for (int wr = 0; wr < NF + RS; ++wr) {
       const int frow = ly + wr;  // local fine row (tile origin is Y0 - RF)
-      float v[3][NF + 1];
+      float v[PL][NF + 1];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
+      for (int c = 0; c < PL; ++c) {
         const float* rp = sfine + (c * SS::FR + frow) * SS::FCP + 2 * tx;
 #pragma unroll
         for (int q = 0; q + 1 < NF + 1; q += 2) {
@@ -232,7 +261,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
           for (int dx = 0; dx < NF; ++dx) {
             const float tap = tp[i][j][dy * NF + dx];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(tap, v[c][j + dx], acc[i][j][c]);
+            for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(tap, v[c][j + dx], acc[i][j][c]);
           }
       }
     }
@@ -244,13 +273,13 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
       if (!row_ok[i]) continue;
       const long long ro = (long long)(y0 + i * RS - a.out.row0) * a.out.W;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
+      for (int c = 0; c < PL; ++c) {
         float v0 = acc[i][0][c], v1 = acc[i][1][c];
         if (a.clamp) {
           v0 = fminf(fmaxf(v0, 0.0f), 1.0f);
           v1 = fminf(fmaxf(v1, 0.0f), 1.0f);
         }
-        float* d = op + c * a.out.plane + ro + x;
+        float* d = op + (CH3 ? chn : c) * a.out.plane + ro + x;
         if (col_ok[1] && ((reinterpret_cast<uintptr_t>(d) & 7) == 0)) {
           *reinterpret_cast<float2*>(d) = make_float2(v0, v1);
         } else {
@@ -259,6 +288,31 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
         }
       }
     }
+  }
+}
+
+// YCbCr -> RGB in place over rows [0, rows) of a level view (exact inverse of rgb_to_ycc_ch up
+// to fp32 rounding; R25), with the optional final clamp.
+template <int = 0>
+__global__ void k_ycc_to_rgb(float* p, long long plane, long long frame, long long per_frame, int N, int clamp) {
+  const long long total = (long long)N * per_frame;
+  const float kO = 128.0f / 255.0f;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long n = i / per_frame, o = i - n * per_frame;
+    float* q = p + n * frame + o;
+    const float Y = q[0], Cb = q[plane], Cr = q[2 * plane];
+    float R = Y + (Cr - kO) / 0.713f;
+    float B = Y + (Cb - kO) / 0.564f;
+    float G = (Y - 0.299f * R - 0.114f * B) / 0.587f;
+    if (clamp) {
+      R = fminf(fmaxf(R, 0.0f), 1.0f);
+      G = fminf(fmaxf(G, 0.0f), 1.0f);
+      B = fminf(fmaxf(B, 0.0f), 1.0f);
+    }
+    q[0] = R;
+    q[plane] = G;
+    q[2 * plane] = B;
   }
 }
 

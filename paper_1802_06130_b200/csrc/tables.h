@@ -18,6 +18,7 @@ struct StageVariant {
   int nf, nc, rs, by;
   StageKernel fn;
   int tile_floats, threads, trows, tcols;
+  bool ch3;  // per-channel (Y, Cb, Cr) banks: CTAs specialised by channel (NEXT f1)
 };
 // Generic stage kernels (any shape; row-parity CTAs for the big pair banks).
 const std::vector<StageVariant>& stage_variants();

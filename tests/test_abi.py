@@ -68,7 +68,8 @@ EINVAL, ENONFINITE, ESHAPE, EDEVICE, EUNSUP = 1, 2, 3, 4, 7
     (dict(tc=[0.3, np.nan, 0.3, 0.6]), ENONFINITE),
     (dict(ntaps=7), ESHAPE),
     (dict(K=(16, 4, 5)), EUNSUP),              # K = 320 > 256 (uint8 maps)
-    (dict(n_filter_channels=3), EUNSUP),       # per-channel YCbCr banks (NEXT f1)
+    (dict(n_filter_channels=3), ESHAPE),       # per-channel banks need 3x the taps
+    (dict(n_filter_channels=2), EINVAL),
 ])
 def test_create_rejects_bad_arguments(kw, status):
     rc, h = _create(**kw)

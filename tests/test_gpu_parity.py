@@ -261,3 +261,49 @@ def test_no_writes_outside_buffers(name, H, W, N):
     maps = h.selector(x, workspace=ws_buf[:ws_n])
     torch.cuda.synchronize()
     assert bool((ws_buf[ws_n:] == 0xA5).all())
+
+
+# ------------------------------------------------------------------------- per-channel YCbCr (f1)
+
+@pytest.mark.parametrize("name,H,W,N", [("c0", 64, 64, 1), ("c1", 203, 333, 2), ("c2", 151, 97, 1),
+                                        ("c4", 77, 190, 1), ("c3", 256, 384, 1)])
+def test_ycc_channel_banks_parity(name, H, W, N):
+    """NEXT f1: per-channel Y/Cb/Cr banks with the shared RGB selector against the oracle's
+    denoise_ycc (same parity rule: outputs within 1e-4 outside the cone of bucket mismatches)."""
+    cfg = _cfg_like(name, H, W, N)
+    taps = cfg.taps(channels=3)
+    h = _handle(cfg, taps)
+    x_np = cfg.batch()
+    x = torch.from_numpy(x_np).cuda()
+    out = h.denoise(x).cpu().numpy()
+    maps = [m.cpu().numpy() for m in h.selector(x)]
+    ts, tc = cfg.thresholds()
+    for n in range(N):
+        parts = oracle.cascade_parts(cfg, x_np[n], taps[:, :1])
+        ref = oracle.denoise_ycc(x_np[n], cfg.levels, cfg.fine_size, cfg.coarse_size, cfg.n_phases,
+                                 cfg.n_orient, cfg.n_strength, cfg.n_coherence, ts, tc, taps)
+        mism = [check_buckets(maps[l][n], parts["buckets"][l], parts["features"][l], cfg.n_orient,
+                              ts[l], tc[l], f"{name} ycc level {l}")[0]
+                for l in range(len(parts["buckets"]))]
+        dims = [p.shape[1:] for p in parts["levels"]]
+        tainted = taint_cone(mism, dims, cfg.coarse_size // 2) if cfg.levels > 1 else mism[0]
+        err = max_err_outside(out[n], ref, tainted)
+        assert err <= OUT_ATOL, f"{name} ycc frame {n}: max |gpu - oracle| = {err}"
+
+
+def test_ycc_equal_banks_match_rgb_path():
+    cfg = _cfg_like("c1", 130, 200, 2)
+    t1 = cfg.taps()
+    x = torch.from_numpy(cfg.batch()).cuda()
+    rgb = _handle(cfg, t1).denoise(x)
+    ycc = _handle(cfg, np.repeat(t1, 3, axis=1)).denoise(x)
+    assert float((rgb - ycc).abs().max()) < 1e-5
+
+
+def test_ycc_clamp_applies_after_conversion():
+    cfg = _cfg_like("c1", 64, 64, 1)
+    taps = cfg.taps(channels=3)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    raw = _handle(cfg, taps).denoise(x)
+    cl = _handle(cfg, taps, clamp_output=True).denoise(x)
+    assert torch.equal(cl, raw.clamp(0, 1))
