@@ -464,7 +464,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       a.out = outv.p;
       a.out_row0 = outv.row0;
       a.out_rows = outv.rows;
-      a.bank = h->d_bank_tma + (size_t)l * h->cfg.n_phases * h->PS_tma;
+      a.bank = h->d_bank_tma + (size_t)l * h->cfg.n_filter_channels * h->cfg.n_phases * h->PS_tma;
       a.K = h->K;
       a.S = h->S_tma;
       a.PS = h->PS_tma;
@@ -477,14 +477,25 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       a.tiles_y = (r.hi - y_base + tv.trows - 1) / tv.trows;
       a.n_tiles = N * a.tiles_x * a.tiles_y;
       a.clamp = clamp;
-      if (tv.phase_split) {  // 4 phase-CTAs per tile group, 2 workers (groups) per CTA
-        const int per_phase = std::max(1, std::min(h->num_sms / 4, (a.n_tiles + 1) / 2));
-        tv.fn<<<4 * per_phase, dim3(32, 8), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+      if (tv.phase_split) {  // 4 phase-CTAs (x 3 channels) per tile group, 2 workers per CTA
+        const int types = tv.ch3 ? 12 : 4;
+        const int per_type = std::max(1, std::min(h->num_sms / types, (a.n_tiles + 1) / 2));
+        a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
+        if (tv.ch3) a.clamp = 0;  // clamped after the colour conversion
+        tv.fn<<<types * per_type, dim3(32, 8), h->tma_smem, st>>>(tmz, tmu, tmm, a);
       } else {
         const int grid = std::min(h->num_sms, (a.n_tiles + tv.groups - 1) / tv.groups);
         tv.fn<<<grid, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
       }
       LAUNCH_CHECK("k_stage_tma");
+      if (tv.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
+        const long long per_frame = (long long)r.n() * p.W[0];
+        const long long total = (long long)N * per_frame;
+        const unsigned g2 = (unsigned)std::min<long long>((total + 255) / 256, 8LL * h->num_sms);
+        k_ycc_to_rgb<><<<g2, 256, 0, st>>>(outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane,
+                                           outv.frame, per_frame, N, h->cfg.clamp_output);
+        LAUNCH_CHECK("k_ycc_to_rgb");
+      }
       continue;
     }
     StageArgs a{};
@@ -667,9 +678,9 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
       h->PS_tma = (int)tps;
     }
   }
-  if (!h->has_tma && !ch3 && c.levels > 1 && c.n_phases == 4) {
+  if (!h->has_tma && c.levels > 1 && c.n_phases == 4) {
     for (const auto& v : ph_variants()) {
-      if (v.nf != c.fine_size || v.nc != cnc) continue;
+      if (v.nf != c.fine_size || v.nc != cnc || v.ch3 != ch3) continue;
       const size_t tps = (size_t)K * v.S;
       const size_t smem = 2 * (size_t)v.stage_bytes + ((tps * 4 + 127) & ~size_t(127)) + 16;
       if (smem <= (size_t)max_smem && get_encode()) {
@@ -724,7 +735,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   // generic kernel: [K][S] rows, taps in ABI order; TMA kernel (one channel): tma_tap_off layout
   const int nch = c.n_filter_channels;
   const size_t dev_floats = (size_t)n_stages * nch * c.n_phases * PS;
-  const size_t tma_floats = (size_t)n_stages * c.n_phases * h->PS_tma;
+  const size_t tma_floats = (size_t)n_stages * nch * c.n_phases * h->PS_tma;
   std::vector<float> relaid(dev_floats, 0.0f), relaid_tma(tma_floats, 0.0f);
   for (int s = 0; s < n_stages; ++s)
     for (int ch = 0; ch < nch; ++ch)
@@ -734,7 +745,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
         float* dst = relaid.data() + (((size_t)s * nch + ch) * c.n_phases + p) * PS + (size_t)k * S;
         memcpy(dst, src, sizeof(float) * nt);
         if (!h->has_tma) continue;
-        float* dt = relaid_tma.data() + ((size_t)s * c.n_phases + p) * h->PS_tma + (size_t)k * h->S_tma;
+        float* dt = relaid_tma.data() + (((size_t)s * nch + ch) * c.n_phases + p) * h->PS_tma + (size_t)k * h->S_tma;
         for (int dy = 0; dy < c.fine_size; ++dy)
           for (int dx = 0; dx < c.fine_size; ++dx)
             dt[tma_tap_off(c.fine_size, cnc, 0, dy, dx)] = src[dy * c.fine_size + dx];

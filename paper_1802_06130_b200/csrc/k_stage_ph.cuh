@@ -47,12 +47,16 @@ struct PhShape {
 
 // One tile of phase (py, PX) by one 128-thread group: fix-up of border cells, then the 2 x 2
 // sub-lattice block of each thread.
-template <int NF, int NC, int PX>
+// CH3 (per-channel Y/Cb/Cr banks, NEXT f1): the CTA also serves one channel chn; after the
+// fix-up the fine patch (RGB z^l) is converted to channel chn in plane 0, the coarse patch too
+// when it is z^{L-1} (RGB), else plane chn of the YCbCr u^{l+1} is read; one accumulator per pixel.
+template <int NF, int NC, int PX, bool CH3>
 __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, int Y0, int py, float* sfine,
                                        float* scoarse, const uint8_t* smap, const float* sbank, int tid,
-                                       int tx, int ty, int g) {
+                                       int tx, int ty, int g, int chn) {
   using SS = PhShape<NF, NC>;
   constexpr int RF = SS::RF, RC = SS::RC;
+  constexpr int PL = CH3 ? 1 : 3;
   auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(SS::threads) : "memory"); };
   const int FY = Y0 + py - RF, FX = X0 - SS::FM;          // fine box origin
   const int CY = Y0 / 2 - RC, CX = X0 / 2 - SS::CM;       // coarse box origin
@@ -103,6 +107,18 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
     }
     group_sync();
   }
+  const float* scoarse_c = scoarse;
+  if constexpr (CH3) {  // colour conversion of the staged patches into plane 0
+    for (int i = tid; i < SS::FR * SS::FCB; i += SS::threads)
+      sfine[i] = rgb_to_ycc_ch(chn, sfine[i], sfine[SS::FR * SS::FCB + i], sfine[2 * SS::FR * SS::FCB + i]);
+    if (a.u_rgb) {
+      for (int i = tid; i < SS::CR * SS::CCB; i += SS::threads)
+        scoarse[i] = rgb_to_ycc_ch(chn, scoarse[i], scoarse[SS::CR * SS::CCB + i], scoarse[2 * SS::CR * SS::CCB + i]);
+    } else {
+      scoarse_c = scoarse + chn * SS::CR * SS::CCB;
+    }
+    group_sync();
+  }
 
   // ---- this thread's 2 x 2 sub-lattice block: image pixels (Y0 + py + 4 ty + 2 i, X0 + PX + 4 tx + 2 j)
   const float* tp[2][2];
@@ -113,23 +129,23 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
       const int k = smap[(py + 4 * ty + 2 * i) * SS::TCOLS + PX + 4 * tx + 2 * j];
       tp[i][j] = sbank + k * SS::S;
     }
-  float acc[2][2][3];
+  float acc[2][2][PL];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) acc[i][j][c] = 0.0f;
+      for (int c = 0; c < PL; ++c) acc[i][j][c] = 0.0f;
 
   // coarse: pixel (i, j) has centre (Y0/2 + 2ty + i, X0/2 + 2tx + j); window rows 2ty + i + dy,
   // columns (box) 2tx + j + dx + CM - RC
   constexpr int CO = SS::CM - RC;
 #pragma unroll
   for (int wr = 0; wr < NC + 1; ++wr) {
-    float v[3][SS::CW];
+    float v[PL][SS::CW];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
-      lds_run<(CO & 1), SS::CW, 2>(scoarse + (c * SS::CR + 2 * ty + wr) * SS::CCB + 2 * tx + CO, v[c]);
+    for (int c = 0; c < PL; ++c)
+      lds_run<(CO & 1), SS::CW, 2>(scoarse_c + (c * SS::CR + 2 * ty + wr) * SS::CCB + 2 * tx + CO, v[c]);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int dy = wr - i;
@@ -141,7 +157,7 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
 #pragma unroll
         for (int dx = 0; dx < NC; ++dx)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][j + dx], acc[i][j][c]);
+          for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(t[dx], v[c][j + dx], acc[i][j][c]);
       }
     }
   }
@@ -150,9 +166,9 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
   constexpr int FO = PX + SS::FM - RF;
 #pragma unroll
   for (int wr = 0; wr < NF + 2; ++wr) {
-    float v[3][SS::FW];
+    float v[PL][SS::FW];
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < PL; ++c)
       lds_run<(FO & 3), SS::FW>(sfine + (c * SS::FR + 4 * ty + wr) * SS::FCB + 4 * tx + FO, v[c]);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -165,7 +181,7 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
 #pragma unroll
         for (int dx = 0; dx < NF; ++dx)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][2 * j + dx], acc[i][j][c]);
+          for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(t[dx], v[c][2 * j + dx], acc[i][j][c]);
       }
     }
   }
@@ -181,18 +197,18 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
       if (xx >= a.W) continue;
       float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.W + xx;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
+      for (int c = 0; c < PL; ++c) {
         float v = acc[i][j][c];
         if (a.clamp) v = fminf(fmaxf(v, 0.0f), 1.0f);
-        op[(long long)c * a.out_rows * a.W] = v;
+        op[(long long)(CH3 ? chn : c) * a.out_rows * a.W] = v;
       }
     }
   }
 }
 
-// grid: 4 * m CTAs (CTA b serves phase b % 4), 256 threads = 2 groups of 128; n_tiles counts the
-// 16 x 128 image tiles; each phase's 2m workers stride over them.
-template <int NF, int NC>
+// grid: 4 * m CTAs (CTA b serves phase b % 4; with CH3 12 * m, channel (b / 4) % 3), 256 threads =
+// 2 groups of 128; n_tiles counts the 16 x 128 image tiles; each type's 2m workers stride over them.
+template <int NF, int NC, bool CH3>
 __global__ void __launch_bounds__(256, 1)
     k_stage_ph(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
@@ -205,11 +221,13 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* mbar = reinterpret_cast<uint64_t*>(ph_smem + 2 * SS::stage_bytes + ((bank_floats * 4 + 127) & ~127));
 
   const int p = blockIdx.x & 3, py = p >> 1, px = p & 1;
+  const int chn = CH3 ? (int)(blockIdx.x >> 2) % 3 : 0;   // filter channel (CH3)
+  const int ci = CH3 ? (int)(blockIdx.x >> 2) / 3 : (int)(blockIdx.x >> 2);  // CTA index within its type
   const int g = threadIdx.y >> 2;                          // group (0, 1)
   const int tx = threadIdx.x, ty = threadIdx.y & 3;
   const int tid = ty * SS::BX + tx;                        // within the group
   const int ctid = threadIdx.y * SS::BX + threadIdx.x;
-  const int cpp = gridDim.x >> 2;                          // CTAs per phase
+  const int cpp = gridDim.x / (CH3 ? 12 : 4);              // CTAs per (phase, channel) type
   const int workers = 2 * cpp;
   constexpr uint32_t tx_bytes = SS::fine_bytes + SS::coarse_bytes + SS::map_bytes;
 
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[g]);
   };
 
-  int t = (blockIdx.x >> 2) * 2 + g;
+  int t = ci * 2 + g;
   if (ctid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -239,7 +257,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (tid == 0 && t < a.n_tiles) issue(t);
   {
-    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)p * a.PS);
+    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)(chn * 4 + p) * a.PS);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     for (int i = ctid; i < (bank_floats >> 2); i += 2 * SS::threads) s4[i] = __ldg(g4 + i);
   }
@@ -253,9 +271,9 @@ __global__ void __launch_bounds__(256, 1)
     float* scoarse = reinterpret_cast<float*>(buf0 + g * SS::stage_bytes + SS::coarse_off);
     const uint8_t* smap = buf0 + g * SS::stage_bytes + SS::map_off;
     if (px)
-      ph_tile<NF, NC, 1>(a, n, X0, Y0, py, sfine, scoarse, smap, sbank, tid, tx, ty, g);
+      ph_tile<NF, NC, 1, CH3>(a, n, X0, Y0, py, sfine, scoarse, smap, sbank, tid, tx, ty, g, chn);
     else
-      ph_tile<NF, NC, 0>(a, n, X0, Y0, py, sfine, scoarse, smap, sbank, tid, tx, ty, g);
+      ph_tile<NF, NC, 0, CH3>(a, n, X0, Y0, py, sfine, scoarse, smap, sbank, tid, tx, ty, g, chn);
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(SS::threads) : "memory");  // buffer free
     if (tid == 0 && t + workers < a.n_tiles) {
       fence_proxy_async();

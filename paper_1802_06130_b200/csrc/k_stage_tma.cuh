@@ -160,6 +160,7 @@ struct StageTmaArgs {
   int o_r0, o_rn;      // output rows computed
   int tiles_x, tiles_y, n_tiles;
   int clamp;
+  int u_rgb;           // CH3 (k_stage_ph): the coarse input is RGB z^{L-1}, not YCbCr planes
 };
 
 // G = 1: one 256-thread group, double-buffered tiles (TMA of tile i+1 overlaps tile i).

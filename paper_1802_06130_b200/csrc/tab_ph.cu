@@ -3,15 +3,18 @@
 
 namespace blade {
 namespace tables {
-template <int NF, int NC>
+template <int NF, int NC, bool CH3 = false>
 static TmaVariant make_ph() {
   using SS = PhShape<NF, NC>;
-  return TmaVariant{NF, NC, 2, &k_stage_ph<NF, NC>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, true};
+  return TmaVariant{NF, NC, 2, &k_stage_ph<NF, NC, CH3>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, true, CH3};
 }
 const std::vector<TmaVariant>& ph_variants() {
   static const std::vector<TmaVariant> v = {
       make_ph<7, 7>(), make_ph<9, 9>(), make_ph<7, 5>(), make_ph<9, 7>(), make_ph<5, 7>(), make_ph<7, 9>(),
+      // per-channel YCbCr banks (NEXT f1) for the large footprints; smaller ones stay on the generic
+      // kernel, where one CTA type (of 12) per tile leaves too little work per TMA tile
+      make_ph<7, 7, true>(), make_ph<9, 9, true>(), make_ph<7, 5, true>(), make_ph<9, 7, true>(),
   };
   return v;
 }

@@ -10,7 +10,7 @@ template <int NF, int NC, int G = BLADE_TMA_GROUPS>
 static TmaVariant make_tma() {
   using SS = TmaShape<NF, NC>;
   return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false};
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, false};
 }
 const std::vector<TmaVariant>& tma_variants() {
   static const std::vector<TmaVariant> v = {

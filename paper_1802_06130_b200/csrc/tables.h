@@ -29,6 +29,7 @@ struct TmaVariant {
   TmaKernel fn;
   int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc, S;
   bool phase_split;  // k_stage_ph: CTAs specialised by output phase, one phase's bank each
+  bool ch3;          // per-channel (Y, Cb, Cr) banks (k_stage_ph only)
 };
 // TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
 const std::vector<TmaVariant>& tma_variants();

@@ -266,7 +266,9 @@ def test_no_writes_outside_buffers(name, H, W, N):
 # ------------------------------------------------------------------------- per-channel YCbCr (f1)
 
 @pytest.mark.parametrize("name,H,W,N", [("c0", 64, 64, 1), ("c1", 203, 333, 2), ("c2", 151, 97, 1),
-                                        ("c4", 77, 190, 1), ("c3", 256, 384, 1)])
+                                        ("c4", 77, 190, 1), ("c3", 256, 384, 1),
+                                        # widths % 16 == 0: the TMA phase-split kernel (k_stage_ph)
+                                        ("c1", 160, 256, 2), ("c2", 128, 192, 1), ("c4", 96, 256, 1)])
 def test_ycc_channel_banks_parity(name, H, W, N):
     """NEXT f1: per-channel Y/Cb/Cr banks with the shared RGB selector against the oracle's
     denoise_ycc (same parity rule: outputs within 1e-4 outside the cone of bucket mismatches)."""
