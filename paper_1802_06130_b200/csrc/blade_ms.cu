@@ -483,6 +483,11 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
         a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
         if (tv.ch3) a.clamp = 0;  // clamped after the colour conversion
         tv.fn<<<types * per_type, dim3(32, 8), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+      } else if (tv.ch3) {  // CTA b serves channel b % 3
+        const int per_ch = std::max(1, std::min(h->num_sms / 3, (a.n_tiles + tv.groups - 1) / tv.groups));
+        a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
+        a.clamp = 0;  // clamped after the colour conversion
+        tv.fn<<<3 * per_ch, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
       } else {
         const int grid = std::min(h->num_sms, (a.n_tiles + tv.groups - 1) / tv.groups);
         tv.fn<<<grid, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
@@ -666,7 +671,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->stage = *best;
   h->stage_smem = best_smem;
   for (const auto& v : tma_variants()) {
-    if (ch3 || v.nf != c.fine_size || v.nc != cnc) continue;
+    if (v.ch3 != ch3 || v.nf != c.fine_size || v.nc != cnc) continue;
     const size_t tps = (size_t)K * v.S;  // phase stride of the TMA tap layout (multiple of 4)
     const size_t bank = ((size_t)c.n_phases * tps * 4 + 127) & ~size_t(127);
     const size_t smem = 2 * (size_t)v.stage_bytes + bank + 16;

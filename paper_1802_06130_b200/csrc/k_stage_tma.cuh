@@ -167,12 +167,19 @@ struct StageTmaArgs {
 // G = 2: two 256-thread groups (16 warps) share the bank; each group owns one tile buffer and works
 //        on every other tile, so one group computes while the other waits for its TMA (twice the
 //        resident warps for the same shared memory).
-template <int NF, int NC, int G>
+// CH3 (per-channel Y/Cb/Cr banks, NEXT f1): CTA b serves channel b % 3 (all four phases of that
+// channel's bank); the staged patches are converted to that channel in plane 0 after the fix-up
+// (the coarse patch only when it is the RGB z^{L-1}; else plane chn of the YCbCr u^{l+1} is read).
+template <int NF, int NC, int G, bool CH3>
 __global__ void __launch_bounds__(256 * G, 1)
     k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
   using SS = TmaShape<NF, NC>;
   constexpr int RF = SS::RF, RC = SS::RC;
+  constexpr int PL = CH3 ? 1 : 3;
+  const int chn = CH3 ? (int)(blockIdx.x % 3) : 0;
+  const int cta = CH3 ? (int)(blockIdx.x / 3) : (int)blockIdx.x;
+  const int nctas = CH3 ? (int)(gridDim.x / 3) : (int)gridDim.x;
   extern __shared__ __align__(128) unsigned char tma_smem[];
   // layout: [stage buffers x2][bank][mbarriers]
   unsigned char* buf0 = tma_smem;
@@ -210,8 +217,8 @@ __global__ void __launch_bounds__(256 * G, 1)
   };
 
   const int ctid = threadIdx.y * SS::BX + threadIdx.x;
-  int t = blockIdx.x + g * gridDim.x;
-  const int tstride = G * gridDim.x;
+  int t = cta + g * nctas;
+  const int tstride = G * nctas;
   if (ctid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(256 * G, 1)
   if (tid == 0 && t < a.n_tiles) issue(t, g);
   // ---- the bank -> shared memory, once
   {
-    const float4* g4 = reinterpret_cast<const float4*>(a.bank);
+    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)chn * bank_floats);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     for (int i = ctid; i < (bank_floats >> 2); i += SS::threads * G) s4[i] = __ldg(g4 + i);
   }
@@ -294,6 +301,20 @@ __global__ void __launch_bounds__(256 * G, 1)
       }
       group_sync();
     }
+    const float* scoarse_c = scoarse;
+    if constexpr (CH3) {  // colour conversion of the staged patches into plane 0
+      for (int i = tid; i < SS::FR * SS::FCB; i += SS::threads)
+        sfine[i] = rgb_to_ycc_ch(chn, sfine[i], sfine[SS::FR * SS::FCB + i], sfine[2 * SS::FR * SS::FCB + i]);
+      if constexpr (NC > 0) {
+        if (a.u_rgb) {
+          for (int i = tid; i < SS::CR * SS::CCB; i += SS::threads)
+            scoarse[i] = rgb_to_ycc_ch(chn, scoarse[i], scoarse[SS::CR * SS::CCB + i], scoarse[2 * SS::CR * SS::CCB + i]);
+        } else {
+          scoarse_c = scoarse + chn * SS::CR * SS::CCB;
+        }
+      }
+      group_sync();
+    }
 
     // ---- this thread's 2 x 4 block
     const int x = X0 + SS::RX * tx;
@@ -309,22 +330,22 @@ __global__ void __launch_bounds__(256 * G, 1)
       tp[0][j] = sbank + ph0 * a.PS + k0 * SS::S;
       tp[1][j] = sbank + ph1 * a.PS + k1 * SS::S;
     }
-    float acc[2][4][3];
+    float acc[2][4][PL];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[i][j][c] = 0.0f;
+        for (int c = 0; c < PL; ++c) acc[i][j][c] = 0.0f;
 
     if constexpr (NC > 0) {
       // coarse rows local ty .. ty+NC-1 (both pixel rows share floor(y/2)); cols 2tx .. 2tx+NC
 #pragma unroll
       for (int wr = 0; wr < NC; ++wr) {
-        float v[3][SS::CWIN];
+        float v[PL][SS::CWIN];
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-          lds_run<(SS::CO & 1), SS::CWIN, 2>(scoarse + (c * SS::CR + ty + wr) * SS::CCB + 2 * tx + SS::CO, v[c]);
+        for (int c = 0; c < PL; ++c)
+          lds_run<(SS::CO & 1), SS::CWIN, 2>(scoarse_c + (c * SS::CR + ty + wr) * SS::CCB + 2 * tx + SS::CO, v[c]);
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -334,7 +355,7 @@ __global__ void __launch_bounds__(256 * G, 1)
 #pragma unroll
             for (int dx = 0; dx < NC; ++dx) {
 #pragma unroll
-              for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][(j >> 1) + dx], acc[i][j][c]);
+              for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(t[dx], v[c][(j >> 1) + dx], acc[i][j][c]);
             }
           }
       }
@@ -342,9 +363,9 @@ __global__ void __launch_bounds__(256 * G, 1)
     // fine rows local 2ty .. 2ty+NF (NF+1 rows), cols 4tx .. 4tx+NF+2
 #pragma unroll
     for (int wr = 0; wr < NF + 1; ++wr) {
-      float v[3][SS::FWIN];
+      float v[PL][SS::FWIN];
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
+      for (int c = 0; c < PL; ++c)
         lds_run<SS::FO, SS::FWIN>(sfine + (c * SS::FR + 2 * ty + wr) * SS::FCB + 4 * tx + SS::FO, v[c]);
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
@@ -357,7 +378,7 @@ __global__ void __launch_bounds__(256 * G, 1)
 #pragma unroll
           for (int dx = 0; dx < NF; ++dx) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) acc[i][j][c] = fmaf(t[dx], v[c][j + dx], acc[i][j][c]);
+            for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(t[dx], v[c][j + dx], acc[i][j][c]);
           }
         }
       }
@@ -370,7 +391,7 @@ __global__ void __launch_bounds__(256 * G, 1)
       if (yy < a.o_r0 || yy >= a.o_r0 + a.o_rn || x >= a.W) continue;
       float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.W + x;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
+      for (int c = 0; c < PL; ++c) {
         float v0 = acc[i][0][c], v1 = acc[i][1][c], v2 = acc[i][2][c], v3 = acc[i][3][c];
         if (a.clamp) {
           v0 = fminf(fmaxf(v0, 0.0f), 1.0f);
@@ -378,7 +399,7 @@ __global__ void __launch_bounds__(256 * G, 1)
           v2 = fminf(fmaxf(v2, 0.0f), 1.0f);
           v3 = fminf(fmaxf(v3, 0.0f), 1.0f);
         }
-        float* d = op + (long long)c * a.out_rows * a.W;
+        float* d = op + (long long)(CH3 ? chn : c) * a.out_rows * a.W;
         if (x + 3 < a.W) {
           *reinterpret_cast<float4*>(d) = make_float4(v0, v1, v2, v3);  // W % 4 == 0 on this path
         } else {

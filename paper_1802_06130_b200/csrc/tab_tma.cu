@@ -6,16 +6,19 @@
 #endif
 namespace blade {
 namespace tables {
-template <int NF, int NC, int G = BLADE_TMA_GROUPS>
+template <int NF, int NC, bool CH3 = false, int G = BLADE_TMA_GROUPS>
 static TmaVariant make_tma() {
   using SS = TmaShape<NF, NC>;
-  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, false};
+  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G, CH3>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3};
 }
 const std::vector<TmaVariant>& tma_variants() {
   static const std::vector<TmaVariant> v = {
       make_tma<3, 0>(), make_tma<5, 0>(), make_tma<7, 0>(), make_tma<9, 0>(),
       make_tma<3, 3>(), make_tma<5, 5>(), make_tma<5, 3>(),
+      // per-channel YCbCr banks (NEXT f1): CTAs specialised by channel
+      make_tma<3, 0, true>(), make_tma<5, 0, true>(), make_tma<7, 0, true>(), make_tma<9, 0, true>(),
+      make_tma<3, 3, true>(), make_tma<5, 5, true>(), make_tma<5, 3, true>(),
   };
   return v;
 }
