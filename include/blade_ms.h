@@ -64,7 +64,7 @@ typedef struct {
                                 1 = bucket only (SPEC.md reading); must be 1 if L == 1          */
   int32_t n_filter_channels; /* 1 = one filter for R, G and B [R13]; 3 = per-channel Y, Cb, Cr
                                 banks with the shared RGB selector (PAPER.md:198-202 footnote 1;
-                                full-range BT.601 [R25], DESIGN.md §11)                          */
+                                full-range BT.601 [R25], DESIGN.md §10)                          */
   int32_t window_size;       /* structure-tensor window: 1, 3 or 5 (configs: 5) [R4]            */
   float window_sigma;        /* Gaussian std of the window, > 0 (configs: 1.5) [R4]             */
   int32_t clamp_output;      /* 0 = raw cascade output (parity); 1 = clamp final u^0 to [0,1]
