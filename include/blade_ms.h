@@ -74,7 +74,9 @@ typedef struct {
 typedef struct {
   int32_t n_orient;    /* n_o >= 1 orientation bins over [0, pi) (configs: 16)                 */
   int32_t n_strength;  /* n_s >= 1 (configs: 3)                                                */
-  int32_t n_coherence; /* n_c >= 1 (configs: 3); K = n_o * n_s * n_c <= 256 (uint8 maps)       */
+  int32_t n_coherence; /* n_c >= 1 (configs: 3); K = n_o * n_s * n_c <= 65536: K <= 256 keeps uint8
+                          maps and the bank in shared memory; K > 256 (e.g. the paper's 16 x 16 x
+                          16) uses uint16 maps and an L2-resident bank (NEXT f2)     */
   /* Thresholds per stage, stage index = output level l (0 = finest), n_stages = max(L-1, 1):
      strength_thresholds[stage * (n_s - 1) + t], coherence_thresholds[stage * (n_c - 1) + t];
      strictly ascending and finite within a stage. Quantiser [R7]:
@@ -163,12 +165,13 @@ blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t i
                                    size_t ws_bytes, void* cuda_stream);
 
 /*
- * Diagnostic: the bucket maps s^l (uint8, device, [N][H_l][W_l]) for every selector level
+ * Diagnostic: the bucket maps s^l (device, [N][H_l][W_l]; uint8 entries when K <= 256, uint16
+ * when K > 256 — the paper's 16 x 16 x 16 layout, NEXT f2) for every selector level
  * l = 0 .. n_stages-1 (maps_per_level[l]; a NULL entry skips that level). Also leaves the
  * pyramid in the workspace.
  */
 blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W,
-                               uint8_t* const* maps_per_level, void* workspace, size_t ws_bytes,
+                               void* const* maps_per_level, void* workspace, size_t ws_bytes,
                                void* cuda_stream);
 
 /* Diagnostic: pyramid levels 1..L-1 into levels[l-1] (device fp32 [N][3][H_l][W_l]). */

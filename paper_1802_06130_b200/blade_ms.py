@@ -154,6 +154,8 @@ class BladeMS:
         self.device = device
         self.levels = levels
         self.n_stages = max(levels - 1, 1)
+        self.K = n_orient * n_strength * n_coherence
+        self.map_dtype = torch.uint16 if self.K > 256 else torch.uint8
 
     @classmethod
     def from_config(cls, cfg, taps=None, device: int = 0, clamp_output: bool = False):
@@ -250,11 +252,11 @@ class BladeMS:
 
     def selector(self, x: torch.Tensor, workspace: torch.Tensor | None = None,
                  stream=None) -> list[torch.Tensor]:
-        """Bucket maps s^l (uint8 [N,H_l,W_l]) for l = 0 .. n_stages-1."""
+        """Bucket maps s^l (uint8 [N,H_l,W_l]; uint16 when K > 256) for l = 0 .. n_stages-1."""
         self._check_img(x, "x")
         N, _, H, W = x.shape
         dims = self.level_dims(H, W)
-        maps = [torch.empty((N, dims[l][0], dims[l][1]), dtype=torch.uint8, device=x.device)
+        maps = [torch.empty((N, dims[l][0], dims[l][1]), dtype=self.map_dtype, device=x.device)
                 for l in range(self.n_stages)]
         arr = (ctypes.c_void_p * len(maps))(*[m.data_ptr() for m in maps])
         ws = self.workspace(N, H, W) if workspace is None else workspace

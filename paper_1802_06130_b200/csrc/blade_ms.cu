@@ -182,11 +182,11 @@ struct Plan {
 };
 
 // Dependency cone of output rows [o0, o0+on) of the final output.
-void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int on, Plan& p);
+void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int on, Plan& p, int map_es = 1);
 void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) {
-  plan_rows_cfg(h->cfg, N, H, W, o0, on, p);
+  plan_rows_cfg(h->cfg, N, H, W, o0, on, p, h->K > 256 ? 2 : 1);
 }
-void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int on, Plan& p) {
+void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int on, Plan& p, int map_es) {
   const int L = cfg.levels;
   p.L = L;
   p.N = N;
@@ -240,7 +240,7 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
   const int nsel = L == 1 ? 1 : L - 1;
   for (int l = 0; l < nsel; ++l) {
     p.map_off[l] = off;
-    off = align256(off + (size_t)N * p.u[l].n() * p.W[l]);
+    off = align256(off + (size_t)map_es * N * p.u[l].n() * p.W[l]);
   }
   // uncertified-pixel lists of the fp32 selector (DESIGN.md §6 H1): 1/64 of each level's map
   p.fb_off.assign(nsel, 0);
@@ -339,7 +339,7 @@ bool sync_debug() {
 // Enqueue the cascade for plan p. in_view: level-0 input (fp32, rows >= p.z[0]); out_view: final
 // output rows p.u[0]. levels_out (diagnostic) receives z^l (fp32) for l >= 1; maps_out the maps.
 blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view, char* ws,
-                     cudaStream_t st, bool run_stages, uint8_t* const* maps_out,
+                     cudaStream_t st, bool run_stages, void* const* maps_out,
                      float* const* levels_out) {
   const int L = p.L, N = p.N;
   if (N == 0) return BLADE_OK;
@@ -353,9 +353,9 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     if (l + 1 < L) zlo[l] = reinterpret_cast<float*>(ws + p.zlo_off[l]);
   }
   const int nsel = L == 1 ? 1 : L - 1;
-  std::vector<uint8_t*> maps(nsel);
+  std::vector<uint8_t*> maps(nsel);  // byte addresses of uint8 / uint16 maps
   for (int l = 0; l < nsel; ++l)
-    maps[l] = (maps_out && maps_out[l]) ? maps_out[l] : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
+    maps[l] = (maps_out && maps_out[l]) ? static_cast<uint8_t*>(maps_out[l]) : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
 
   // ---- down pass: k_down(l) -> s^l, z^{l+1} (hi, and lo when level l+1 feeds a selector);
   //      k_down_fixup(l) recomputes the (rare) pixels whose fp32 orientation is uncertified
@@ -405,11 +405,12 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     ProfScope ps(h, st, 1, l);
     const bool hilo = l > 0;
     const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
-    auto fn = down_kernel(hilo, dec, fast);
+    const bool wide = h->K > 256;
+    auto fn = down_kernel(hilo, dec, fast, wide);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     fn<<<grid, 32 * down::WARPS, down_smem(hilo), st>>>(da, h->down[l]);
     LAUNCH_CHECK("k_down");
-    auto fx = fixup_kernel(hilo, fast);
+    auto fx = fixup_kernel(hilo, fast, wide);
     fx<<<4 * h->num_sms, 128, 0, st>>>(da, h->down[l]);
     LAUNCH_CHECK("k_down_fixup");
   }
@@ -437,7 +438,10 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     if (use_tma) {
       const TmaVariant& tv = h->tma;
       use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb, tv.fr, 3) &&
-                encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.W[l], r.n(), N, tv.tcols, tv.trows, 1);
+                (h->K > 256 ? encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p.W[l], r.n(), N, tv.tcols,
+                                        tv.trows, 1)
+                            : encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.W[l], r.n(), N, tv.tcols,
+                                        tv.trows, 1));
       if (use_tma) {
         if (L > 1)
           use_tma = encode_3d(&tmu, u1.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l + 1], u1.rows, N * 3, tv.ccb,
@@ -592,7 +596,10 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   if (bl->n_strength - 1 > kMaxThr2 || bl->n_coherence - 1 > kMaxThr2)
     return fail(BLADE_EUNSUPPORTED, "at most %d thresholds per feature", kMaxThr2);
   const long long K = (long long)bl->n_orient * bl->n_strength * bl->n_coherence;
-  if (K > 256) return fail(BLADE_EUNSUPPORTED, "K = %lld > 256 needs uint16 maps (SURVEY.md §8 f2)", K);
+  if (K > 65536) return fail(BLADE_EUNSUPPORTED, "K = %lld > 65536 (uint16 bucket maps)", K);
+  const bool wide = K > 256;  // uint16 maps, bank read from global memory (NEXT f2)
+  if (wide && c.n_filter_channels == 3)
+    return fail(BLADE_EUNSUPPORTED, "K > 256 with per-channel banks is not built");
   if ((bl->n_strength > 1 && !bl->strength_thresholds) || (bl->n_coherence > 1 && !bl->coherence_thresholds))
     return fail(BLADE_EINVAL, "threshold arrays must be non-NULL");
   const int n_stages = std::max(c.levels - 1, 1);
@@ -641,9 +648,10 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   size_t best_smem = 0;
   const bool ch3 = c.n_filter_channels == 3;
   for (const auto& v : stage_variants()) {
-    if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs || v.ch3 != ch3) continue;
+    if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs || v.ch3 != ch3 || v.wide != wide) continue;
     const int nph_cta = c.n_phases == 4 ? (v.rs == 2 ? 2 : 4) : 1;
-    const size_t smem = sizeof(float) * ((((size_t)nph_cta * PS) + 3) / 4 * 4 + (size_t)v.tile_floats);
+    const size_t bank_f = wide ? 0 : (((size_t)nph_cta * PS) + 3) / 4 * 4;
+    const size_t smem = sizeof(float) * (bank_f + (size_t)v.tile_floats);
     if (smem > (size_t)max_smem) continue;
     if (!best || v.by > best->by) {
       best = &v;
@@ -671,9 +679,9 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->stage = *best;
   h->stage_smem = best_smem;
   for (const auto& v : tma_variants()) {
-    if (v.ch3 != ch3 || v.nf != c.fine_size || v.nc != cnc) continue;
+    if (v.ch3 != ch3 || v.wide != wide || v.nf != c.fine_size || v.nc != cnc) continue;
     const size_t tps = (size_t)K * v.S;  // phase stride of the TMA tap layout (multiple of 4)
-    const size_t bank = ((size_t)c.n_phases * tps * 4 + 127) & ~size_t(127);
+    const size_t bank = wide ? 0 : ((size_t)c.n_phases * tps * 4 + 127) & ~size_t(127);
     const size_t smem = 2 * (size_t)v.stage_bytes + bank + 16;
     if (smem <= (size_t)max_smem && get_encode()) {
       h->has_tma = true;
@@ -685,7 +693,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   }
   if (!h->has_tma && c.levels > 1 && c.n_phases == 4) {
     for (const auto& v : ph_variants()) {
-      if (v.nf != c.fine_size || v.nc != cnc || v.ch3 != ch3) continue;
+      if (v.nf != c.fine_size || v.nc != cnc || v.ch3 != ch3 || v.wide != wide) continue;
       const size_t tps = (size_t)K * v.S;
       const size_t smem = 2 * (size_t)v.stage_bytes + ((tps * 4 + 127) & ~size_t(127)) + 16;
       if (smem <= (size_t)max_smem && get_encode()) {
@@ -782,8 +790,8 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   if (ce == cudaSuccess) {
     for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl)
       for (int dc = 0; dc < 2 && ce == cudaSuccess; ++dc)
-        for (int sm = 0; sm < 2 && ce == cudaSuccess; ++sm)
-          ce = cudaFuncSetAttribute(down_kernel(hl, dc, sm), cudaFuncAttributeMaxDynamicSharedMemorySize,
+        for (int sm = 0; sm < 3 && ce == cudaSuccess; ++sm)
+          ce = cudaFuncSetAttribute(down_kernel(hl, dc, sm == 1, sm == 2), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)down_smem(hl));
   }
   int occ = 0;
@@ -922,7 +930,7 @@ blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t
   return enqueue(h, p, inv, outv, (char*)ws, (cudaStream_t)stream, true, nullptr, nullptr);
 }
 
-blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W, uint8_t* const* maps,
+blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W, void* const* maps,
                                void* ws, size_t ws_bytes, void* stream) {
   g_last_error.clear();
   if (!h) return fail(BLADE_EINVAL, "handle is NULL");

@@ -27,6 +27,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include "kernels.cuh"
 
@@ -55,7 +56,8 @@ struct DownArgs {
   const float* zlo;  // level l lo plane (nullptr at l = 0)
   int H, W, in_row0, in_rows;
   long long in_plane, in_frame;
-  uint8_t* map;      // s^l rows [s_r0, s_r0 + s_rn), pitch W, frame stride s_rn * W
+  void* map;         // s^l rows [s_r0, s_r0 + s_rn), pitch W, frame stride s_rn * W; uint8
+                     // entries (K <= 256) or uint16 (WIDE, K <= 65536)
   int s_r0, s_rn;
   float* ohi;        // z^{l+1} hi: rows [d_buf_row0, + d_buf_rows), pitch W1 (nullptr: no dec)
   float* olo;        // z^{l+1} lo (nullptr: not needed, l + 1 is the coarsest level)
@@ -222,19 +224,29 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
   }
   // certified iff every sign test clears the error bound; exact zero gradients => theta = 0 [R5]
   safe = zero ? !(T > 0.0f) : (mn > bound);
-  int s = 0;
-#pragma unroll
-  for (int t = 0; t < MAXT; ++t) {
-    if (!FAST && t >= prm.n_s - 1) break;
-    const float d = prm.ts2[t] - h;
-    s += (d <= 0.0f) || (q >= d * d);
-  }
   const float h2 = h * h;
-  int k = 0;
+  int s = 0, k = 0;
+  if constexpr (FAST) {
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t) {
-    if (!FAST && t >= prm.n_c - 1) break;
-    k += (q >= prm.kc2[t] * h2);
+    for (int t = 0; t < MAXT; ++t) {
+      const float d = prm.ts2[t] - h;
+      s += (d <= 0.0f) || (q >= d * d);
+    }
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) k += (q >= prm.kc2[t] * h2);
+  } else {
+    // the tests are monotone in t (ascending thresholds, +inf padding up to kMaxThr2 = 15):
+    // binary search for the count of passed thresholds
+#pragma unroll
+    for (int step = 8; step >= 1; step >>= 1) {
+      const int t = s + step - 1;
+      if (t < kMaxThr2) {
+        const float d = prm.ts2[t] - h;
+        if ((d <= 0.0f) || (q >= d * d)) s += step;
+      }
+      const int u = k + step - 1;
+      if (u < kMaxThr2 && q >= prm.kc2[u] * h2) k += step;
+    }
   }
   k = prm.tc_nonpos + (h > 0.0f ? k : 0);  // C = 0 when l1 = 0 [R6]
   if constexpr (FAST) return (o * 3 + s) * 3 + k;  // FAST layout: 16 x 3 x 3
@@ -279,8 +291,9 @@ __device__ __forceinline__ void abc_fp64(const DownArgs& a, const DownParams& pr
 }
 
 // grid: ceil(n_tasks / WARPS) CTAs of 32 * WARPS threads; task = (frame, band, strip), strip fastest.
-template <bool HILO, bool DEC, bool FAST>
+template <bool HILO, bool DEC, bool FAST, bool WIDE>
 __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, const DownParams prm) {
+  using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;  // bucket map entry
   using namespace down;
   constexpr int NP = HILO ? 6 : 3;  // planes per ring row (3 channels, x2 with lo)
   extern __shared__ __align__(16) float dsm[];
@@ -359,11 +372,11 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
     lm[c][0] = lm[c][1] = lc[c][0] = lc[c][1] = lL[c] = lR[c] = 0.0f;
   }
 
-  uint8_t* mapf = a.map + (long long)n * a.s_rn * a.W;
+  MT* mapf = static_cast<MT*>(a.map) + (long long)n * a.s_rn * a.W;
   const long long oframe = (long long)n * 3 * a.d_buf_rows * a.W1;
   const int Xd = x >> 1;  // decimated column (x even)
   // 2-byte map stores when every map row starts 2-B aligned (x is even)
-  const bool map16 = ((a.W | (int)(reinterpret_cast<uintptr_t>(a.map) & 1)) & 1) == 0;
+  const bool map16 = (a.W & 1) == 0 && (reinterpret_cast<uintptr_t>(a.map) & (2 * sizeof(MT) - 1)) == 0;
 
 #pragma unroll 2
   for (int i = 0; i < nrows; ++i) {
@@ -505,12 +518,15 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
         }
       }
       if (emit && x < a.W) {
-        uint8_t* mrow = mapf + (long long)(y - a.s_r0) * a.W + x;
-        if (map16 && x + 1 < a.W)
-          *reinterpret_cast<uint16_t*>(mrow) = (uint16_t)(bk[0] | (bk[1] << 8));
-        else {
-          mrow[0] = (uint8_t)bk[0];
-          if (x + 1 < a.W) mrow[1] = (uint8_t)bk[1];
+        MT* mrow = mapf + (long long)(y - a.s_r0) * a.W + x;
+        if (map16 && x + 1 < a.W) {  // both entries in one store
+          if constexpr (WIDE)
+            *reinterpret_cast<uint32_t*>(mrow) = (uint32_t)bk[0] | ((uint32_t)bk[1] << 16);
+          else
+            *reinterpret_cast<uint16_t*>(mrow) = (uint16_t)(bk[0] | (bk[1] << 8));
+        } else {
+          mrow[0] = (MT)bk[0];
+          if (x + 1 < a.W) mrow[1] = (MT)bk[1];
         }
       }
     }
@@ -536,8 +552,9 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
 // Fix-up of the uncertified pixels of one k_down launch: fp64 (a, b, c) and the bucket rule in
 // fp64-derived fp32 as the fp64 selector. If the list overflowed (pathological inputs with many
 // exactly isotropic tensors), every map entry of the launch is recomputed.
-template <bool HILO, bool FAST>
+template <bool HILO, bool FAST, bool WIDE>
 __global__ void __launch_bounds__(128) k_down_fixup(const DownArgs a, const DownParams prm) {
+  using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;
   // one warp per pixel: lane t < 25 evaluates the gradient products at window offset
   // (t / 5 - 2, t % 5 - 2) in fp64, the weighted products are summed over the warp (fp64)
   const unsigned int cnt = *a.fb_count;
@@ -583,7 +600,7 @@ __global__ void __launch_bounds__(128) k_down_fixup(const DownArgs a, const Down
       pb += __shfl_xor_sync(0xffffffffu, pb, o);
       pc += __shfl_xor_sync(0xffffffffu, pc, o);
     }
-    if (lane == 0) a.map[e] = (uint8_t)bucket_of<FAST>(pa, pb, pc, prm);
+    if (lane == 0) static_cast<MT*>(a.map)[e] = (MT)bucket_of<FAST>(pa, pb, pc, prm);
   }
 }
 

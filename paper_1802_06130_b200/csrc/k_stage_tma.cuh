@@ -99,22 +99,27 @@ __host__ __device__ constexpr int tma_tap_stride(int nf, int nc) {
 }
 
 // Loads the NB taps of row dy of `block` of the filter at tp (16-B aligned) into t[0..NB).
-template <int NF, int NC, int BLOCK>
+// GL: the bank lives in global memory (L2-resident, read-only path) instead of shared memory.
+template <int NF, int NC, int BLOCK, bool GL = false>
 __device__ __forceinline__ void load_tap_row(const float* tp, int dy, float* t) {
   constexpr int NB = BLOCK == 0 ? NF : NC;
 #pragma unroll
   for (int q = 0; q < NB / 4; ++q) {
-    const float4 v = *reinterpret_cast<const float4*>(tp + tma_tap_off(NF, NC, BLOCK, dy, 4 * q));
+    const float4* p4 = reinterpret_cast<const float4*>(tp + tma_tap_off(NF, NC, BLOCK, dy, 4 * q));
+    const float4 v = GL ? __ldg(p4) : *p4;
     t[4 * q] = v.x;
     t[4 * q + 1] = v.y;
     t[4 * q + 2] = v.z;
     t[4 * q + 3] = v.w;
   }
 #pragma unroll
-  for (int k = 4 * (NB / 4); k < NB; ++k) t[k] = tp[tma_tap_off(NF, NC, BLOCK, dy, k)];
+  for (int k = 4 * (NB / 4); k < NB; ++k) {
+    const float* p = tp + tma_tap_off(NF, NC, BLOCK, dy, k);
+    t[k] = GL ? __ldg(p) : *p;
+  }
 }
 
-template <int NF, int NC>
+template <int NF, int NC, bool WIDE = false>
 struct TmaShape {
   static constexpr int RX = 4, RY = 2, BX = 32, BY = 8;
   static constexpr int threads = BX * BY;
@@ -132,7 +137,7 @@ struct TmaShape {
   static_assert(RF <= FM && RC <= CM, "halo wider than the TMA margin");
   static constexpr int fine_bytes = 3 * FR * FCB * 4;
   static constexpr int coarse_bytes = 3 * CR * CCB * 4;
-  static constexpr int map_bytes = TROWS * TCOLS;
+  static constexpr int map_bytes = TROWS * TCOLS * (WIDE ? 2 : 1);  // uint16 buckets when WIDE
   static constexpr int al(int x) { return (x + 127) & ~127; }
   static constexpr int fine_off = 0;
   static constexpr int coarse_off = al(fine_bytes);
@@ -170,11 +175,13 @@ struct StageTmaArgs {
 // CH3 (per-channel Y/Cb/Cr banks, NEXT f1): CTA b serves channel b % 3 (all four phases of that
 // channel's bank); the staged patches are converted to that channel in plane 0 after the fix-up
 // (the coarse patch only when it is the RGB z^{L-1}; else plane chn of the YCbCr u^{l+1} is read).
-template <int NF, int NC, int G, bool CH3>
+// WIDE (NEXT f2, K > 256): uint16 bucket tiles and the bank read from global memory (the paper's
+// 16 x 16 x 16 layout is 4.8 MB per stage: L2-resident, not shared-memory resident).
+template <int NF, int NC, int G, bool CH3, bool WIDE = false>
 __global__ void __launch_bounds__(256 * G, 1)
     k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
-  using SS = TmaShape<NF, NC>;
+  using SS = TmaShape<NF, NC, WIDE>;
   constexpr int RF = SS::RF, RC = SS::RC;
   constexpr int PL = CH3 ? 1 : 3;
   const int chn = CH3 ? (int)(blockIdx.x % 3) : 0;
@@ -185,7 +192,9 @@ __global__ void __launch_bounds__(256 * G, 1)
   unsigned char* buf0 = tma_smem;
   const int bank_floats = a.n_phases * a.PS;
   float* sbank = reinterpret_cast<float*>(tma_smem + 2 * SS::stage_bytes);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(tma_smem + 2 * SS::stage_bytes + ((bank_floats * 4 + 127) & ~127));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tma_smem + 2 * SS::stage_bytes +
+                                               (WIDE ? 0 : ((bank_floats * 4 + 127) & ~127)));
+  const float* bank = WIDE ? a.bank + (long long)chn * bank_floats : sbank;
 
   const int g = G == 2 ? (int)(threadIdx.y >> 3) : 0;  // thread group
   const int tid = (threadIdx.y & 7) * SS::BX + threadIdx.x;  // thread index within the group
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(256 * G, 1)
   __syncthreads();
   if (tid == 0 && t < a.n_tiles) issue(t, g);
   // ---- the bank -> shared memory, once
-  {
+  if (!WIDE) {
     const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)chn * bank_floats);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     for (int i = ctid; i < (bank_floats >> 2); i += SS::threads * G) s4[i] = __ldg(g4 + i);
@@ -319,16 +328,24 @@ __global__ void __launch_bounds__(256 * G, 1)
     // ---- this thread's 2 x 4 block
     const int x = X0 + SS::RX * tx;
     const int y = Y0 + SS::RY * ty;
-    const uint32_t mrow0 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty) * SS::TCOLS + 4 * tx);
-    const uint32_t mrow1 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty + 1) * SS::TCOLS + 4 * tx);
+    uint64_t mrow0, mrow1;
+    if constexpr (WIDE) {
+      mrow0 = *reinterpret_cast<const uint64_t*>(smap + 2 * ((2 * ty) * SS::TCOLS + 4 * tx));
+      mrow1 = *reinterpret_cast<const uint64_t*>(smap + 2 * ((2 * ty + 1) * SS::TCOLS + 4 * tx));
+    } else {
+      mrow0 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty) * SS::TCOLS + 4 * tx);
+      mrow1 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty + 1) * SS::TCOLS + 4 * tx);
+    }
+    constexpr int KB = WIDE ? 16 : 8;
+    constexpr uint64_t KM = WIDE ? 0xffff : 0xff;
     const float* tp[2][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int k0 = (mrow0 >> (8 * j)) & 0xff, k1 = (mrow1 >> (8 * j)) & 0xff;
+      const int k0 = (int)((mrow0 >> (KB * j)) & KM), k1 = (int)((mrow1 >> (KB * j)) & KM);
       const int ph0 = a.n_phases == 4 ? (j & 1) : 0;
       const int ph1 = a.n_phases == 4 ? 2 + (j & 1) : 0;
-      tp[0][j] = sbank + ph0 * a.PS + k0 * SS::S;
-      tp[1][j] = sbank + ph1 * a.PS + k1 * SS::S;
+      tp[0][j] = bank + ph0 * a.PS + k0 * SS::S;
+      tp[1][j] = bank + ph1 * a.PS + k1 * SS::S;
     }
     float acc[2][4][PL];
 #pragma unroll
@@ -351,7 +368,7 @@ __global__ void __launch_bounds__(256 * G, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float t[NC > 0 ? NC : 1];
-            load_tap_row<NF, NC, 1>(tp[i][j], wr, t);
+            load_tap_row<NF, NC, 1, WIDE>(tp[i][j], wr, t);
 #pragma unroll
             for (int dx = 0; dx < NC; ++dx) {
 #pragma unroll
@@ -374,7 +391,7 @@ __global__ void __launch_bounds__(256 * G, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float t[NF];
-          load_tap_row<NF, NC, 0>(tp[i][j], dy, t);
+          load_tap_row<NF, NC, 0, WIDE>(tp[i][j], dy, t);
 #pragma unroll
           for (int dx = 0; dx < NF; ++dx) {
 #pragma unroll

@@ -15,6 +15,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <type_traits>
 
 namespace blade {
 
@@ -59,7 +60,7 @@ struct StageArgs {
   LevelView z;         // z^l
   LevelView u1;        // u^{l+1} (unused when NC == 0)
   LevelView out;       // u^l (output rows [out_r0, out_r0 + out_rn))
-  const uint8_t* map;  // s^l, [N][map_rows][W], buffer row 0 = global row map_row0
+  const void* map;     // s^l, [N][map_rows][W] uint8 (uint16 when WIDE), row 0 = global row map_row0
   int map_row0, map_rows;
   const float* bank;   // device bank of this stage: [phase][PS floats: K x S taps, padded]
   int K, S, PS;        // buckets, padded tap stride (odd), phase stride (multiple of 4)
@@ -102,14 +103,16 @@ struct StageShape {
 // fine patch (RGB z^l) is converted to channel c while staged, the coarse patch too when it is
 // z^{L-1} (RGB), else it is plane c of the YCbCr u^{l+1}; the output is plane c of a YCbCr u^l
 // (level 0 is converted back to RGB by k_ycc_to_rgb).
-template <int NF, int NC, int RS, int BY, bool CH3>
+// WIDE (NEXT f2, K > 256): uint16 bucket maps and the bank read from global memory (L2-resident).
+template <int NF, int NC, int RS, int BY, bool CH3, bool WIDE = false>
 __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
   using SS = StageShape<NF, NC, RS, BY, CH3>;
+  using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;
   constexpr int PL = SS::PL;
   constexpr int RF = SS::RF, RC = SS::RC;
   extern __shared__ __align__(16) float smem[];
   const int nph_cta = a.n_phases == 4 ? SS::NPH_CTA : 1;
-  const int bank_floats = nph_cta * a.PS;
+  const int bank_floats = WIDE ? 0 : nph_cta * a.PS;
   float* sbank = smem;
   float* sfine = smem + ((bank_floats + 3) & ~3);
   float* scoarse = sfine + PL * SS::FR * SS::FCP;
@@ -121,10 +124,11 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
   const int ngroups = (int)gridDim.x / (RS * (CH3 ? 3 : 1));
   const int tid = threadIdx.y * SS::BX + threadIdx.x;
 
-  // ---- filterbank -> shared memory, once per CTA
-  {
-    const int ph0 = (a.n_phases == 4 && RS == 2) ? 2 * par : 0;
-    const long long boff = (long long)(chn * a.n_phases + ph0) * a.PS;
+  // ---- filterbank -> shared memory, once per CTA (WIDE: read in place from global memory)
+  const int ph0 = (a.n_phases == 4 && RS == 2) ? 2 * par : 0;
+  const long long boff = (long long)(chn * a.n_phases + ph0) * a.PS;
+  const float* bank = WIDE ? a.bank + boff : sbank;
+  if (!WIDE) {
     const float4* g4 = reinterpret_cast<const float4*>(a.bank + boff);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     const int n4 = bank_floats >> 2;
@@ -194,10 +198,11 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
       for (int j = 0; j < 2; ++j) {
         const int yy = y0 + i * RS, xx = min(x + j, a.z.W - 1);
         int k = 0;
-        if (row_ok[i]) k = a.map[(long long)n * a.map_rows * a.z.W + (long long)(yy - a.map_row0) * a.z.W + xx];
+        if (row_ok[i])
+          k = static_cast<const MT*>(a.map)[(long long)n * a.map_rows * a.z.W + (long long)(yy - a.map_row0) * a.z.W + xx];
         int ps = 0;
         if (a.n_phases == 4) ps = RS == 2 ? j : 2 * (yy & 1) + j;
-        tp[i][j] = sbank + ps * a.PS + k * a.S;
+        tp[i][j] = bank + ps * a.PS + k * a.S;
       }
 
     float acc[2][2][PL];
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
           for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int dx = 0; dx < NC; ++dx) {
-              const float tap = tp[i][j][NF * NF + dy * NC + dx];
+              const float tap = WIDE ? __ldg(tp[i][j] + NF * NF + dy * NC + dx) : tp[i][j][NF * NF + dy * NC + dx];
 #pragma unroll
               for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(tap, v[c][dx], acc[i][j][c]);
             }
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int dx = 0; dx < NF; ++dx) {
-            const float tap = tp[i][j][dy * NF + dx];
+            const float tap = WIDE ? __ldg(tp[i][j] + dy * NF + dx) : tp[i][j][dy * NF + dx];
 #pragma unroll
             for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(tap, v[c][j + dx], acc[i][j][c]);
           }

@@ -3,17 +3,19 @@
 
 namespace blade {
 namespace tables {
-template <bool FAST>
+template <bool FAST, bool WIDE>
 static DownKernel down_kernel_t(bool hilo, bool dec) {
-  if (hilo) return dec ? &k_down<true, true, FAST> : &k_down<true, false, FAST>;
-  return dec ? &k_down<false, true, FAST> : &k_down<false, false, FAST>;
+  if (hilo) return dec ? &k_down<true, true, FAST, WIDE> : &k_down<true, false, FAST, WIDE>;
+  return dec ? &k_down<false, true, FAST, WIDE> : &k_down<false, false, FAST, WIDE>;
 }
-DownKernel down_kernel(bool hilo, bool dec, bool fast) {
-  return fast ? down_kernel_t<true>(hilo, dec) : down_kernel_t<false>(hilo, dec);
+DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide) {
+  if (wide) return down_kernel_t<false, true>(hilo, dec);  // FAST implies K = 144
+  return fast ? down_kernel_t<true, false>(hilo, dec) : down_kernel_t<false, false>(hilo, dec);
 }
-DownKernel fixup_kernel(bool hilo, bool fast) {
-  if (hilo) return fast ? &k_down_fixup<true, true> : &k_down_fixup<true, false>;
-  return fast ? &k_down_fixup<false, true> : &k_down_fixup<false, false>;
+DownKernel fixup_kernel(bool hilo, bool fast, bool wide) {
+  if (wide) return hilo ? &k_down_fixup<true, false, true> : &k_down_fixup<false, false, true>;
+  if (hilo) return fast ? &k_down_fixup<true, true, false> : &k_down_fixup<true, false, false>;
+  return fast ? &k_down_fixup<false, true, false> : &k_down_fixup<false, false, false>;
 }
 }  // namespace tables
 }  // namespace blade

@@ -6,11 +6,11 @@
 #endif
 namespace blade {
 namespace tables {
-template <int NF, int NC, bool CH3 = false, int G = BLADE_TMA_GROUPS>
+template <int NF, int NC, bool CH3 = false, bool WIDE = false, int G = BLADE_TMA_GROUPS>
 static TmaVariant make_tma() {
-  using SS = TmaShape<NF, NC>;
-  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G, CH3>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3};
+  using SS = TmaShape<NF, NC, WIDE>;
+  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G, CH3, WIDE>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3, WIDE};
 }
 const std::vector<TmaVariant>& tma_variants() {
   static const std::vector<TmaVariant> v = {
@@ -19,6 +19,11 @@ const std::vector<TmaVariant>& tma_variants() {
       // per-channel YCbCr banks (NEXT f1): CTAs specialised by channel
       make_tma<3, 0, true>(), make_tma<5, 0, true>(), make_tma<7, 0, true>(), make_tma<9, 0, true>(),
       make_tma<3, 3, true>(), make_tma<5, 5, true>(), make_tma<5, 3, true>(),
+      // K > 256 (NEXT f2): uint16 bucket tiles, bank read from global memory
+      make_tma<3, 0, false, true>(), make_tma<5, 0, false, true>(), make_tma<7, 0, false, true>(),
+      make_tma<9, 0, false, true>(), make_tma<5, 5, false, true>(), make_tma<7, 5, false, true>(),
+      make_tma<7, 7, false, true>(), make_tma<9, 9, false, true>(), make_tma<5, 3, false, true>(),
+      make_tma<9, 7, false, true>(),
   };
   return v;
 }

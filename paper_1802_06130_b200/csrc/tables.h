@@ -18,7 +18,8 @@ struct StageVariant {
   int nf, nc, rs, by;
   StageKernel fn;
   int tile_floats, threads, trows, tcols;
-  bool ch3;  // per-channel (Y, Cb, Cr) banks: CTAs specialised by channel (NEXT f1)
+  bool ch3;   // per-channel (Y, Cb, Cr) banks: CTAs specialised by channel (NEXT f1)
+  bool wide;  // K > 256: uint16 maps, bank read from global memory (NEXT f2)
 };
 // Generic stage kernels (any shape; row-parity CTAs for the big pair banks).
 const std::vector<StageVariant>& stage_variants();
@@ -29,7 +30,8 @@ struct TmaVariant {
   TmaKernel fn;
   int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc, S;
   bool phase_split;  // k_stage_ph: CTAs specialised by output phase, one phase's bank each
-  bool ch3;          // per-channel (Y, Cb, Cr) banks (k_stage_ph only)
+  bool ch3;          // per-channel (Y, Cb, Cr) banks
+  bool wide;         // K > 256: uint16 maps, bank read from global memory (NEXT f2)
 };
 // TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
 const std::vector<TmaVariant>& tma_variants();
@@ -38,8 +40,9 @@ const std::vector<TmaVariant>& ph_variants();
 
 using DownKernel = void (*)(const DownArgs, const DownParams);
 // FAST: the configs' bucket layout (16 orientations x 3 strength x 3 coherence bins)
-DownKernel down_kernel(bool hilo, bool dec, bool fast);
-DownKernel fixup_kernel(bool hilo, bool fast);
+// wide: uint16 bucket maps (K > 256, NEXT f2)
+DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide);
+DownKernel fixup_kernel(bool hilo, bool fast, bool wide);
 
 }  // namespace tables
 }  // namespace blade

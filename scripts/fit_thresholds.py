@@ -49,7 +49,7 @@ def fit(name: str) -> dict:
     d = json.loads(p.read_text())
     d["strength_thresholds"] = ts_all
     d["coherence_thresholds"] = tc_all
-    d["thresholds_recipe"] = ("per-level tertiles of the fp64 oracle's strength/coherence on a "
+    d["thresholds_recipe"] = (f"per-level {cfg.n_strength}- / {cfg.n_coherence}-quantiles of the fp64 oracle's strength/coherence on a "
                               "calibration frame (seed+1000), rounded to fp32; "
                               "scripts/fit_thresholds.py")
     p.write_text(json.dumps(d, indent=1) + "\n")

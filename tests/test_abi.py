@@ -67,7 +67,7 @@ EINVAL, ENONFINITE, ESHAPE, EDEVICE, EUNSUP = 1, 2, 3, 4, 7
     (dict(ts=[0.2, 0.1, 0.2, 0.3]), EINVAL),   # not ascending
     (dict(tc=[0.3, np.nan, 0.3, 0.6]), ENONFINITE),
     (dict(ntaps=7), ESHAPE),
-    (dict(K=(16, 4, 5)), EUNSUP),              # K = 320 > 256 (uint8 maps)
+    (dict(K=(512, 16, 16)), EUNSUP),           # K = 131072 > 65536 (uint16 maps)
     (dict(n_filter_channels=3), ESHAPE),       # per-channel banks need 3x the taps
     (dict(n_filter_channels=2), EINVAL),
 ])

@@ -309,3 +309,42 @@ def test_ycc_clamp_applies_after_conversion():
     raw = _handle(cfg, taps).denoise(x)
     cl = _handle(cfg, taps, clamp_output=True).denoise(x)
     assert torch.equal(cl, raw.clamp(0, 1))
+
+
+def test_runtime_argument_errors_launch_nothing():
+    """Every call-time argument error is reported before any launch (ABI contract): the output
+    buffer keeps its canary values."""
+    from paper_1802_06130_b200 import BladeError
+    cfg = _cfg_like("c1", 64, 96, 1)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    out = torch.full_like(x, 3.5)
+    ws_n = h.workspace_size(1, 64, 96)
+    with pytest.raises(BladeError, match="ESHAPE"):  # workspace too small
+        h.denoise(x, out, torch.empty(ws_n - 256, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(BladeError, match="EINVAL"):  # out overlaps in
+        h.denoise(x, x)
+    from paper_1802_06130_b200 import lib
+    xh = x.cpu()
+    ws = h.workspace(1, 64, 96)
+    rc = lib().blade_ms_denoise(h._h, xh.data_ptr(), out.data_ptr(), 1, 64, 96, ws.data_ptr(),
+                                ws.numel(), None)
+    assert rc == 4, lib().blade_ms_last_error()  # EDEVICE: host pointer
+    with pytest.raises(BladeError, match="ESHAPE"):  # band that does not cover the cone
+        i0, ni = h.band_rows(64, 20, 10)
+        h.denoise_rows(x[0, :, i0 + 2:i0 + ni].contiguous(), i0 + 2, 20, 10, 64)
+    torch.cuda.synchronize()
+    assert bool((out == 3.5).all())
+
+
+# ------------------------------------------------------------------------- paper-scale buckets (f2)
+
+@pytest.mark.parametrize("H,W,N", [(1080, 1920, 1), (256, 384, 2), (130, 200, 1), (9, 17, 1)])
+def test_c5_paper_bucket_layout_parity(H, W, N):
+    """NEXT f2: the paper's 16 x 16 x 16 = 4096 buckets with 7x7 / 5x5 pairs:
+    uint16 maps, bank read from global memory; same parity rule."""
+    cfg = _cfg_like("c5", H, W, N)
+    assert cfg.K == 4096
+    out, stats, worst = _full_parity(cfg, cfg.batch(), label=f"c5@{H}x{W}")
+    h = _handle(cfg)
+    assert h.map_dtype == torch.uint16
