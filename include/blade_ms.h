@@ -137,6 +137,37 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
 blade_status blade_ms_band_rows(blade_ms_t h, int32_t H, int32_t out_row0, int32_t out_rows,
                                 int32_t* in_row0, int32_t* in_rows);
 
+/*
+ * Training (NEXT f4): the per-(phase, bucket) least-squares filters of PAPER.md:186-198 (§3,
+ * Eqs. 7-8) for one stage, from noisy / clean pairs (readings R27-R30).
+ * blade_ms_train_layout: nt = taps per filter (n_f^2 + n_c^2), ntp = pitch of the accumulator
+ * matrices (nt + 1 rounded up to 4), n_seg = n_phases * K.
+ */
+blade_status blade_ms_train_layout(blade_ms_t h, int32_t* nt, int32_t* ntp, int32_t* n_seg);
+blade_status blade_ms_train_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t W,
+                                           size_t* bytes);
+/*
+ * Accumulate the normal equations of stage `level` over N frames (DEVICE fp32 [N][3][H][W]):
+ * z = the noisy image at that level, u_clean = the clean target at that level, u_coarse = the
+ * filtered coarser level u^{level+1} ([N][3][ceil(H/2)][ceil(W/2)]; NULL when levels == 1).
+ * Every pixel and every channel is one sample x = [fine patch of z ; coarse patch of u_coarse]
+ * (ABI tap order) of the (phase, bucket) segment its selector (computed here from z with the
+ * thresholds of `level`) picks. E: DEVICE fp64 [n_seg][ntp][ntp], accumulated (the caller zeroes
+ * it once): E[s] = sum [x; u][x; u]^T over the segment, in its upper 4 x 4-block triangle (G in
+ * [0, nt)^2, m in column nt). count: DEVICE uint64 [n_seg], accumulated. Asynchronous.
+ */
+blade_status blade_ms_train_accumulate(blade_ms_t h, int32_t level, const float* z,
+                                       const float* u_clean, const float* u_coarse, int32_t N,
+                                       int32_t H, int32_t W, double* E, uint64_t* count,
+                                       void* workspace, size_t ws_bytes, void* cuda_stream);
+/*
+ * Solve every segment on the host (fp64 Cholesky): h = (G + ridge tr(G)/nt I)^-1 m when
+ * count >= min_count, else the centred fine delta with a zero coarse block. E, count: HOST copies
+ * of the accumulators; taps: HOST fp32 [n_phases][K][nt] (the stage's block of the create layout).
+ */
+blade_status blade_ms_train_solve(blade_ms_t h, const double* E, const uint64_t* count,
+                                  double ridge, uint64_t min_count, float* taps);
+
 /* Diagnostic (synchronous): after a blade_ms_denoise / _selector call of N x H x W frames with
  * workspace ws has completed, counts[l] (l < n_stages) = the number of pixels of selector level l
  * whose fp32 orientation bin was not certified and was recomputed in fp64 (DESIGN.md §6 H1). */

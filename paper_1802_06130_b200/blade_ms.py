@@ -50,7 +50,9 @@ class _Info(ctypes.Structure):
 
 
 EXPORTS = ["blade_ms_create", "blade_ms_workspace_size", "blade_ms_denoise", "blade_ms_denoise_host",
-           "blade_ms_band_rows", "blade_ms_band_plan", "blade_ms_fallback_count", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
+           "blade_ms_band_rows", "blade_ms_band_plan", "blade_ms_fallback_count",
+           "blade_ms_train_layout", "blade_ms_train_workspace_size", "blade_ms_train_accumulate",
+           "blade_ms_train_solve", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
            "blade_ms_selector", "blade_ms_pyramid", "blade_ms_get_info", "blade_ms_launch_count",
            "blade_ms_set_profiling", "blade_ms_profile_read",
            "blade_ms_destroy", "blade_ms_status_string", "blade_ms_last_error"]
@@ -85,6 +87,10 @@ def lib():
     L.blade_ms_band_plan.argtypes = [ctypes.POINTER(_Config), i32, i32, i32, ctypes.POINTER(i32),
                                      ctypes.POINTER(i32)]
     L.blade_ms_fallback_count.argtypes = [P, i32, i32, i32, P, sz, P]
+    L.blade_ms_train_layout.argtypes = [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.blade_ms_train_workspace_size.argtypes = [P, i32, i32, i32, ctypes.POINTER(sz)]
+    L.blade_ms_train_accumulate.argtypes = [P, i32, P, P, P, i32, i32, i32, P, P, P, sz, P]
+    L.blade_ms_train_solve.argtypes = [P, P, P, ctypes.c_double, ctypes.c_uint64, P]
     L.blade_ms_band_workspace_size.argtypes = [P, i32, i32, i32, i32, ctypes.POINTER(sz)]
     L.blade_ms_denoise_rows.argtypes = [P, P, i32, i32, P, i32, i32, i32, i32, P, sz, P]
     L.blade_ms_selector.argtypes = [P, P, i32, i32, i32, P, P, sz, P]
@@ -203,6 +209,48 @@ class BladeMS:
         _check(lib().blade_ms_fallback_count(self._h, N, H, W, _ptr(workspace), workspace.numel(),
                                              c.ctypes.data))
         return [int(v) for v in c[:self.n_stages]]
+
+    # -------------------------------------------------------------------------------- training
+    def train_layout(self) -> tuple[int, int, int]:
+        """(nt, ntp, n_seg) of the training accumulators (NEXT f4)."""
+        a, b, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().blade_ms_train_layout(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def train_accumulators(self, device=None):
+        """Zeroed (E, count) device accumulators for one stage."""
+        nt, ntp, n_seg = self.train_layout()
+        dev = device or f"cuda:{self.device}"
+        return (torch.zeros((n_seg, ntp, ntp), dtype=torch.float64, device=dev),
+                torch.zeros(n_seg, dtype=torch.int64, device=dev))
+
+    def train_accumulate(self, level: int, z: torch.Tensor, u_clean: torch.Tensor,
+                         u_coarse: torch.Tensor | None, E: torch.Tensor, count: torch.Tensor,
+                         workspace: torch.Tensor | None = None, stream=None):
+        """blade_ms_train_accumulate over the frames of z / u_clean ([N,3,H,W] CUDA fp32)."""
+        self._check_img(z, "z")
+        self._check_img(u_clean, "u_clean")
+        N, _, H, W = z.shape
+        if workspace is None:
+            b = ctypes.c_size_t()
+            _check(lib().blade_ms_train_workspace_size(self._h, N, H, W, ctypes.byref(b)))
+            workspace = torch.empty(b.value, dtype=torch.uint8, device=z.device)
+        _check(lib().blade_ms_train_accumulate(self._h, level, _ptr(z), _ptr(u_clean),
+                                               _ptr(u_coarse), N, H, W, _ptr(E), _ptr(count),
+                                               _ptr(workspace), workspace.numel(),
+                                               _stream_ptr(stream)))
+
+    def train_solve(self, E: torch.Tensor, count: torch.Tensor, ridge: float = 1e-3,
+                    min_count: int | None = None) -> np.ndarray:
+        """Host fp64 solve of every (phase, bucket): float32 [n_phases, K, nt]."""
+        nt, ntp, n_seg = self.train_layout()
+        Eh = np.ascontiguousarray(E.detach().cpu().numpy())
+        ch = np.ascontiguousarray(count.detach().cpu().numpy().astype(np.uint64))
+        taps = np.empty((n_seg, nt), np.float32)
+        mc = 4 * nt if min_count is None else min_count
+        _check(lib().blade_ms_train_solve(self._h, Eh.ctypes.data, ch.ctypes.data, float(ridge), mc,
+                                          taps.ctypes.data))
+        return taps.reshape(-1, self.K, nt)
 
     def set_profiling(self, enable: bool):
         _check(lib().blade_ms_set_profiling(self._h, int(enable)))

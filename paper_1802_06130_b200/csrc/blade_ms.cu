@@ -993,6 +993,225 @@ blade_status blade_ms_fallback_count(blade_ms_t h, int32_t N, int32_t H, int32_t
   return BLADE_OK;
 }
 
+// ------------------------------------------------------------------------------ training (NEXT f4)
+
+static int train_nt(const blade_ms* h) {
+  return h->cfg.fine_size * h->cfg.fine_size + (h->cfg.levels > 1 ? h->cfg.coarse_size * h->cfg.coarse_size : 0);
+}
+static const TrainVariant* train_variant(const blade_ms* h) {
+  const int cnc = h->cfg.levels > 1 ? h->cfg.coarse_size : 0;
+  for (const auto& v : train_variants())
+    if (v.nf == h->cfg.fine_size && v.nc == cnc && v.wide == (h->K > 256)) return &v;
+  return nullptr;
+}
+
+struct TrainPlan {
+  size_t map_off, fb_off, fbcnt_off, cnt_off, cur_off, sorted_off, bytes;
+  unsigned int fb_cap;
+};
+static TrainPlan train_plan(const blade_ms* h, long long px) {
+  TrainPlan t{};
+  const int n_seg = h->cfg.n_phases * h->K;
+  size_t off = 0;
+  t.map_off = off;
+  off = align256(off + px * (h->K > 256 ? 2 : 1));
+  t.fb_cap = (unsigned int)std::min<long long>(std::max<long long>(px / 64, 1024), 0x7fffffff);
+  t.fb_off = off;
+  off = align256(off + sizeof(unsigned long long) * t.fb_cap);
+  t.fbcnt_off = off;
+  off = align256(off + 16);
+  t.cnt_off = off;
+  off = align256(off + sizeof(unsigned int) * n_seg);
+  t.cur_off = off;
+  off = align256(off + sizeof(unsigned int) * n_seg);
+  t.sorted_off = off;
+  off = align256(off + sizeof(unsigned int) * px);
+  t.bytes = off;
+  return t;
+}
+
+blade_status blade_ms_train_layout(blade_ms_t h, int32_t* nt, int32_t* ntp, int32_t* n_seg) {
+  if (!h || !nt || !ntp || !n_seg) return fail(BLADE_EINVAL, "NULL argument");
+  const TrainVariant* v = train_variant(h);
+  if (!v) return fail(BLADE_EUNSUPPORTED, "no training kernel for this footprint / bucket layout");
+  *nt = train_nt(h);
+  *ntp = v->ntp;
+  *n_seg = h->cfg.n_phases * h->K;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_train_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t W, size_t* bytes) {
+  if (!h || !bytes) return fail(BLADE_EINVAL, "NULL argument");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  *bytes = train_plan(h, (long long)N * H * W).bytes;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_train_accumulate(blade_ms_t h, int32_t level, const float* z, const float* u_clean,
+                                       const float* u_coarse, int32_t N, int32_t H, int32_t W, double* E,
+                                       uint64_t* count, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  if (level < 0 || level >= h->n_stages) return fail(BLADE_EINVAL, "level %d not in [0, %d)", level, h->n_stages);
+  if (h->cfg.n_filter_channels != 1) return fail(BLADE_EUNSUPPORTED, "training of per-channel banks is not built");
+  const TrainVariant* v = train_variant(h);
+  if (!v) return fail(BLADE_EUNSUPPORTED, "no training kernel for this footprint / bucket layout");
+  const int n_seg = h->cfg.n_phases * h->K;
+  if (n_seg > 16384) return fail(BLADE_EUNSUPPORTED, "training supports n_phases * K <= 16384");
+  const long long px = (long long)N * H * W;
+  if (px >= (1LL << 32)) return fail(BLADE_EINVAL, "too many pixels for one training call");
+  if (N == 0) return BLADE_OK;
+  const bool multiscale = h->cfg.levels > 1;
+  if (!z || !u_clean || !E || !count || !ws || (multiscale && !u_coarse))
+    return fail(BLADE_EINVAL, "NULL buffer (u_coarse is required when levels > 1)");
+  const TrainPlan tp = train_plan(h, px);
+  if (ws_bytes < tp.bytes) return fail(BLADE_ESHAPE, "workspace %zu bytes < required %zu", ws_bytes, tp.bytes);
+  if ((s = check_dev_ptr(h, z, "z")) != BLADE_OK) return s;
+  if ((s = check_dev_ptr(h, u_clean, "u_clean")) != BLADE_OK) return s;
+  if (multiscale && (s = check_dev_ptr(h, u_coarse, "u_coarse")) != BLADE_OK) return s;
+  if ((s = check_dev_ptr(h, E, "E")) != BLADE_OK) return s;
+  if ((s = check_dev_ptr(h, count, "count")) != BLADE_OK) return s;
+  if ((s = check_dev_ptr(h, ws, "workspace")) != BLADE_OK) return s;
+  DeviceGuard guard(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)ws;
+  const int l = level;
+  // ---- selector on the noisy level (fp32 input, thresholds of stage `level`)
+  DownArgs da{};
+  da.zhi = z;
+  da.zlo = nullptr;
+  da.H = H;
+  da.W = W;
+  da.in_row0 = 0;
+  da.in_rows = H;
+  da.in_plane = (long long)H * W;
+  da.in_frame = 3 * da.in_plane;
+  da.map = w + tp.map_off;
+  da.s_r0 = 0;
+  da.s_rn = H;
+  da.H1 = da.W1 = 1;
+  da.base = 0;
+  da.n_strips = (W + down::STRIP - 1) / down::STRIP;
+  const long long col_tasks = (long long)N * da.n_strips;
+  const long long want_bands = std::max<long long>(1, (4LL * 16 * h->num_sms + col_tasks - 1) / col_tasks);
+  int RB = (int)std::min<long long>(128, std::max<long long>(16, (H + want_bands - 1) / want_bands));
+  RB = (RB + 1) & ~1;
+  da.RB = RB;
+  da.n_bands = (H + RB - 1) / RB;
+  da.n_tasks = (int)(col_tasks * da.n_bands);
+  da.fb_list = reinterpret_cast<unsigned long long*>(w + tp.fb_off);
+  da.fb_count = reinterpret_cast<unsigned int*>(w + tp.fbcnt_off);
+  da.fb_cap = tp.fb_cap;
+  da.N = N;
+  const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
+  const bool wide = h->K > 256;
+  CUDA_TRY(cudaMemsetAsync(da.fb_count, 0, sizeof(unsigned int), st));
+  down_kernel(false, false, fast, wide)<<<(unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS),
+                                           32 * down::WARPS, down_smem(false), st>>>(da, h->down[l]);
+  LAUNCH_CHECK("k_down (training selector)");
+  fixup_kernel(false, fast, wide)<<<4 * h->num_sms, 128, 0, st>>>(da, h->down[l]);
+  LAUNCH_CHECK("k_down_fixup (training selector)");
+  // ---- counting sort of the pixels by (phase, bucket), then the segmented fp64 SYRK
+  TrainArgs ta{};
+  ta.z = z;
+  ta.uc = u_clean;
+  ta.u1 = u_coarse;
+  ta.map = w + tp.map_off;
+  ta.N = N;
+  ta.H = H;
+  ta.W = W;
+  ta.H1 = (H + 1) / 2;
+  ta.W1 = (W + 1) / 2;
+  ta.n_phases = h->cfg.n_phases;
+  ta.K = h->K;
+  ta.n_seg = n_seg;
+  ta.count = reinterpret_cast<unsigned int*>(w + tp.cnt_off);
+  ta.cursor = reinterpret_cast<unsigned int*>(w + tp.cur_off);
+  ta.sorted = reinterpret_cast<unsigned int*>(w + tp.sorted_off);
+  ta.E = E;
+  ta.count_out = reinterpret_cast<unsigned long long*>(count);
+  ta.pix_per_cta = 512;
+  CUDA_TRY(cudaMemsetAsync(ta.count, 0, sizeof(unsigned int) * n_seg, st));
+  CUDA_TRY(cudaFuncSetAttribute(train_hist(wide), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(unsigned int) * n_seg)));
+  const unsigned g_px = (unsigned)std::min<long long>((px + 255) / 256, 4LL * h->num_sms);
+  train_hist(wide)<<<g_px, 256, sizeof(unsigned int) * n_seg, st>>>(ta);
+  LAUNCH_CHECK("k_train_hist");
+  train_scan()<<<1, 1024, 0, st>>>(ta);
+  LAUNCH_CHECK("k_train_scan");
+  train_scatter(wide)<<<g_px, 256, 0, st>>>(ta);
+  LAUNCH_CHECK("k_train_scatter");
+  v->gram<<<(unsigned)((px + ta.pix_per_cta - 1) / ta.pix_per_cta), 256, 0, st>>>(ta);
+  LAUNCH_CHECK("k_train_gram");
+  return BLADE_OK;
+}
+
+blade_status blade_ms_train_solve(blade_ms_t h, const double* E, const uint64_t* count, double ridge,
+                                  uint64_t min_count, float* taps) {
+  g_last_error.clear();
+  if (!h || !E || !count || !taps) return fail(BLADE_EINVAL, "NULL argument");
+  const TrainVariant* v = train_variant(h);
+  if (!v) return fail(BLADE_EUNSUPPORTED, "no training kernel for this footprint / bucket layout");
+  if (!(ridge >= 0.0) || !std::isfinite(ridge)) return fail(BLADE_EINVAL, "ridge must be finite and >= 0");
+  const int nt = train_nt(h), ntp = v->ntp, n_seg = h->cfg.n_phases * h->K, nf = h->cfg.fine_size;
+  std::vector<double> A((size_t)nt * nt), b(nt);
+  for (int sg = 0; sg < n_seg; ++sg) {
+    float* out = taps + (size_t)sg * nt;
+    const double* Es = E + (size_t)sg * ntp * ntp;
+    auto e = [&](int r, int c) { return (r / 4 <= c / 4) ? Es[(size_t)r * ntp + c] : Es[(size_t)c * ntp + r]; };
+    bool ok = count[sg] >= min_count && count[sg] > 0;
+    if (ok) {
+      double tr = 0.0;
+      for (int i = 0; i < nt; ++i) tr += e(i, i);
+      const double lam = ridge * tr / nt;
+      for (int i = 0; i < nt; ++i) {
+        for (int j = 0; j < nt; ++j) A[(size_t)i * nt + j] = e(i, j) + (i == j ? lam : 0.0);
+        b[i] = e(i, nt);
+      }
+      // Cholesky A = L L^T (in place, lower), then two triangular solves
+      for (int j = 0; j < nt && ok; ++j) {
+        double d = A[(size_t)j * nt + j];
+        for (int k = 0; k < j; ++k) d -= A[(size_t)j * nt + k] * A[(size_t)j * nt + k];
+        if (!(d > 0.0)) {
+          ok = false;
+          break;
+        }
+        const double ljj = std::sqrt(d);
+        A[(size_t)j * nt + j] = ljj;
+        for (int i = j + 1; i < nt; ++i) {
+          double x = A[(size_t)i * nt + j];
+          for (int k = 0; k < j; ++k) x -= A[(size_t)i * nt + k] * A[(size_t)j * nt + k];
+          A[(size_t)i * nt + j] = x / ljj;
+        }
+      }
+      if (ok) {
+        for (int i = 0; i < nt; ++i) {  // L y = b
+          double x = b[i];
+          for (int k = 0; k < i; ++k) x -= A[(size_t)i * nt + k] * b[k];
+          b[i] = x / A[(size_t)i * nt + i];
+        }
+        for (int i = nt - 1; i >= 0; --i) {  // L^T h = y
+          double x = b[i];
+          for (int k = i + 1; k < nt; ++k) x -= A[(size_t)k * nt + i] * b[k];
+          b[i] = x / A[(size_t)i * nt + i];
+        }
+        for (int i = 0; i < nt; ++i) {
+          if (!std::isfinite(b[i])) ok = false;
+          out[i] = (float)b[i];
+        }
+      }
+    }
+    if (!ok) {  // fallback: centred fine delta, zero coarse block [R28]
+      for (int i = 0; i < nt; ++i) out[i] = 0.0f;
+      out[(nf / 2) * nf + nf / 2] = 1.0f;
+    }
+  }
+  return BLADE_OK;
+}
+
 blade_status blade_ms_band_plan(const blade_ms_config* cfg, int32_t H, int32_t out_row0, int32_t out_rows,
                                 int32_t* in_row0, int32_t* in_rows) {
   if (!cfg || !in_row0 || !in_rows) return fail(BLADE_EINVAL, "NULL argument");

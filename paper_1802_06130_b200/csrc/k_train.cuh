@@ -1,0 +1,218 @@
+// NEXT f4: filter learning of PAPER.md:186-198 (§3, Eqs. 7-8) on the GPU — the per-(phase, bucket)
+// normal equations G = sum x x^T, m = sum x u of the stacked sample x = [R_i z^l ; R_{i/2} u^{l+1}]
+// (ABI tap order, R27), accumulated in fp64 as a segmented SYRK:
+//   k_train_hist    count the pixels of every segment s = phase * K + bucket
+//   k_train_scan    exclusive scan of the counts (one CTA)
+//   k_train_scatter counting sort of the pixel indices by segment
+//   k_train_gram    each CTA walks a slice of the sorted pixels in batches of 32: it gathers the
+//                   samples of the three channels (fine patch, coarse patch, target appended as
+//                   column nt) into shared memory as fp64, every thread accumulates 4 x 4 blocks of
+//                   the extended matrix E = sum [x; u][x; u]^T in registers (upper block triangle),
+//                   and flushes them with fp64 atomics to E[segment] when the segment changes.
+// E[s] (NTP x NTP, NTP = nt + 1 rounded up to 4) holds G in [0, nt)^2 and m in column nt.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <type_traits>
+
+#include "kernels.cuh"
+
+namespace blade {
+
+struct TrainArgs {
+  const float* z;       // noisy level l [N][3][H][W]
+  const float* uc;      // clean target at level l [N][3][H][W]
+  const float* u1;      // u^{l+1} [N][3][H1][W1] (nullptr when single-level)
+  const void* map;      // bucket map [N][H][W] (uint8, or uint16 when WIDE)
+  int N, H, W, H1, W1;
+  int n_phases, K, n_seg;
+  unsigned int* count;  // [n_seg] (per call)
+  unsigned int* cursor; // [n_seg]
+  unsigned int* sorted; // [N H W] pixel indices sorted by segment
+  double* E;            // [n_seg][NTP][NTP] (accumulated)
+  unsigned long long* count_out;  // [n_seg] (accumulated)
+  int pix_per_cta;
+};
+
+template <bool WIDE>
+__device__ __forceinline__ int train_seg(const TrainArgs& a, long long i) {
+  using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;
+  const long long hw = (long long)a.H * a.W;
+  const long long r = i % hw;
+  const int y = (int)(r / a.W), x = (int)(r - (long long)y * a.W);
+  const int k = static_cast<const MT*>(a.map)[i];
+  const int p = a.n_phases == 4 ? 2 * (y & 1) + (x & 1) : 0;
+  return p * a.K + k;
+}
+
+template <bool WIDE>
+__global__ void __launch_bounds__(256) k_train_hist(const TrainArgs a) {
+  extern __shared__ unsigned int hist[];
+  for (int i = threadIdx.x; i < a.n_seg; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const long long total = (long long)a.N * a.H * a.W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
+    atomicAdd(&hist[train_seg<WIDE>(a, i)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.n_seg; i += blockDim.x)
+    if (hist[i]) atomicAdd(&a.count[i], hist[i]);
+}
+
+// one CTA of 1024 threads: cursor = exclusive scan of count; count_out += count
+template <int = 0>
+__global__ void __launch_bounds__(1024) k_train_scan(const TrainArgs a) {
+  __shared__ unsigned int part[1024];
+  const int t = threadIdx.x;
+  const int per = (a.n_seg + 1023) / 1024;
+  const int b0 = t * per, b1 = min(b0 + per, a.n_seg);
+  unsigned int s = 0;
+  for (int i = b0; i < b1; ++i) s += a.count[i];
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
+    const unsigned int v = t >= off ? part[t - off] : 0u;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  unsigned int run = part[t] - s;  // exclusive prefix of this thread's range
+  for (int i = b0; i < b1; ++i) {
+    a.cursor[i] = run;
+    run += a.count[i];
+    a.count_out[i] += a.count[i];
+  }
+}
+
+template <bool WIDE>
+__global__ void __launch_bounds__(256) k_train_scatter(const TrainArgs a) {
+  const long long total = (long long)a.N * a.H * a.W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned int pos = atomicAdd(&a.cursor[train_seg<WIDE>(a, i)], 1u);
+    a.sorted[pos] = (unsigned int)i;
+  }
+}
+
+template <int NF, int NC>
+struct TrainShape {
+  static constexpr int NT = NF * NF + NC * NC;
+  static constexpr int NTP = (NT + 1 + 3) & ~3;  // + target column, 4-aligned
+  static constexpr int NB = NTP / 4;
+  static constexpr int UB = NB * (NB + 1) / 2;    // upper 4 x 4 blocks
+  static constexpr int THREADS = 256;
+  static constexpr int BPT = (UB + THREADS - 1) / THREADS;  // blocks per thread
+  static constexpr int BATCH = NTP <= 64 ? 32 : 16;  // pixels per gather (<= 40 KB of fp64)
+  static_assert(BPT <= 2, "training supports nt + 1 <= 88 (up to 7x7 + 5x5 pairs / 9x9 single)");
+};
+
+template <int NF, int NC, bool WIDE>
+__global__ void __launch_bounds__(256) k_train_gram(const TrainArgs a) {
+  using TS = TrainShape<NF, NC>;
+  constexpr int NTP = TS::NTP, NT = TS::NT, B = TS::BATCH;
+  constexpr int RF = NF / 2, RC = NC / 2;
+  __shared__ double xs[B][3][NTP];
+  __shared__ int segs[B];
+  const int t = threadIdx.x;
+  // this thread's upper blocks (ra, cb)
+  int ba[TS::BPT], bb[TS::BPT];
+  bool act[TS::BPT];
+#pragma unroll
+  for (int q = 0; q < TS::BPT; ++q) {
+    int blk = t + q * TS::THREADS;
+    act[q] = blk < TS::UB;
+    int r = 0;
+    while (act[q] && blk >= TS::NB - r) {
+      blk -= TS::NB - r;
+      ++r;
+    }
+    ba[q] = r;
+    bb[q] = r + blk;
+  }
+  double acc[TS::BPT][4][4];
+#pragma unroll
+  for (int q = 0; q < TS::BPT; ++q)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[q][i][j] = 0.0;
+
+  const long long total = (long long)a.N * a.H * a.W;
+  const long long r0 = (long long)blockIdx.x * a.pix_per_cta;
+  const long long r1 = min(total, r0 + a.pix_per_cta);
+  int cur = -1;
+  auto flush = [&]() {
+    if (cur < 0) return;
+    double* Es = a.E + (long long)cur * NTP * NTP;
+#pragma unroll
+    for (int q = 0; q < TS::BPT; ++q) {
+      if (!act[q]) continue;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          atomicAdd(Es + (4 * ba[q] + i) * NTP + 4 * bb[q] + j, acc[q][i][j]);
+          acc[q][i][j] = 0.0;
+        }
+    }
+  };
+  const long long hw = (long long)a.H * a.W;
+  for (long long b0 = r0; b0 < r1; b0 += B) {
+    const int nb = (int)min((long long)B, r1 - b0);
+    __syncthreads();  // previous batch consumed
+    // ---- gather the samples (fp64), the target as column NT, zero padding
+    for (int e = t; e < nb * 3 * NTP; e += TS::THREADS) {
+      const int j = e / (3 * NTP), rem = e - j * 3 * NTP;
+      const int c = rem / NTP, tap = rem - c * NTP;
+      const long long pix = a.sorted[b0 + j];
+      const int n = (int)(pix / hw);
+      const long long r = pix - n * hw;
+      const int y = (int)(r / a.W), x = (int)(r - (long long)y * a.W);
+      float v = 0.0f;
+      if (tap < NF * NF) {
+        const int dy = tap / NF - RF, dx = tap % NF - RF;
+        v = __ldg(a.z + (((long long)n * 3 + c) * a.H + fold_idx(y + dy, a.H)) * a.W + fold_idx(x + dx, a.W));
+      } else if (tap < NT) {
+        if constexpr (NC > 0) {
+          const int tc = tap - NF * NF;
+          const int dy = tc / NC - RC, dx = tc % NC - RC;
+          v = __ldg(a.u1 + (((long long)n * 3 + c) * a.H1 + fold_idx(y / 2 + dy, a.H1)) * a.W1 +
+                    fold_idx(x / 2 + dx, a.W1));
+        }
+      } else if (tap == NT) {
+        v = __ldg(a.uc + (((long long)n * 3 + c) * a.H + y) * a.W + x);
+      }
+      xs[j][c][tap] = (double)v;
+    }
+    for (int j = t; j < nb; j += TS::THREADS) segs[j] = train_seg<WIDE>(a, a.sorted[b0 + j]);
+    __syncthreads();
+    // ---- accumulate (uniform over the CTA: segment changes flush)
+    for (int j = 0; j < nb; ++j) {
+      const int sg = segs[j];
+      if (sg != cur) {
+        flush();
+        cur = sg;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int q = 0; q < TS::BPT; ++q) {
+          if (!act[q]) continue;
+          const double* xa = &xs[j][c][4 * ba[q]];
+          const double* xb = &xs[j][c][4 * bb[q]];
+          double va[4], vb[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            va[i] = xa[i];
+            vb[i] = xb[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) acc[q][i][k] = fma(va[i], vb[k], acc[q][i][k]);
+        }
+      }
+    }
+  }
+  flush();
+}
+
+}  // namespace blade

@@ -8,6 +8,7 @@
 #include "k_down.cuh"
 #include "k_stage_ph.cuh"
 #include "k_stage_tma.cuh"
+#include "k_train.cuh"
 #include "kernels.cuh"
 
 namespace blade {
@@ -43,6 +44,18 @@ using DownKernel = void (*)(const DownArgs, const DownParams);
 // wide: uint16 bucket maps (K > 256, NEXT f2)
 DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide);
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide);
+
+// Training (NEXT f4): segmented fp64 SYRK of the normal equations.
+using TrainKernel = void (*)(const TrainArgs);
+struct TrainVariant {
+  int nf, nc, ntp;
+  TrainKernel gram;
+  bool wide;
+};
+const std::vector<TrainVariant>& train_variants();
+TrainKernel train_hist(bool wide);
+TrainKernel train_scatter(bool wide);
+TrainKernel train_scan();
 
 }  // namespace tables
 }  // namespace blade
