@@ -47,6 +47,9 @@ def parse():
                     help="override the frame count (profiling only; not a bench line)")
     ap.add_argument("--impl", default="blade", choices=["blade", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--train", action="store_true",
+                    help="NEXT f4: time the training accumulation (normal equations) of stage 0 "
+                         "over this rank's frames instead of the denoise (not the headline)")
     ap.add_argument("--ycc", action="store_true",
                     help="per-channel Y/Cb/Cr banks (NEXT row f1) instead of one bank for R,G,B")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -304,6 +307,26 @@ def main():
         io_in = 3 * shard.in_rows * W * 4
         io_out = 3 * shard.out_rows * W * 4
 
+    if args.train:
+        if shard.mode != "frames":
+            raise SystemExit("--train needs a frame-split config")
+        clean_host = torch.empty_like(x_host)
+        for i in range(n_local):
+            bs.scene(cfg.seed, f0 + i, H, W, cfg.n_grat, cfg.n_disk, "none", 0.0, 0.0,
+                     out=clean_host[i].numpy())
+        clean = clean_host.to(dev)
+        coarse = h.pyramid(x)[0] if cfg.levels > 1 else None
+        E, cnt = h.train_accumulators()
+        tws = torch.empty(1, dtype=torch.uint8, device=dev)
+        import ctypes as _ct
+        from paper_1802_06130_b200.blade_ms import lib as _lib
+        b = _ct.c_size_t()
+        _lib().blade_ms_train_workspace_size(h._h, n_local, H, W, _ct.byref(b))
+        tws = torch.empty(b.value, dtype=torch.uint8, device=dev)
+
+        def step():  # noqa: F811 - the timed step is one accumulation pass over the frames
+            h.train_accumulate(0, x, clean, coarse, E, cnt, tws, stream)
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -334,6 +357,23 @@ def main():
     total_px = cfg.N * H * W  # all ranks together (frames: the batch; bands: the whole image)
     assert world > 1 or units(cfg, shard) == total_px
     value = total_px / 1e6 / (ms_per_step / 1e3)
+
+    if args.train:
+        nt = cfg.fine_size ** 2 + (cfg.coarse_size ** 2 if cfg.levels > 1 else 0)
+        line = {"metric": "megapixels/sec of training data (stage-0 normal equations, f4)",
+                "value": value, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64 accumulation",
+                "data": "synthetic", "config": {"workload": cfg.name, "frames": cfg.N, "H": H, "W": W,
+                                                 "taps": nt, "segments": cfg.n_phases * cfg.K},
+                "dfma_per_px": 3 * (((nt + 1 + 3) // 4) * (((nt + 1 + 3) // 4) + 1) // 2) * 16,
+                "clocks": clocks}
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
 
     # ---- per-kernel breakdown: same steps again with events around every launch
     h.set_profiling(True)

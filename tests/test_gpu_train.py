@@ -111,3 +111,27 @@ def test_train_recovers_a_known_bank():
     well = ok & np.array([np.linalg.cond(G[k]) < 1e5 if ok[k] else False for k in range(len(ok))])
     if well.any():
         np.testing.assert_allclose(taps[well], bank.reshape(-1, nt)[well], atol=1e-3)
+
+
+def _psnr(a, b):
+    return float(10 * np.log10(1.0 / np.mean((np.asarray(a, np.float64) - b) ** 2)))
+
+
+@pytest.mark.parametrize("name,H,W,N", [("c1", 256, 256, 6), ("c0", 192, 192, 6), ("c3", 216, 384, 4)])
+def test_train_multiscale_denoises_its_training_set(name, H, W, N):
+    """SPEC.md:359 ("training then inference on the training images themselves -> PSNR strictly
+    greater than noisy-input PSNR"): the coarse-to-fine schedule end to end."""
+    from paper_1802_06130_b200 import BladeMS
+    from paper_1802_06130_b200.train import train_multiscale
+    cfg = copy.deepcopy(bs.load_config(name))
+    cfg.H, cfg.W, cfg.N = H, W, N
+    noisy = cfg.batch()
+    clean = np.stack([bs.scene(cfg.seed, i, H, W, cfg.n_grat, cfg.n_disk, "none", 0.0, 0.0)
+                      for i in range(N)]).astype(np.float32)
+    nd, cd = torch.from_numpy(noisy).cuda(), torch.from_numpy(clean).cuda()
+    taps, counts = train_multiscale(cfg, nd, cd, ridge=1e-3)
+    assert np.isfinite(taps).all()
+    out = BladeMS.from_config(cfg, taps=taps).denoise(nd).cpu().numpy()
+    p_noisy, p_out = _psnr(noisy, clean), _psnr(out, clean)
+    print(f"{name}: noisy {p_noisy:.2f} dB -> trained BLADE {p_out:.2f} dB")
+    assert p_out > p_noisy + 3.0
