@@ -9,19 +9,15 @@
 // decimated column x / 2. Lanes 2..29 produce outputs (56 columns per strip); lanes 0, 1, 30, 31
 // only supply the horizontal halo (gradient 1 + window 2 columns; decimation 3 / 4 columns).
 // Horizontal neighbours come from warp shuffles, vertical neighbours from registers:
-//   - each lane prefetches its own two columns of the next rows with 4-byte cp.async into a
+//   - each lane prefetches its own two columns of the next rows with 4/8-byte cp.async into a
 //     lane-private ring in shared memory (RING rows deep, no cross-lane smem traffic, no barrier);
 //   - gradients (unscaled: 2 g), the products A = sum_c gx^2, B = sum_c gx gy, C = sum_c gy^2
-//     and the 5x5 Gaussian window are fp64 (the window runs as a horizontal pass over shuffled
+//     and the 5x5 Gaussian window are fp32 (the window runs as a horizontal pass over shuffled
 //     neighbour products and a 5-deep vertical ring of pending output rows);
-//   - decimation: horizontal 8 taps over shuffled neighbours, then a 4-deep vertical ring.
-//
-// Precision (DESIGN.md §6 H1): theta = atan2(2B, A - C) / 2 + pi / 2 is ill-conditioned where the
-// tensor is near-isotropic (an absolute error e in the window sums moves theta by ~e/(l1 - l2)),
-// so every sum that feeds theta is fp64 from an exact fp64 pyramid; the final atan2f runs on the
-// fp32-rounded, well-conditioned vector (A - C, 2B). Strength and coherence decisions are
-// well-conditioned and use the fp32 tests of k_down.cuh:
-//   S >= t <=> T/2 + r >= t^2,   C >= t <=> r (1 + t^2) >= 2 t T/2   (r = sqrt((A-C)^2/4 + B^2)).
+//   - the bucket decision is fp32 with a certificate: a pixel whose orientation bin the fp32 error
+//     bound cannot guarantee is queued for k_down_fixup, which recomputes it in fp64 (below);
+//   - decimation is fp64 (the next level's selector needs the pyramid to ~1e-12): horizontal 8
+//     taps over shuffled fp64 neighbours, then a 4-deep vertical ring; output hi/lo fp32 pair.
 // fp32 -> fp64 conversions run at 16/clk/SM on B200 (measured, scripts/probes/tput.cu), so each
 // element is converted exactly once, by the lane that loads it.
 #pragma once
@@ -162,7 +158,7 @@ __device__ __forceinline__ int bucket_of(double a, double b, double c, const Dow
 // psi decides the orientation bin, are each off by <= 16 u T, and every sign test below (the
 // quadrant signs of X, Y and the cross products with the bin edges, |v| <= T) is off by at most
 // 32 u T. A test whose |value| exceeds kCert T = 64 u T therefore has the sign of the exact test;
-// a pixel with any closer test is recomputed in fp64 (abc_fp64). Strength and coherence are
+// a pixel with any closer test is queued and recomputed in fp64 (k_down_fixup). Strength and coherence are
 // well-conditioned: their fp32 errors (~1e-6 relative) stay far inside the 1e-5 parity window.
 constexpr float kCert = 64.0f * 5.9604644775390625e-8f;
 
@@ -251,43 +247,6 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
   k = prm.tc_nonpos + (h > 0.0f ? k : 0);  // C = 0 when l1 = 0 [R6]
   if constexpr (FAST) return (o * 3 + s) * 3 + k;  // FAST layout: 16 x 3 x 3
   return (o * prm.n_s + s) * prm.n_c + k;
-}
-
-// fp64 recomputation of (a, b, c) at one pixel (unscaled gradients, fp64 sums, the exact fp64
-// level from hi + lo). Unused by the fix-up kernel (which spreads the window over a warp); kept as
-// the plain single-thread reference of the same sums.
-template <bool HILO>
-__device__ __forceinline__ void abc_fp64(const DownArgs& a, const DownParams& prm, int n, int xp, int yp,
-                                      double& A, double& B, double& C) {
-  auto Z = [&](int c, int y, int x) -> double {
-    int br = fold_idx(y, a.H) - a.in_row0;
-    br = min(max(br, 0), a.in_rows - 1);
-    const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.W + fold_idx(x, a.W);
-    double v = (double)a.zhi[o];
-    if constexpr (HILO) v += (double)a.zlo[o];
-    return v;
-  };
-  A = B = C = 0.0;
-  for (int dy = -2; dy <= 2; ++dy) {
-    double ra = 0.0, rb = 0.0, rc = 0.0;
-    for (int dx = -2; dx <= 2; ++dx) {
-      const int y = yp + dy, x = xp + dx;
-      double pa = 0.0, pb = 0.0, pc = 0.0;
-      for (int c = 0; c < 3; ++c) {
-        const double gx = Z(c, y, x + 1) - Z(c, y, x - 1);
-        const double gy = Z(c, y + 1, x) - Z(c, y - 1, x);
-        pa = fma(gx, gx, pa);
-        pb = fma(gx, gy, pb);
-        pc = fma(gy, gy, pc);
-      }
-      ra = fma(prm.wp[dx + 2], pa, ra);
-      rb = fma(prm.wp[dx + 2], pb, rb);
-      rc = fma(prm.wp[dx + 2], pc, rc);
-    }
-    A = fma(prm.wp[dy + 2], ra, A);
-    B = fma(prm.wp[dy + 2], rb, B);
-    C = fma(prm.wp[dy + 2], rc, C);
-  }
 }
 
 // grid: ceil(n_tasks / WARPS) CTAs of 32 * WARPS threads; task = (frame, band, strip), strip fastest.
