@@ -35,11 +35,11 @@ struct TrainArgs {
 };
 
 template <bool WIDE>
-__device__ __forceinline__ int train_seg(const TrainArgs& a, long long i) {
+__device__ __forceinline__ int train_seg(const TrainArgs& a, unsigned int i) {
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;
-  const long long hw = (long long)a.H * a.W;
-  const long long r = i % hw;
-  const int y = (int)(r / a.W), x = (int)(r - (long long)y * a.W);
+  const unsigned int hw = (unsigned int)a.H * (unsigned int)a.W;  // N H W < 2^32 (host check)
+  const unsigned int r = i % hw;
+  const int y = (int)(r / (unsigned int)a.W), x = (int)(r - (unsigned int)y * (unsigned int)a.W);
   const int k = static_cast<const MT*>(a.map)[i];
   const int p = a.n_phases == 4 ? 2 * (y & 1) + (x & 1) : 0;
   return p * a.K + k;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) k_train_hist(const TrainArgs a) {
   __syncthreads();
   const long long total = (long long)a.N * a.H * a.W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
-    atomicAdd(&hist[train_seg<WIDE>(a, i)], 1u);
+    atomicAdd(&hist[train_seg<WIDE>(a, (unsigned int)i)], 1u);
   __syncthreads();
   for (int i = threadIdx.x; i < a.n_seg; i += blockDim.x)
     if (hist[i]) atomicAdd(&a.count[i], hist[i]);
@@ -87,7 +87,7 @@ template <bool WIDE>
 __global__ void __launch_bounds__(256) k_train_scatter(const TrainArgs a) {
   const long long total = (long long)a.N * a.H * a.W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const unsigned int pos = atomicAdd(&a.cursor[train_seg<WIDE>(a, i)], 1u);
+    const unsigned int pos = atomicAdd(&a.cursor[train_seg<WIDE>(a, (unsigned int)i)], 1u);
     a.sorted[pos] = (unsigned int)i;
   }
 }
@@ -100,6 +100,7 @@ struct TrainShape {
   static constexpr int UB = NB * (NB + 1) / 2;    // upper 4 x 4 blocks
   static constexpr int THREADS = 256;
   static constexpr int BPT = (UB + THREADS - 1) / THREADS;  // blocks per thread
+  static constexpr int GROUPS = UB <= THREADS ? THREADS / UB : 1;  // thread groups splitting the samples
   static constexpr int BATCH = NTP <= 64 ? 32 : 16;  // pixels per gather (<= 40 KB of fp64)
   static_assert(BPT <= 2, "training supports nt + 1 <= 88 (up to 7x7 + 5x5 pairs / 9x9 single)");
 };
@@ -112,13 +113,16 @@ __global__ void __launch_bounds__(256) k_train_gram(const TrainArgs a) {
   __shared__ double xs[B][3][NTP];
   __shared__ int segs[B];
   const int t = threadIdx.x;
-  // this thread's upper blocks (ra, cb)
+  // this thread's upper blocks (ra, cb); with GROUPS > 1 the blocks are replicated over thread
+  // groups that take every GROUPS-th pixel of a batch (no idle threads for small filters)
+  const int grp = TS::GROUPS > 1 ? t / TS::UB : 0;
+  const int tb = TS::GROUPS > 1 ? t - grp * TS::UB : t;
   int ba[TS::BPT], bb[TS::BPT];
   bool act[TS::BPT];
 #pragma unroll
   for (int q = 0; q < TS::BPT; ++q) {
-    int blk = t + q * TS::THREADS;
-    act[q] = blk < TS::UB;
+    int blk = tb + q * TS::THREADS;
+    act[q] = blk < TS::UB && grp < TS::GROUPS;
     int r = 0;
     while (act[q] && blk >= TS::NB - r) {
       blk -= TS::NB - r;
@@ -154,38 +158,53 @@ __global__ void __launch_bounds__(256) k_train_gram(const TrainArgs a) {
         }
     }
   };
-  const long long hw = (long long)a.H * a.W;
+  const unsigned int hw = (unsigned int)a.H * (unsigned int)a.W;  // N H W < 2^32 (checked on the host)
+  __shared__ int pn[B], py[B], px[B];
+  for (int e = t; e < B * 3 * (NTP - NT - 1); e += TS::THREADS) {  // padding columns stay zero
+    const int j = e / (3 * (NTP - NT - 1)), rem = e - j * 3 * (NTP - NT - 1);
+    const int c = rem / (NTP - NT - 1), q = rem - c * (NTP - NT - 1);
+    xs[j][c][NT + 1 + q] = 0.0;
+  }
   for (long long b0 = r0; b0 < r1; b0 += B) {
     const int nb = (int)min((long long)B, r1 - b0);
     __syncthreads();  // previous batch consumed
-    // ---- gather the samples (fp64), the target as column NT, zero padding
-    for (int e = t; e < nb * 3 * NTP; e += TS::THREADS) {
-      const int j = e / (3 * NTP), rem = e - j * 3 * NTP;
-      const int c = rem / NTP, tap = rem - c * NTP;
-      const long long pix = a.sorted[b0 + j];
-      const int n = (int)(pix / hw);
-      const long long r = pix - n * hw;
-      const int y = (int)(r / a.W), x = (int)(r - (long long)y * a.W);
-      float v = 0.0f;
-      if (tap < NF * NF) {
-        const int dy = tap / NF - RF, dx = tap % NF - RF;
-        v = __ldg(a.z + (((long long)n * 3 + c) * a.H + fold_idx(y + dy, a.H)) * a.W + fold_idx(x + dx, a.W));
-      } else if (tap < NT) {
-        if constexpr (NC > 0) {
-          const int tc = tap - NF * NF;
-          const int dy = tc / NC - RC, dx = tc % NC - RC;
-          v = __ldg(a.u1 + (((long long)n * 3 + c) * a.H1 + fold_idx(y / 2 + dy, a.H1)) * a.W1 +
-                    fold_idx(x / 2 + dx, a.W1));
-        }
-      } else if (tap == NT) {
-        v = __ldg(a.uc + (((long long)n * 3 + c) * a.H + y) * a.W + x);
-      }
-      xs[j][c][tap] = (double)v;
+    // ---- decode the batch's pixels once (32-bit), with their segments
+    if (t < nb) {
+      const unsigned int pix = a.sorted[b0 + t];
+      const unsigned int n = pix / hw, r = pix - n * hw;
+      const unsigned int y = r / (unsigned int)a.W;
+      pn[t] = (int)n;
+      py[t] = (int)y;
+      px[t] = (int)(r - y * (unsigned int)a.W);
+      segs[t] = train_seg<WIDE>(a, pix);
     }
-    for (int j = t; j < nb; j += TS::THREADS) segs[j] = train_seg<WIDE>(a, a.sorted[b0 + j]);
+    __syncthreads();
+    // ---- gather the samples (fp64): fine taps, coarse taps, target (column NT); three
+    //      branch-free loops so the lanes of a warp stay converged
+    for (int e = t; e < nb * 3 * NF * NF; e += TS::THREADS) {
+      const int j = e / (3 * NF * NF), rem = e - j * (3 * NF * NF);
+      const int c = rem / (NF * NF), tap = rem - c * (NF * NF);
+      const int dy = tap / NF - RF, dx = tap % NF - RF;
+      xs[j][c][tap] = (double)__ldg(a.z + (((long long)pn[j] * 3 + c) * a.H + fold_idx(py[j] + dy, a.H)) * a.W +
+                                    fold_idx(px[j] + dx, a.W));
+    }
+    if constexpr (NC > 0) {
+      for (int e = t; e < nb * 3 * NC * NC; e += TS::THREADS) {
+        const int j = e / (3 * NC * NC), rem = e - j * (3 * NC * NC);
+        const int c = rem / (NC * NC), tc = rem - c * (NC * NC);
+        const int dy = tc / NC - RC, dx = tc % NC - RC;
+        xs[j][c][NF * NF + tc] =
+            (double)__ldg(a.u1 + (((long long)pn[j] * 3 + c) * a.H1 + fold_idx(py[j] / 2 + dy, a.H1)) * a.W1 +
+                          fold_idx(px[j] / 2 + dx, a.W1));
+      }
+    }
+    for (int e = t; e < nb * 3; e += TS::THREADS) {
+      const int j = e / 3, c = e - 3 * j;
+      xs[j][c][NT] = (double)__ldg(a.uc + (((long long)pn[j] * 3 + c) * a.H + py[j]) * a.W + px[j]);
+    }
     __syncthreads();
     // ---- accumulate (uniform over the CTA: segment changes flush)
-    for (int j = 0; j < nb; ++j) {
+    for (int j = grp; j < nb; j += TS::GROUPS) {
       const int sg = segs[j];
       if (sg != cur) {
         flush();
