@@ -390,10 +390,10 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.base = R.lo & ~1;
     const int span = R.hi - da.base;
     da.n_strips = (p.W[l] + down::STRIP - 1) / down::STRIP;
-    // band height: enough warps for ~4 waves of 16 resident warps per SM, 16..128 rows (even)
+    // band height: enough warps for ~4 waves of 16 resident warps per SM, 8..128 rows (even)
     const long long col_tasks = (long long)N * da.n_strips;
     const long long want_bands = std::max<long long>(1, (4LL * 16 * h->num_sms + col_tasks - 1) / col_tasks);
-    int RB = (int)std::min<long long>(128, std::max<long long>(16, (span + want_bands - 1) / want_bands));
+    int RB = (int)std::min<long long>(128, std::max<long long>(8, (span + want_bands - 1) / want_bands));
     RB = (RB + 1) & ~1;
     da.RB = RB;
     da.n_bands = (span + RB - 1) / RB;
