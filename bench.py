@@ -52,6 +52,9 @@ def parse():
                          "over this rank's frames instead of the denoise (not the headline)")
     ap.add_argument("--ycc", action="store_true",
                     help="per-channel Y/Cb/Cr banks (NEXT row f1) instead of one bank for R,G,B")
+    ap.add_argument("--chunk", type=int, default=0,
+                    help="NEXT f3: frame-chunked schedule, chunks of this many frames (0 = off)")
+    ap.add_argument("--streams", type=int, default=2, help="internal streams of the chunked schedule")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the oracle sample (cpu_baseline)")
@@ -273,15 +276,27 @@ def main():
                      out=xn[i])
         x = x_host.to(dev, non_blocking=False)
         out = torch.empty_like(x)
-        ws = h.workspace(n_local, H, W)
+        if args.chunk:
+            ws = torch.empty(h.pipeline_workspace_size(args.chunk, args.streams, H, W),
+                             dtype=torch.uint8, device=dev)
 
-        def step():
-            h.denoise(x, out, ws, stream)
+            def step():
+                h.denoise_pipelined(x, out, args.chunk, args.streams, ws, stream)
+        else:
+            ws = h.workspace(n_local, H, W)
+
+            def step():
+                h.denoise(x, out, ws, stream)
 
         def e2e_step():
             h.denoise_host(x_host, out_host, d_in, out, ws, stream)
         out_host = torch.empty_like(x_host).pin_memory()
         d_in = torch.empty_like(x)
+        if args.chunk:
+            ws_e2e = h.workspace(n_local, H, W)
+
+            def e2e_step():  # noqa: F811 - the host path keeps its own frame pipeline
+                h.denoise_host(x_host, out_host, d_in, out, ws_e2e, stream)
         io_in = io_out = n_local * 3 * H * W * 4
     else:
         # ---- this rank's row band of the one image: input rows of its dependency cone
@@ -398,8 +413,8 @@ def main():
     e2e_val = total_px / 1e6 / (e2e_t / 1e3)
 
     # ---- roofline of the dominant kernel
-    if shard.mode == "frames":
-        work = algorithmic_work(cfg, n_local)
+    if shard.mode == "frames":  # per launch: a chunk of frames under the chunked schedule
+        work = algorithmic_work(cfg, min(args.chunk, n_local) if args.chunk else n_local)
     else:  # a band: the work model of an out_rows-row image (the halo rows are not counted)
         work = algorithmic_work(bs.Config(**{**cfg.__dict__, "H": shard.out_rows}), 1)
     kern = {k: (t / c, c) for k, (t, c) in prof.items()}
@@ -448,7 +463,8 @@ def main():
         roof = {"bound": "hbm", "kernel": f"k_down level {dom[1]}", "achieved": ach, "peak": hbm_peak,
                 "unit": "GB/s", "frac": ach / hbm_peak, "traffic": traffic,
                 "ms_per_launch": dom_ms}
-    step_bytes = sum(v["bytes"] for v in work.values())
+    step_work = algorithmic_work(cfg, n_local) if shard.mode == "frames" else work
+    step_bytes = sum(v["bytes"] for v in step_work.values())
     hbm_ach = step_bytes / (ms_per_step / 1e3) / 1e9  # per GPU
     names = {"selector": "k_down", "stage": "k_stage", "decimate": "k_decimate"}
     breakdown = {f"{names.get(k[0], k[0])}{k[1]}": round(t, 4) for k, (t, c) in sorted(kern.items())}
@@ -480,7 +496,9 @@ def main():
                                        f"row bands over {world} GPU(s) with recomputed halo "
                                        f"(rank 0: out rows {shard.out_row0}+{shard.out_rows}, "
                                        f"in rows {shard.in_row0}+{shard.in_rows}), no collective"),
-                       "l2": "inputs larger than L2 (no flush)"},
+                       "l2": "inputs larger than L2 (no flush)",
+                       "schedule": (f"frame chunks of {args.chunk} on {args.streams} streams (f3)"
+                                    if args.chunk and shard.mode == "frames" else "whole batch per launch")},
             "roofline": roof,
             "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm_ach / hbm_peak,
@@ -491,7 +509,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "MP/s", "h2d_bytes_per_step": io_in,
                     "d2h_bytes_per_step": io_out, "ms_per_step": e2e_t},
-            "gpu_launches": args.steps * h.launch_count(n_local, H, W) * world,
+            "gpu_launches": args.steps * world * (
+                h.launch_count(n_local, H, W) if not (args.chunk and shard.mode == "frames") else
+                h.launch_count(args.chunk, H, W) * -(-n_local // args.chunk)),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -129,6 +129,24 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
                                    void* workspace, size_t ws_bytes, void* cuda_stream);
 
 /*
+ * Frame-chunked schedule (NEXT f3, SURVEY.md §8 "L2-resident band pipeline on 1 GPU", PAPER.md:314
+ * "time is linear in pixels"): the batch is cut into chunks of `chunk` frames (the last one may be
+ * shorter); chunk i runs the whole cascade of blade_ms_denoise on internal stream i % n_streams,
+ * forked from and joined back into `cuda_stream`, in its own slice of the workspace. A chunk's
+ * input, pyramid levels, maps and stage outputs (about 48 MB per 1080p frame) then stay resident
+ * in the 126 MB L2 between the down pass and the up pass instead of round-tripping through HBM
+ * (DESIGN.md §10c). chunk >= 1, n_streams in 1..4 (EINVAL otherwise). Same buffer rules as
+ * blade_ms_denoise; the workspace size comes from blade_ms_pipeline_workspace_size (n_streams
+ * slices of a chunk-sized workspace). Output equals blade_ms_denoise bit-exactly. Asynchronous
+ * on `cuda_stream` (graph-capturable: the fork / join are event waits).
+ */
+blade_status blade_ms_pipeline_workspace_size(blade_ms_t h, int32_t chunk, int32_t n_streams,
+                                              int32_t H, int32_t W, size_t* bytes);
+blade_status blade_ms_denoise_pipelined(blade_ms_t h, const float* in, float* out, int32_t N,
+                                        int32_t H, int32_t W, int32_t chunk, int32_t n_streams,
+                                        void* workspace, size_t ws_bytes, void* cuda_stream);
+
+/*
  * Row bands (one huge image split over GPUs, BASELINE.json configs[4]).
  * blade_ms_band_rows: input rows [*in_row0, *in_row0 + *in_rows) of the full H-row image needed
  * to produce output rows [out_row0, out_row0 + out_rows) bit-identically to the full-image call

@@ -50,6 +50,7 @@ class _Info(ctypes.Structure):
 
 
 EXPORTS = ["blade_ms_create", "blade_ms_workspace_size", "blade_ms_denoise", "blade_ms_denoise_host",
+           "blade_ms_pipeline_workspace_size", "blade_ms_denoise_pipelined",
            "blade_ms_band_rows", "blade_ms_band_plan", "blade_ms_fallback_count",
            "blade_ms_train_layout", "blade_ms_train_workspace_size", "blade_ms_train_accumulate",
            "blade_ms_train_solve", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
@@ -82,6 +83,8 @@ def lib():
                                   ctypes.c_int, ctypes.POINTER(P)]
     L.blade_ms_workspace_size.argtypes = [P, i32, i32, i32, ctypes.POINTER(sz)]
     L.blade_ms_denoise.argtypes = [P, P, P, i32, i32, i32, P, sz, P]
+    L.blade_ms_pipeline_workspace_size.argtypes = [P, i32, i32, i32, i32, ctypes.POINTER(sz)]
+    L.blade_ms_denoise_pipelined.argtypes = [P, P, P, i32, i32, i32, i32, i32, P, sz, P]
     L.blade_ms_denoise_host.argtypes = [P, P, P, i32, i32, i32, P, P, P, sz, P]
     L.blade_ms_band_rows.argtypes = [P, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.blade_ms_band_plan.argtypes = [ctypes.POINTER(_Config), i32, i32, i32, ctypes.POINTER(i32),
@@ -285,6 +288,28 @@ class BladeMS:
         ws = self.workspace(N, H, W) if workspace is None else workspace
         _check(lib().blade_ms_denoise(self._h, _ptr(x), _ptr(out), N, H, W, _ptr(ws), ws.numel(),
                                       _stream_ptr(stream)))
+        return out
+
+    def pipeline_workspace_size(self, chunk: int, n_streams: int, H: int, W: int) -> int:
+        n = ctypes.c_size_t()
+        _check(lib().blade_ms_pipeline_workspace_size(self._h, chunk, n_streams, H, W, ctypes.byref(n)))
+        return n.value
+
+    def denoise_pipelined(self, x: torch.Tensor, out: torch.Tensor | None = None, chunk: int = 1,
+                          n_streams: int = 2, workspace: torch.Tensor | None = None,
+                          stream=None) -> torch.Tensor:
+        """Frame-chunked schedule (NEXT f3): chunks of `chunk` frames on `n_streams` internal
+        streams, intermediates L2-resident; bit-identical to denoise()."""
+        self._check_img(x, "x")
+        N, _, H, W = x.shape
+        out = torch.empty_like(x) if out is None else out
+        self._check_img(out, "out")
+        if workspace is None:
+            workspace = torch.empty(self.pipeline_workspace_size(chunk, n_streams, H, W),
+                                    dtype=torch.uint8, device=f"cuda:{self.device}")
+        _check(lib().blade_ms_denoise_pipelined(self._h, _ptr(x), _ptr(out), N, H, W, chunk,
+                                                n_streams, _ptr(workspace), workspace.numel(),
+                                                _stream_ptr(stream)))
         return out
 
     def denoise_host(self, x_host: torch.Tensor, out_host: torch.Tensor, d_in: torch.Tensor,

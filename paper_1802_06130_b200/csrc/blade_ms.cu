@@ -166,6 +166,11 @@ struct blade_ms {
   bool profiling = false;
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
+  // frame-chunked schedule (blade_ms_denoise_pipelined): internal streams, fork / join events
+  static constexpr int kMaxStreams = 4;
+  cudaStream_t pipe[kMaxStreams] = {};
+  cudaEvent_t pipe_fork = nullptr;
+  cudaEvent_t pipe_join[kMaxStreams] = {};
 };
 
 namespace {
@@ -390,9 +395,14 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.base = R.lo & ~1;
     const int span = R.hi - da.base;
     da.n_strips = (p.W[l] + down::STRIP - 1) / down::STRIP;
-    // band height: enough warps for ~4 waves of 16 resident warps per SM, 8..128 rows (even)
+    // band height: enough warps for ~2 waves of 16 resident warps per SM, 8..128 rows (even);
+    // BLADE_DOWN_WAVES overrides the wave count (tuning experiments, profiles/r01_f3_*.txt)
+    static const int waves = [] {
+      const char* e = getenv("BLADE_DOWN_WAVES");
+      return e ? std::max(1, atoi(e)) : 2;
+    }();
     const long long col_tasks = (long long)N * da.n_strips;
-    const long long want_bands = std::max<long long>(1, (4LL * 16 * h->num_sms + col_tasks - 1) / col_tasks);
+    const long long want_bands = std::max<long long>(1, ((long long)waves * 16 * h->num_sms + col_tasks - 1) / col_tasks);
     int RB = (int)std::min<long long>(128, std::max<long long>(8, (span + want_bands - 1) / want_bands));
     RB = (RB + 1) & ~1;
     da.RB = RB;
@@ -804,6 +814,15 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     return fail(BLADE_ECUDA, "kernel setup failed: %s (occupancy %d)", cudaGetErrorString(ce), occ);
   }
   h->stage_ctas_per_sm = occ;
+  ce = cudaEventCreateWithFlags(&h->pipe_fork, cudaEventDisableTiming);
+  for (int i = 0; i < blade_ms::kMaxStreams && ce == cudaSuccess; ++i) {
+    ce = cudaStreamCreateWithFlags(&h->pipe[i], cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->pipe_join[i], cudaEventDisableTiming);
+  }
+  if (ce != cudaSuccess) {
+    blade_ms_destroy(h);
+    return fail(BLADE_ECUDA, "stream setup failed: %s", cudaGetErrorString(ce));
+  }
   *out = h;
   return BLADE_OK;
 }
@@ -845,6 +864,11 @@ blade_status blade_ms_destroy(blade_ms_t h) {
     cudaEventDestroy(r.e1);
   }
   for (auto e : h->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < blade_ms::kMaxStreams; ++i) {
+    if (h->pipe[i]) cudaStreamDestroy(h->pipe[i]);
+    if (h->pipe_join[i]) cudaEventDestroy(h->pipe_join[i]);
+  }
+  if (h->pipe_fork) cudaEventDestroy(h->pipe_fork);
   cudaFree(h->d_bank);
   cudaFree(h->d_bank_tma);
   delete h;
@@ -928,6 +952,72 @@ blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t
   LevelView inv = make_view(const_cast<float*>(in), H, W, Range{0, H});
   LevelView outv = make_view(out, H, W, Range{0, H});
   return enqueue(h, p, inv, outv, (char*)ws, (cudaStream_t)stream, true, nullptr, nullptr);
+}
+
+static size_t pipe_slice_bytes(const blade_ms* h, int chunk, int H, int W) {
+  Plan p;
+  plan_rows(h, chunk, H, W, 0, H, p);
+  return align256(p.ws_bytes);
+}
+
+blade_status blade_ms_pipeline_workspace_size(blade_ms_t h, int32_t chunk, int32_t n_streams, int32_t H, int32_t W,
+                                              size_t* bytes) {
+  if (!h || !bytes) return fail(BLADE_EINVAL, "NULL argument");
+  blade_status s = check_dims(chunk, H, W);
+  if (s != BLADE_OK) return s;
+  if (chunk < 1) return fail(BLADE_EINVAL, "chunk must be >= 1");
+  if (n_streams < 1 || n_streams > blade_ms::kMaxStreams)
+    return fail(BLADE_EINVAL, "n_streams must be in 1..%d", blade_ms::kMaxStreams);
+  *bytes = (size_t)n_streams * pipe_slice_bytes(h, chunk, H, W);
+  return BLADE_OK;
+}
+
+// NEXT f3: chunk i of `chunk` frames -> internal stream i % n_streams, own
+// workspace slice; fork from / join into the caller's stream with events.
+blade_status blade_ms_denoise_pipelined(blade_ms_t h, const float* in, float* out, int32_t N, int32_t H, int32_t W,
+                                        int32_t chunk, int32_t n_streams, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  if (chunk < 1 || chunk > 65535) return fail(BLADE_EINVAL, "chunk must be in 1..65535");
+  if (n_streams < 1 || n_streams > blade_ms::kMaxStreams)
+    return fail(BLADE_EINVAL, "n_streams must be in 1..%d", blade_ms::kMaxStreams);
+  if (N == 0) return BLADE_OK;
+  const size_t slice = pipe_slice_bytes(h, chunk, H, W);
+  Plan pneed;
+  pneed.ws_bytes = (size_t)n_streams * slice;
+  if ((s = common_checks(h, in, N, ws, ws_bytes, pneed)) != BLADE_OK) return s;
+  if (!out) return fail(BLADE_EINVAL, "out is NULL");
+  if ((s = check_dev_ptr(h, out, "out")) != BLADE_OK) return s;
+  const size_t img = sizeof(float) * (size_t)N * 3 * H * W;
+  if (ranges_overlap(in, img, out, img)) return fail(BLADE_EINVAL, "out overlaps in");
+  if (ranges_overlap(ws, pneed.ws_bytes, out, img) || ranges_overlap(ws, pneed.ws_bytes, in, img))
+    return fail(BLADE_EINVAL, "workspace overlaps in/out");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nchunks = (N + chunk - 1) / chunk;
+  const int ns = std::min(n_streams, nchunks);
+  cudaError_t ce = cudaEventRecord(h->pipe_fork, st);
+  for (int i = 0; i < ns && ce == cudaSuccess; ++i) ce = cudaStreamWaitEvent(h->pipe[i], h->pipe_fork, 0);
+  if (ce != cudaSuccess) return fail(BLADE_ECUDA, "fork: %s", cudaGetErrorString(ce));
+  blade_status rs = BLADE_OK;
+  const size_t fr = (size_t)3 * H * W;
+  for (int i = 0; i < nchunks && rs == BLADE_OK; ++i) {
+    const int f0 = i * chunk, nf = std::min(chunk, N - f0);
+    Plan p;
+    plan_rows(h, nf, H, W, 0, H, p);
+    LevelView inv = make_view(const_cast<float*>(in) + (size_t)f0 * fr, H, W, Range{0, H});
+    LevelView outv = make_view(out + (size_t)f0 * fr, H, W, Range{0, H});
+    rs = enqueue(h, p, inv, outv, (char*)ws + (size_t)(i % ns) * slice, h->pipe[i % ns], true, nullptr, nullptr);
+  }
+  // join (also after a failed enqueue, so the caller's stream never runs ahead of queued work)
+  for (int i = 0; i < ns; ++i) {
+    cudaError_t e = cudaEventRecord(h->pipe_join[i], h->pipe[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, h->pipe_join[i], 0);
+    if (e != cudaSuccess && rs == BLADE_OK) rs = fail(BLADE_ECUDA, "join: %s", cudaGetErrorString(e));
+  }
+  return rs;
 }
 
 blade_status blade_ms_selector(blade_ms_t h, const float* in, int32_t N, int32_t H, int32_t W, void* const* maps,

@@ -40,12 +40,14 @@ def _cfg_like(name, H, W, N=1, **over):
     return cfg
 
 
-def _full_parity(cfg, x_np, taps=None, label=""):
-    """Run GPU denoise + selector on x_np [N,3,H,W]; compare with the oracle frame by frame."""
+def _full_parity(cfg, x_np, taps=None, label="", pipelined=None):
+    """Run GPU denoise + selector on x_np [N,3,H,W]; compare with the oracle frame by frame.
+    pipelined=(chunk, n_streams): the frame-chunked schedule (NEXT f3) instead of denoise()."""
     taps = cfg.taps() if taps is None else taps
     h = _handle(cfg, taps)
     x = torch.from_numpy(x_np).cuda()
-    out = h.denoise(x)
+    out = h.denoise(x) if pipelined is None else h.denoise_pipelined(x, chunk=pipelined[0],
+                                                                      n_streams=pipelined[1])
     maps = h.selector(x)
     lv = h.pyramid(x)
     torch.cuda.synchronize()
@@ -166,6 +168,60 @@ def test_batch_equals_per_frame_bit_exact():
     for n in range(3):
         one = h.denoise(x[n:n + 1].contiguous())
         assert torch.equal(one[0], full[n])
+
+
+# ------------------------------------------------------------------------- NEXT f3: chunked schedule
+
+@pytest.mark.parametrize("name,H,W,N,chunk,streams", [("c3", 256, 384, 7, 2, 2), ("c3", 120, 200, 5, 1, 4),
+                                                      ("c1", 203, 333, 3, 2, 3), ("c4", 130, 190, 2, 1, 2),
+                                                      ("c0", 64, 64, 5, 3, 1), ("c2", 97, 131, 4, 8, 2)])
+def test_pipelined_equals_denoise_bit_exact(name, H, W, N, chunk, streams):
+    """blade_ms_denoise_pipelined: chunks of frames on internal streams give the batched output
+    bit-exactly (ragged last chunk, more streams than chunks, chunk > N)."""
+    cfg = _cfg_like(name, H, W, N)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    ref = h.denoise(x)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        out = h.denoise_pipelined(x, chunk=chunk, n_streams=streams, stream=s)
+    s.synchronize()
+    assert torch.equal(out, ref)
+
+
+def test_pipelined_oracle_parity_c3_frames():
+    cfg = bs.load_config("c3")
+    _full_parity(cfg, cfg.batch(N=3), label="c3 pipelined", pipelined=(1, 2))
+
+
+def test_pipelined_graph_capture_and_errors():
+    """The fork / join are event waits: the schedule captures into a CUDA graph and replays
+    bit-exactly; bad chunk / stream counts and short workspaces are rejected."""
+    from paper_1802_06130_b200.blade_ms import BladeError
+    cfg = _cfg_like("c3", 96, 160, 6)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    ref = h.denoise(x)
+    out = torch.empty_like(x)
+    ws = torch.empty(h.pipeline_workspace_size(2, 3, 96, 160), dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        h.denoise_pipelined(x, out, chunk=2, n_streams=3, workspace=ws, stream=s)  # warm-up
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    out.zero_()
+    with torch.cuda.graph(g, stream=s):
+        h.denoise_pipelined(x, out, chunk=2, n_streams=3, workspace=ws, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    for kw, code in [(dict(chunk=0), 1), (dict(n_streams=5), 1), (dict(n_streams=0), 1)]:
+        with pytest.raises(BladeError) as ei:
+            h.denoise_pipelined(x, out, workspace=ws, **kw)
+        assert ei.value.status == code
+    with pytest.raises(BladeError) as ei:
+        h.denoise_pipelined(x, out, chunk=2, n_streams=3, workspace=ws[:ws.numel() // 2])
+    assert ei.value.status == 3
 
 
 @pytest.mark.parametrize("name,H,W,bands", [("c4", 700, 300, 4), ("c2", 333, 260, 3),
