@@ -373,10 +373,11 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
       const bool odd_r = (i & 1) == 0;  // Yb even => r = Yb - 3 + i is odd for even i
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        const double z0 = (double)hn[c][0] + (double)ln[c][0];
-        const double z1 = (double)hn[c][1] + (double)ln[c][1];
-        const double zL1 = (double)nL[c] + (double)nlL[c];
-        const double zR2 = (double)nR[c] + (double)nlR[c];
+        // level 0 has no lo part: skip the (useless, issue-slot costing) fp64 adds of zero
+        const double z0 = HILO ? (double)hn[c][0] + (double)ln[c][0] : (double)hn[c][0];
+        const double z1 = HILO ? (double)hn[c][1] + (double)ln[c][1] : (double)hn[c][1];
+        const double zL1 = HILO ? (double)nL[c] + (double)nlL[c] : (double)nL[c];
+        const double zR2 = HILO ? (double)nR[c] + (double)nlR[c] : (double)nR[c];
         const double zL2 = shfl_up_d(z0, 1);   // x-2
         const double zL3 = shfl_up_d(z1, 2);   // x-3
         const double zR3 = shfl_dn_d(z1, 1);   // x+3
