@@ -40,9 +40,10 @@ def _cfg_like(name, H, W, N=1, **over):
     return cfg
 
 
-def _full_parity(cfg, x_np, taps=None, label="", pipelined=None):
+def _full_parity(cfg, x_np, taps=None, label="", pipelined=None, frames=None):
     """Run GPU denoise + selector on x_np [N,3,H,W]; compare with the oracle frame by frame.
-    pipelined=(chunk, n_streams): the frame-chunked schedule (NEXT f3) instead of denoise()."""
+    pipelined=(chunk, n_streams): the frame-chunked schedule (NEXT f3) instead of denoise().
+    frames: the frames checked against the oracle (default all; the GPU runs the whole batch)."""
     taps = cfg.taps() if taps is None else taps
     h = _handle(cfg, taps)
     x = torch.from_numpy(x_np).cuda()
@@ -51,9 +52,12 @@ def _full_parity(cfg, x_np, taps=None, label="", pipelined=None):
     maps = h.selector(x)
     lv = h.pyramid(x)
     torch.cuda.synchronize()
-    out = out.cpu().numpy()
-    maps = [m.cpu().numpy() for m in maps]
-    lv = [t.cpu().numpy() for t in lv]
+    sel = list(range(x_np.shape[0])) if frames is None else list(frames)
+    pick = lambda t: np.stack([t[i].cpu().numpy() for i in sel])  # noqa: E731 (views: uint16 too)
+    out = pick(out)
+    maps = [pick(m) for m in maps]
+    lv = [pick(t) for t in lv]
+    x_np = x_np[sel]
     ts, tc = cfg.thresholds()
     stats_all = []
     worst = 0.0
@@ -93,6 +97,15 @@ def test_c3_frames_batched():
     """c3 recipe (1080p, 5x5 pairs, L=3) on 2 full frames batched in one call."""
     cfg = bs.load_config("c3")
     _full_parity(cfg, cfg.batch(N=2), label="c3")
+
+
+@pytest.mark.parametrize("name,frames", [("c3", (0, 37, 63)), ("c5", (0, 7))])
+def test_bench_launch_configuration_sampled_frames(name, frames):
+    """The whole batch bench.py times (c3: 64 frames of 1080p in one launch; c5: 8 frames),
+    the same launch configuration (band heights and grids depend on N), with sampled frames
+    checked against the oracle one by one."""
+    cfg = bs.load_config(name)
+    _full_parity(cfg, cfg.batch(), label=f"{name} bench batch", frames=frames)
 
 
 def test_c2_full_size():
