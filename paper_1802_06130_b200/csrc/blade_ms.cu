@@ -341,6 +341,41 @@ bool sync_debug() {
       return fail(BLADE_ECUDA, "%s (level %d): %s", name, l, cudaGetErrorString(e__));           \
   } while (0)
 
+// Kernel launch; with `pdl` the launch allows programmatic stream serialisation (PDL): the grid
+// may be scheduled while the previous kernel in the stream drains, and its kernels call pdl_wait()
+// before reading that kernel's outputs (kernels.cuh). BLADE_PDL=0 turns it off (A/B timing).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BLADE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                   Args&&... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, fn, std::forward<Args>(args)...);
+}
+#define LAUNCH(name, expr)                                                                       \
+  do {                                                                                           \
+    cudaError_t e0__ = (expr);                                                                   \
+    if (e0__ != cudaSuccess) {                                                                   \
+      cudaGetLastError();                                                                        \
+      return fail(BLADE_ECUDA, "%s (level %d): launch: %s", name, l, cudaGetErrorString(e0__)); \
+    }                                                                                            \
+    LAUNCH_CHECK(name);                                                                          \
+  } while (0)
+
 // Enqueue the cascade for plan p. in_view: level-0 input (fp32, rows >= p.z[0]); out_view: final
 // output rows p.u[0]. levels_out (diagnostic) receives z^l (fp32) for l >= 1; maps_out the maps.
 blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view, char* ws,
@@ -418,11 +453,9 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     const bool wide = h->K > 256;
     auto fn = down_kernel(hilo, dec, fast, wide);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
-    fn<<<grid, 32 * down::WARPS, down_smem(hilo), st>>>(da, h->down[l]);
-    LAUNCH_CHECK("k_down");
+    LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
     auto fx = fixup_kernel(hilo, fast, wide);
-    fx<<<4 * h->num_sms, 128, 0, st>>>(da, h->down[l]);
-    LAUNCH_CHECK("k_down_fixup");
+    LAUNCH("k_down_fixup", launch(fx, 4 * h->num_sms, 128, 0, st, true, da, h->down[l]));
   }
   if (!run_stages) return BLADE_OK;
 
@@ -496,24 +529,23 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
         const int per_type = std::max(1, std::min(h->num_sms / types, (a.n_tiles + 1) / 2));
         a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
         if (tv.ch3) a.clamp = 0;  // clamped after the colour conversion
-        tv.fn<<<types * per_type, dim3(32, 8), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+        LAUNCH("k_stage_ph", launch(tv.fn, types * per_type, dim3(32, 8), h->tma_smem, st, true, tmz, tmu, tmm, a));
       } else if (tv.ch3) {  // CTA b serves channel b % 3
         const int per_ch = std::max(1, std::min(h->num_sms / 3, (a.n_tiles + tv.groups - 1) / tv.groups));
         a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
         a.clamp = 0;  // clamped after the colour conversion
-        tv.fn<<<3 * per_ch, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+        LAUNCH("k_stage_tma", launch(tv.fn, 3 * per_ch, dim3(32, 8 * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
       } else {
         const int grid = std::min(h->num_sms, (a.n_tiles + tv.groups - 1) / tv.groups);
-        tv.fn<<<grid, dim3(32, 8 * tv.groups), h->tma_smem, st>>>(tmz, tmu, tmm, a);
+        LAUNCH("k_stage_tma", launch(tv.fn, grid, dim3(32, 8 * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
       }
-      LAUNCH_CHECK("k_stage_tma");
       if (tv.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
         const long long per_frame = (long long)r.n() * p.W[0];
         const long long total = (long long)N * per_frame;
         const unsigned g2 = (unsigned)std::min<long long>((total + 255) / 256, 8LL * h->num_sms);
-        k_ycc_to_rgb<><<<g2, 256, 0, st>>>(outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane,
-                                           outv.frame, per_frame, N, h->cfg.clamp_output);
-        LAUNCH_CHECK("k_ycc_to_rgb");
+        LAUNCH("k_ycc_to_rgb", launch(k_ycc_to_rgb<>, g2, 256, 0, st, true,
+                                      outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane, outv.frame,
+                                      per_frame, N, h->cfg.clamp_output));
       }
       continue;
     }
@@ -543,15 +575,14 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     grid = std::max<long long>(set, grid / set * set);
     a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
     if (h->stage.ch3) a.clamp = 0;  // clamped after the colour conversion
-    h->stage.fn<<<(unsigned)grid, dim3(32, h->stage.by), h->stage_smem, st>>>(a);
-    LAUNCH_CHECK("k_stage");
+    LAUNCH("k_stage", launch(h->stage.fn, (unsigned)grid, dim3(32, h->stage.by), h->stage_smem, st, true, a));
     if (h->stage.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
       const long long per_frame = (long long)r.n() * p.W[0];
       const long long total = (long long)N * per_frame;
       const unsigned g2 = (unsigned)std::min<long long>((total + 255) / 256, 8LL * h->num_sms);
-      k_ycc_to_rgb<><<<g2, 256, 0, st>>>(outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane, outv.frame,
-                                       per_frame, N, h->cfg.clamp_output);
-      LAUNCH_CHECK("k_ycc_to_rgb");
+      LAUNCH("k_ycc_to_rgb", launch(k_ycc_to_rgb<>, g2, 256, 0, st, true,
+                                    outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane, outv.frame,
+                                    per_frame, N, h->cfg.clamp_output));
     }
   }
   return BLADE_OK;

@@ -258,7 +258,9 @@ __global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, 
   extern __shared__ __align__(16) float dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x * WARPS + warp;
+  pdl_trigger();
   if (task >= a.n_tasks) return;
+  pdl_wait();
   float* ring = dsm + (size_t)warp * RING * NP * 64 + 2 * lane;  // this lane's 2 columns
 
   const int strip = task % a.n_strips;
@@ -517,6 +519,8 @@ __global__ void __launch_bounds__(128) k_down_fixup(const DownArgs a, const Down
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;
   // one warp per pixel: lane t < 25 evaluates the gradient products at window offset
   // (t / 5 - 2, t % 5 - 2) in fp64, the weighted products are summed over the warp (fp64)
+  pdl_trigger();
+  pdl_wait();
   const unsigned int cnt = *a.fb_count;
   const bool all = cnt > a.fb_cap;
   const unsigned long long per_frame = (unsigned long long)a.s_rn * a.W;

@@ -254,14 +254,15 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  if (tid == 0 && t < a.n_tiles) issue(t);
-  {
+  pdl_trigger();
+  {  // the bank (constant data) before waiting on the previous grid
     const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)(chn * 4 + p) * a.PS);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     for (int i = ctid; i < (bank_floats >> 2); i += 2 * SS::threads) s4[i] = __ldg(g4 + i);
   }
+  pdl_wait();
   __syncthreads();
+  if (tid == 0 && t < a.n_tiles) issue(t);
 
   for (int it = 0; t < a.n_tiles; ++it, t += workers) {
     int n, X0, Y0;

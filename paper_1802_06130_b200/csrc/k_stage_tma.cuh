@@ -233,15 +233,16 @@ __global__ void __launch_bounds__(256 * G, 1)
     mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  if (tid == 0 && t < a.n_tiles) issue(t, g);
-  // ---- the bank -> shared memory, once
+  pdl_trigger();
+  // ---- the bank -> shared memory, once (constant data: before waiting on the previous grid)
   if (!WIDE) {
     const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)chn * bank_floats);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     for (int i = ctid; i < (bank_floats >> 2); i += SS::threads * G) s4[i] = __ldg(g4 + i);
   }
+  pdl_wait();
   __syncthreads();
+  if (tid == 0 && t < a.n_tiles) issue(t, g);
 
   for (int it = 0; t < a.n_tiles; ++it, t += tstride) {
     const int b = G == 2 ? g : (it & 1);

@@ -27,6 +27,14 @@ struct LevelView {
   long long frame;  // floats per frame of the buffer (3 * plane)
 };
 
+// Programmatic dependent launch (sm_90+): the host launches every kernel of a cascade after the
+// first with programmatic stream serialisation, so its CTAs can be scheduled (and do work that
+// does not read the previous kernel's output, e.g. loading the bank) while the previous grid
+// drains. pdl_wait() blocks until the previous grid has completed and its writes are visible;
+// pdl_trigger() lets the next grid launch. Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // [R2] half-sample symmetric fold, periodic with period 2n.
 __device__ __forceinline__ int fold_idx(int i, int n) {
   if (i >= 0 && i < n) return i;
@@ -123,6 +131,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
   const int group = CH3 ? rest / 3 : rest;
   const int ngroups = (int)gridDim.x / (RS * (CH3 ? 3 : 1));
   const int tid = threadIdx.y * SS::BX + threadIdx.x;
+  pdl_trigger();
 
   // ---- filterbank -> shared memory, once per CTA (WIDE: read in place from global memory)
   const int ph0 = (a.n_phases == 4 && RS == 2) ? 2 * par : 0;
@@ -135,6 +144,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
     for (int i = tid; i < n4; i += SS::threads) s4[i] = __ldg(g4 + i);
     for (int i = (n4 << 2) + tid; i < bank_floats; i += SS::threads) sbank[i] = __ldg(a.bank + boff + i);
   }
+  pdl_wait();  // the bank is constant; everything below reads the previous kernels' outputs
 
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int y_base = (a.out_r0 & ~1);  // tiles start on an even global row
@@ -300,6 +310,8 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
 // to fp32 rounding; R25), with the optional final clamp.
 template <int = 0>
 __global__ void k_ycc_to_rgb(float* p, long long plane, long long frame, long long per_frame, int N, int clamp) {
+  pdl_trigger();
+  pdl_wait();
   const long long total = (long long)N * per_frame;
   const float kO = 128.0f / 255.0f;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
