@@ -153,6 +153,7 @@ struct blade_ms {
   float* d_bank_tma = nullptr;  // [stage][phase][PS_tma], tma_tap_off layout (k_stage_tma)
   size_t bank_bytes = 0;
   std::vector<DownParams> down;  // per stage (selector level)
+  int down_slots[2] = {1, 1};    // resident k_down warps on the device (level 0 / hi-lo levels)
   // generic stage kernel
   StageVariant stage{};
   size_t stage_smem = 0;
@@ -430,15 +431,23 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.base = R.lo & ~1;
     const int span = R.hi - da.base;
     da.n_strips = (p.W[l] + down::STRIP - 1) / down::STRIP;
-    // band height: enough warps for ~2 waves of 16 resident warps per SM, 8..128 rows (even);
-    // BLADE_DOWN_WAVES overrides the wave count (tuning experiments, profiles/r01_f3_*.txt)
-    static const int waves = [] {
-      const char* e = getenv("BLADE_DOWN_WAVES");
-      return e ? std::max(1, atoi(e)) : 2;
-    }();
+    // band height RB (even, 4..128): a task is RB + 6 input rows of one 64-column strip; pick
+    // the RB that minimises (RB + 6) x waves, waves = tasks / resident warp slots, counted in whole
+    // waves while the grid is short (< 2 waves: small images want thin bands, their halo rows are
+    // cheaper than idle SMs) and fractionally beyond (large batches want tall bands)
     const long long col_tasks = (long long)N * da.n_strips;
-    const long long want_bands = std::max<long long>(1, ((long long)waves * 16 * h->num_sms + col_tasks - 1) / col_tasks);
-    int RB = (int)std::min<long long>(128, std::max<long long>(8, (span + want_bands - 1) / want_bands));
+    const double slots = (double)h->down_slots[l > 0 ? 1 : 0];
+    int RB = 128;
+    double best = 0.0;
+    for (int rb = 128; rb >= 4; rb -= 2) {
+      const double tasks = (double)col_tasks * (double)((span + rb - 1) / rb);
+      const double w = tasks / slots;
+      const double cost = (rb + 6) * (w < 2.0 ? std::ceil(w) : w);
+      if (rb == 128 || cost < best) {
+        best = cost;
+        RB = rb;
+      }
+    }
     RB = (RB + 1) & ~1;
     da.RB = RB;
     da.n_bands = (span + RB - 1) / RB;
@@ -526,17 +535,19 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       a.clamp = clamp;
       if (tv.phase_split) {  // 4 phase-CTAs (x 3 channels) per tile group, 2 workers per CTA
         const int types = tv.ch3 ? 12 : 4;
-        const int per_type = std::max(1, std::min(h->num_sms / types, (a.n_tiles + 1) / 2));
+        // one tile per worker group first: small levels spread over as many SMs as they have
+        // tiles (a CTA's two groups share its SM's shared-memory bandwidth)
+        const int per_type = std::max(1, std::min(h->num_sms / types, a.n_tiles));
         a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
         if (tv.ch3) a.clamp = 0;  // clamped after the colour conversion
         LAUNCH("k_stage_ph", launch(tv.fn, types * per_type, dim3(32, 8), h->tma_smem, st, true, tmz, tmu, tmm, a));
       } else if (tv.ch3) {  // CTA b serves channel b % 3
-        const int per_ch = std::max(1, std::min(h->num_sms / 3, (a.n_tiles + tv.groups - 1) / tv.groups));
+        const int per_ch = std::max(1, std::min(h->num_sms / 3, a.n_tiles));
         a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
         a.clamp = 0;  // clamped after the colour conversion
         LAUNCH("k_stage_tma", launch(tv.fn, 3 * per_ch, dim3(32, 8 * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
       } else {
-        const int grid = std::min(h->num_sms, (a.n_tiles + tv.groups - 1) / tv.groups);
+        const int grid = std::min(h->num_sms, a.n_tiles);  // small levels: one tile per SM
         LAUNCH("k_stage_tma", launch(tv.fn, grid, dim3(32, 8 * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
       }
       if (tv.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
@@ -723,7 +734,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     if (v.ch3 != ch3 || v.wide != wide || v.nf != c.fine_size || v.nc != cnc) continue;
     const size_t tps = (size_t)K * v.S;  // phase stride of the TMA tap layout (multiple of 4)
     const size_t bank = wide ? 0 : ((size_t)c.n_phases * tps * 4 + 127) & ~size_t(127);
-    const size_t smem = 2 * (size_t)v.stage_bytes + bank + 16;
+    const size_t smem = 2 * (size_t)v.stage_bytes + bank + 32;  // + 3 mbarriers
     if (smem <= (size_t)max_smem && get_encode()) {
       h->has_tma = true;
       h->tma = v;
@@ -736,7 +747,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     for (const auto& v : ph_variants()) {
       if (v.nf != c.fine_size || v.nc != cnc || v.ch3 != ch3 || v.wide != wide) continue;
       const size_t tps = (size_t)K * v.S;
-      const size_t smem = 2 * (size_t)v.stage_bytes + ((tps * 4 + 127) & ~size_t(127)) + 16;
+      const size_t smem = 2 * (size_t)v.stage_bytes + ((tps * 4 + 127) & ~size_t(127)) + 32;
       if (smem <= (size_t)max_smem && get_encode()) {
         h->has_tma = true;
         h->tma = v;
@@ -834,6 +845,12 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
         for (int sm = 0; sm < 3 && ce == cudaSuccess; ++sm)
           ce = cudaFuncSetAttribute(down_kernel(hl, dc, sm == 1, sm == 2), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)down_smem(hl));
+  }
+  for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl) {
+    int oc = 0;
+    ce = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, down_kernel(hl, true, h->n_o == 16 && h->n_s == 3 && h->n_c == 3, wide),
+                                                       32 * down::WARPS, down_smem(hl));
+    h->down_slots[hl] = std::max(1, oc) * down::WARPS * nsm;
   }
   int occ = 0;
   if (ce == cudaSuccess)

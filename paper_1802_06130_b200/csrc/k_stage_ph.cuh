@@ -248,21 +248,23 @@ __global__ void __launch_bounds__(256, 1)
     tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[g]);
   };
 
-  int t = ci * 2 + g;
+  // large levels: a CTA's two groups take adjacent tiles (shared halo rows in L2); small levels
+  // (fewer tiles than groups): group 1 starts after every CTA's group 0, one tile per SM
+  int t = a.n_tiles >= 2 * cpp ? ci * 2 + g : ci + g * cpp;
+  pdl_trigger();
   if (ctid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&mbar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_trigger();
-  {  // the bank (constant data) before waiting on the previous grid
-    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)(chn * 4 + p) * a.PS);
-    float4* s4 = reinterpret_cast<float4*>(sbank);
-    for (int i = ctid; i < (bank_floats >> 2); i += 2 * SS::threads) s4[i] = __ldg(g4 + i);
+    // the bank (constant data): one bulk copy, issued before waiting on the previous grid
+    mbar_expect_tx(&mbar[2], (uint32_t)bank_floats * 4u);
+    bulk_g2s(sbank, a.bank + (long long)(chn * 4 + p) * a.PS, (uint32_t)bank_floats * 4u, &mbar[2]);
   }
   pdl_wait();
   __syncthreads();
   if (tid == 0 && t < a.n_tiles) issue(t);
+  mbar_wait(&mbar[2], 0);
 
   for (int it = 0; t < a.n_tiles; ++it, t += workers) {
     int n, X0, Y0;

@@ -51,6 +51,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+// One bulk (non-tensor) copy global -> shared of `bytes` (multiple of 16, both ends 16-B aligned)
+// by the TMA engine, completing on an mbarrier: the whole bank in one instruction.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -228,21 +236,23 @@ __global__ void __launch_bounds__(256 * G, 1)
   const int ctid = threadIdx.y * SS::BX + threadIdx.x;
   int t = cta + g * nctas;
   const int tstride = G * nctas;
+  pdl_trigger();
   if (ctid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&mbar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  pdl_trigger();
-  // ---- the bank -> shared memory, once (constant data: before waiting on the previous grid)
-  if (!WIDE) {
-    const float4* g4 = reinterpret_cast<const float4*>(a.bank + (long long)chn * bank_floats);
-    float4* s4 = reinterpret_cast<float4*>(sbank);
-    for (int i = ctid; i < (bank_floats >> 2); i += SS::threads * G) s4[i] = __ldg(g4 + i);
+    // ---- the bank -> shared memory, once, by one bulk copy (constant data: issued before
+    //      waiting on the previous grid)
+    if (!WIDE) {
+      mbar_expect_tx(&mbar[2], (uint32_t)bank_floats * 4u);
+      bulk_g2s(sbank, a.bank + (long long)chn * bank_floats, (uint32_t)bank_floats * 4u, &mbar[2]);
+    }
   }
   pdl_wait();
   __syncthreads();
   if (tid == 0 && t < a.n_tiles) issue(t, g);
+  if (!WIDE) mbar_wait(&mbar[2], 0);
 
   for (int it = 0; t < a.n_tiles; ++it, t += tstride) {
     const int b = G == 2 ? g : (it & 1);
