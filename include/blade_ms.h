@@ -28,8 +28,11 @@
  *   - Errors: every argument error is detected BEFORE any launch (no partial writes) and
  *     returned as a blade_status; blade_ms_last_error() returns a thread-local message.
  *     Asynchronous device faults surface at the caller's next synchronisation.
- *   - Thread safety: a handle is immutable after create; concurrent calls with distinct
- *     workspaces/outputs (on any streams) are safe. destroy must not race pending work.
+ *   - Thread safety: a handle's bank and plan are immutable after create; concurrent calls
+ *     with distinct workspaces/outputs (on any streams) are safe, except while profiling is on
+ *     (blade_ms_set_profiling). blade_ms_denoise_pipelined's internal streams are shared by
+ *     the handle: concurrent pipelined calls stay correct but may serialise (and a caller's
+ *     join may also wait for another call's chunks). destroy must not race pending work.
  *   - Non-finite PIXEL values are not checked (it would cost a pass); outputs are then
  *     unspecified. Non-finite TAPS and thresholds are rejected at create.
  */
