@@ -161,6 +161,8 @@ struct blade_ms {
   // TMA stage kernel (if the shape has one and the bank fits)
   bool has_tma = false;
   TmaVariant tma{};
+  bool has_tma4 = false;  // the 4-rows-per-thread variant of the same shape (large levels)
+  TmaVariant tma4{};
   size_t tma_smem = 0;
   // profiling (blade_ms_set_profiling): event pairs around each launch
   struct ProfRec { int kind, level; cudaEvent_t e0, e1; };
@@ -342,6 +344,16 @@ bool sync_debug() {
       return fail(BLADE_ECUDA, "%s (level %d): %s", name, l, cudaGetErrorString(e__));           \
   } while (0)
 
+// BLADE_TMA_RY=2 / =4 forces the 2- / 4-row TMA stage variant on every level (A/B timing);
+// default 0 = by level size.
+int tma_ry() {
+  static const int v = [] {
+    const char* e = getenv("BLADE_TMA_RY");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 // Kernel launch; with `pdl` the launch allows programmatic stream serialisation (PDL): the grid
 // may be scheduled while the previous kernel in the stream drains, and its kernels call pdl_wait()
 // before reading that kernel's outputs (kernels.cuh). BLADE_PDL=0 turns it off (A/B timing).
@@ -503,7 +515,14 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       }
     }
     if (use_tma) {
-      const TmaVariant& tv = h->tma;
+      // large, wide levels (many tiles per SM, few border / partial tiles): 4 pixel rows per
+      // thread; otherwise 2 (measured: c3 level 0 2.56 -> 2.36 ms, but level 1 (7.5 tiles wide)
+      // 0.75 -> 0.80 ms and the latency-bound small levels slower with 8 warps per SM)
+      const int tiles_x = (p.W[l] + h->tma.tcols - 1) / h->tma.tcols;
+      const long long tiles_est = (long long)N * tiles_x * ((r.hi - y_base + h->tma.trows - 1) / h->tma.trows);
+      const bool ry4 = h->has_tma4 && tma_ry() != 2 &&
+                       (tma_ry() == 4 || (tiles_x >= 12 && tiles_est >= 8LL * h->num_sms));
+      const TmaVariant& tv = ry4 ? h->tma4 : h->tma;
       StageTmaArgs a{};
       a.H = p.H[l];
       a.W = p.W[l];
@@ -545,10 +564,10 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
         const int per_ch = std::max(1, std::min(h->num_sms / 3, a.n_tiles));
         a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
         a.clamp = 0;  // clamped after the colour conversion
-        LAUNCH("k_stage_tma", launch(tv.fn, 3 * per_ch, dim3(32, 8 * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
+        LAUNCH("k_stage_tma", launch(tv.fn, 3 * per_ch, dim3(32, tv.by * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
       } else {
         const int grid = std::min(h->num_sms, a.n_tiles);  // small levels: one tile per SM
-        LAUNCH("k_stage_tma", launch(tv.fn, grid, dim3(32, 8 * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
+        LAUNCH("k_stage_tma", launch(tv.fn, grid, dim3(32, tv.by * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
       }
       if (tv.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
         const long long per_frame = (long long)r.n() * p.W[0];
@@ -732,6 +751,13 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->stage_smem = best_smem;
   for (const auto& v : tma_variants()) {
     if (v.ch3 != ch3 || v.wide != wide || v.nf != c.fine_size || v.nc != cnc) continue;
+    if (v.by == 4) {  // 4 pixel rows per thread: same tiles and smem as the 2-row variant
+      if (tma_ry() != 2) {
+        h->has_tma4 = true;
+        h->tma4 = v;
+      }
+      continue;
+    }
     const size_t tps = (size_t)K * v.S;  // phase stride of the TMA tap layout (multiple of 4)
     const size_t bank = wide ? 0 : ((size_t)c.n_phases * tps * 4 + 127) & ~size_t(127);
     const size_t smem = 2 * (size_t)v.stage_bytes + bank + 32;  // + 3 mbarriers
@@ -839,6 +865,8 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     ce = cudaFuncSetAttribute(h->stage.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->stage_smem);
   if (ce == cudaSuccess && h->has_tma)
     ce = cudaFuncSetAttribute(h->tma.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
+  if (ce == cudaSuccess && h->has_tma && h->has_tma4)
+    ce = cudaFuncSetAttribute(h->tma4.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
   if (ce == cudaSuccess) {
     for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl)
       for (int dc = 0; dc < 2 && ce == cudaSuccess; ++dc)

@@ -64,10 +64,11 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
   const bool coarse_border = CX < 0 || CX + SS::CCB > a.W1 || CY < 0 || CY + SS::CR > a.H1;
   if (fine_border || coarse_border) {
     if (fine_border) {
-      for (int i = tid; i < SS::FR * SS::FCB; i += SS::threads) {
-        const int r = i / SS::FCB, q = i - r * SS::FCB;
+      const OobBox ob = oob_box(SS::FR, SS::FCB, FY, FX, a.H, a.W);
+      for (int i = tid; i < ob.n; i += SS::threads) {
+        int r, q;
+        oob_cell(ob, i, r, q);
         const int gy = FY + r, gx = FX + q;
-        if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) continue;
         const int fy = fold_idx(gy, a.H), fx = fold_idx(gx, a.W);
         const int ry = fy - FY, rx = fx - FX;
         const bool in_tile = ry >= 0 && ry < SS::FR && rx >= 0 && rx < SS::FCB;
@@ -85,10 +86,11 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
       }
     }
     if (coarse_border) {
-      for (int i = tid; i < SS::CR * SS::CCB; i += SS::threads) {
-        const int r = i / SS::CCB, q = i - r * SS::CCB;
+      const OobBox ob = oob_box(SS::CR, SS::CCB, CY, CX, a.H1, a.W1);
+      for (int i = tid; i < ob.n; i += SS::threads) {
+        int r, q;
+        oob_cell(ob, i, r, q);
         const int gy = CY + r, gx = CX + q;
-        if (gy >= 0 && gy < a.H1 && gx >= 0 && gx < a.W1) continue;
         const int fy = fold_idx(gy, a.H1), fx = fold_idx(gx, a.W1);
         const int ry = fy - CY, rx = fx - CX;
         const bool in_tile = ry >= 0 && ry < SS::CR && rx >= 0 && rx < SS::CCB;

@@ -63,6 +63,45 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// The cells of a rows x cols staging box with image origin (gy0, gx0) that fall outside
+// [0, H) x [0, W): top rows, then the left / right columns of the middle rows, then bottom rows.
+// oob_count() sizes the enumeration, oob_cell() maps its index e to the box cell (r, q), so a
+// border fix-up touches only the out-of-image cells instead of testing the whole box.
+struct OobBox {
+  int cols, top, mid, left, right, n;
+};
+__device__ __forceinline__ OobBox oob_box(int rows, int cols, int gy0, int gx0, int H, int W) {
+  OobBox b;
+  b.cols = cols;
+  b.top = min(rows, max(0, -gy0));
+  const int bot = rows - max(b.top, min(rows, H - gy0));
+  b.mid = rows - b.top - bot;
+  b.left = min(cols, max(0, -gx0));
+  b.right = cols - max(b.left, min(cols, W - gx0));
+  b.n = (b.top + bot) * cols + b.mid * (b.left + b.right);
+  return b;
+}
+__device__ __forceinline__ void oob_cell(const OobBox& b, int e, int& r, int& q) {
+  const int nt = b.top * b.cols;
+  if (e < nt) {
+    r = e / b.cols;
+    q = e - r * b.cols;
+    return;
+  }
+  e -= nt;
+  const int lr = b.left + b.right;
+  if (e < b.mid * lr) {
+    const int rr = e / lr, k = e - rr * lr;
+    r = b.top + rr;
+    q = k < b.left ? k : b.cols - b.right + (k - b.left);
+    return;
+  }
+  e -= b.mid * lr;
+  const int rb = e / b.cols;
+  r = b.top + b.mid + rb;
+  q = e - rb * b.cols;
+}
+
 // Loads N consecutive floats from p into v[0..N). The address of p is congruent to A floats
 // modulo 4 (i.e. p - A is 16-B aligned when MAXV == 4, 8-B aligned when MAXV == 2); at each
 // position the widest naturally aligned LDS (up to MAXV floats) is used. Compile-time recursion.
@@ -127,9 +166,12 @@ __device__ __forceinline__ void load_tap_row(const float* tp, int dy, float* t) 
   }
 }
 
-template <int NF, int NC, bool WIDE = false>
+// RY: pixel rows per thread (2 or 4); a tile is always 16 x 128 outputs, so RY = 4 runs 4 warps
+// per group (one window row then feeds 4 pixel rows instead of 2: fewer shared-memory wavefronts
+// per pixel, 8 warps per SM).
+template <int NF, int NC, bool WIDE = false, int RY_ = 2>
 struct TmaShape {
-  static constexpr int RX = 4, RY = 2, BX = 32, BY = 8;
+  static constexpr int RX = 4, RY = RY_, BX = 32, BY = 16 / RY_;
   static constexpr int threads = BX * BY;
   static constexpr int RF = NF / 2, RC = NC / 2;
   static constexpr int TCOLS = BX * RX, TROWS = BY * RY;  // 128 x 16 outputs per tile
@@ -185,11 +227,11 @@ struct StageTmaArgs {
 // (the coarse patch only when it is the RGB z^{L-1}; else plane chn of the YCbCr u^{l+1} is read).
 // WIDE (NEXT f2, K > 256): uint16 bucket tiles and the bank read from global memory (the paper's
 // 16 x 16 x 16 layout is 4.8 MB per stage: L2-resident, not shared-memory resident).
-template <int NF, int NC, int G, bool CH3, bool WIDE = false>
-__global__ void __launch_bounds__(256 * G, 1)
+template <int NF, int NC, int G, bool CH3, bool WIDE = false, int RY = 2>
+__global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
     k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
-  using SS = TmaShape<NF, NC, WIDE>;
+  using SS = TmaShape<NF, NC, WIDE, RY>;
   constexpr int RF = SS::RF, RC = SS::RC;
   constexpr int PL = CH3 ? 1 : 3;
   const int chn = CH3 ? (int)(blockIdx.x % 3) : 0;
@@ -204,12 +246,12 @@ __global__ void __launch_bounds__(256 * G, 1)
                                                (WIDE ? 0 : ((bank_floats * 4 + 127) & ~127)));
   const float* bank = WIDE ? a.bank + (long long)chn * bank_floats : sbank;
 
-  const int g = G == 2 ? (int)(threadIdx.y >> 3) : 0;  // thread group
-  const int tid = (threadIdx.y & 7) * SS::BX + threadIdx.x;  // thread index within the group
-  const int tx = threadIdx.x, ty = threadIdx.y & 7;
+  const int g = G == 2 ? (int)(threadIdx.y / SS::BY) : 0;  // thread group
+  const int ty = (int)(threadIdx.y % SS::BY), tx = threadIdx.x;
+  const int tid = ty * SS::BX + tx;  // thread index within the group
   auto group_sync = [&]() {
     if constexpr (G == 2)
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(256) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(SS::threads) : "memory");
     else
       __syncthreads();
   };
@@ -275,10 +317,11 @@ __global__ void __launch_bounds__(256 * G, 1)
                                           Y0 / 2 - RC + SS::CR > a.H1);
     if (fine_border || coarse_border) {
       if (fine_border) {
-        for (int i = tid; i < SS::FR * SS::FCB; i += SS::threads) {
-          const int r = i / SS::FCB, q = i - r * SS::FCB;
+        const OobBox ob = oob_box(SS::FR, SS::FCB, Y0 - RF, FX, a.H, a.W);
+        for (int i = tid; i < ob.n; i += SS::threads) {
+          int r, q;
+          oob_cell(ob, i, r, q);
           const int gy = Y0 - RF + r, gx = FX + q;
-          if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) continue;
           const int fy = fold_idx(gy, a.H), fx = fold_idx(gx, a.W);
           const int ry = fy - (Y0 - RF), rx = fx - FX;
           const bool in_tile = ry >= 0 && ry < SS::FR && rx >= 0 && rx < SS::FCB;
@@ -298,10 +341,11 @@ __global__ void __launch_bounds__(256 * G, 1)
       if constexpr (NC > 0) {
         if (coarse_border) {
           const int CY0 = Y0 / 2 - RC, CX0 = CX;
-          for (int i = tid; i < SS::CR * SS::CCB; i += SS::threads) {
-            const int r = i / SS::CCB, q = i - r * SS::CCB;
+          const OobBox ob = oob_box(SS::CR, SS::CCB, CY0, CX0, a.H1, a.W1);
+          for (int i = tid; i < ob.n; i += SS::threads) {
+            int r, q;
+            oob_cell(ob, i, r, q);
             const int gy = CY0 + r, gx = CX0 + q;
-            if (gy >= 0 && gy < a.H1 && gx >= 0 && gx < a.W1) continue;
             const int fy = fold_idx(gy, a.H1), fx = fold_idx(gx, a.W1);
             const int ry = fy - CY0, rx = fx - CX0;
             const bool in_tile = ry >= 0 && ry < SS::CR && rx >= 0 && rx < SS::CCB;
@@ -336,73 +380,76 @@ __global__ void __launch_bounds__(256 * G, 1)
       group_sync();
     }
 
-    // ---- this thread's 2 x 4 block
+    // ---- this thread's RY x 4 block (rows y .. y+RY-1, y even; cols x .. x+3)
     const int x = X0 + SS::RX * tx;
-    const int y = Y0 + SS::RY * ty;
-    uint64_t mrow0, mrow1;
-    if constexpr (WIDE) {
-      mrow0 = *reinterpret_cast<const uint64_t*>(smap + 2 * ((2 * ty) * SS::TCOLS + 4 * tx));
-      mrow1 = *reinterpret_cast<const uint64_t*>(smap + 2 * ((2 * ty + 1) * SS::TCOLS + 4 * tx));
-    } else {
-      mrow0 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty) * SS::TCOLS + 4 * tx);
-      mrow1 = *reinterpret_cast<const uint32_t*>(smap + (2 * ty + 1) * SS::TCOLS + 4 * tx);
-    }
+    const int y = Y0 + RY * ty;
     constexpr int KB = WIDE ? 16 : 8;
     constexpr uint64_t KM = WIDE ? 0xffff : 0xff;
-    const float* tp[2][4];
+    int toff[RY][4];  // filter offsets in the bank: phase (2 (i & 1) + (j & 1)) x PS + bucket x S
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int k0 = (int)((mrow0 >> (KB * j)) & KM), k1 = (int)((mrow1 >> (KB * j)) & KM);
-      const int ph0 = a.n_phases == 4 ? (j & 1) : 0;
-      const int ph1 = a.n_phases == 4 ? 2 + (j & 1) : 0;
-      tp[0][j] = bank + ph0 * a.PS + k0 * SS::S;
-      tp[1][j] = bank + ph1 * a.PS + k1 * SS::S;
+    for (int i = 0; i < RY; ++i) {
+      uint64_t mrow;
+      if constexpr (WIDE)
+        mrow = *reinterpret_cast<const uint64_t*>(smap + 2 * ((RY * ty + i) * SS::TCOLS + 4 * tx));
+      else
+        mrow = *reinterpret_cast<const uint32_t*>(smap + (RY * ty + i) * SS::TCOLS + 4 * tx);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = (int)((mrow >> (KB * j)) & KM);
+        const int ph = a.n_phases == 4 ? 2 * (i & 1) + (j & 1) : 0;
+        toff[i][j] = ph * a.PS + k * SS::S;
+      }
     }
-    float acc[2][4][PL];
+    float acc[RY][4][PL];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < RY; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int c = 0; c < PL; ++c) acc[i][j][c] = 0.0f;
 
     if constexpr (NC > 0) {
-      // coarse rows local ty .. ty+NC-1 (both pixel rows share floor(y/2)); cols 2tx .. 2tx+NC
+      // coarse rows local ty RY/2 .. + NC + RY/2 - 1 (pixel row i sits on coarse row wr - i/2 of its
+      // window); cols 2tx .. 2tx+NC
 #pragma unroll
-      for (int wr = 0; wr < NC; ++wr) {
+      for (int wr = 0; wr < NC + RY / 2 - 1; ++wr) {
         float v[PL][SS::CWIN];
 #pragma unroll
         for (int c = 0; c < PL; ++c)
-          lds_run<(SS::CO & 1), SS::CWIN, 2>(scoarse_c + (c * SS::CR + ty + wr) * SS::CCB + 2 * tx + SS::CO, v[c]);
+          lds_run<(SS::CO & 1), SS::CWIN, 2>(
+              scoarse_c + (c * SS::CR + (RY / 2) * ty + wr) * SS::CCB + 2 * tx + SS::CO, v[c]);
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < RY; ++i) {
+          const int dy = wr - (i >> 1);
+          if (dy < 0 || dy >= NC) continue;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float t[NC > 0 ? NC : 1];
-            load_tap_row<NF, NC, 1, WIDE>(tp[i][j], wr, t);
+            load_tap_row<NF, NC, 1, WIDE>(bank + toff[i][j], dy, t);
 #pragma unroll
             for (int dx = 0; dx < NC; ++dx) {
 #pragma unroll
               for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(t[dx], v[c][(j >> 1) + dx], acc[i][j][c]);
             }
           }
+        }
       }
     }
-    // fine rows local 2ty .. 2ty+NF (NF+1 rows), cols 4tx .. 4tx+NF+2
+    // fine rows local RY ty .. RY ty + NF + RY - 2, cols 4tx .. 4tx+NF+2
 #pragma unroll
-    for (int wr = 0; wr < NF + 1; ++wr) {
+    for (int wr = 0; wr < NF + RY - 1; ++wr) {
       float v[PL][SS::FWIN];
 #pragma unroll
       for (int c = 0; c < PL; ++c)
-        lds_run<SS::FO, SS::FWIN>(sfine + (c * SS::FR + 2 * ty + wr) * SS::FCB + 4 * tx + SS::FO, v[c]);
+        lds_run<SS::FO, SS::FWIN>(sfine + (c * SS::FR + RY * ty + wr) * SS::FCB + 4 * tx + SS::FO, v[c]);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < RY; ++i) {
         const int dy = wr - i;
         if (dy < 0 || dy >= NF) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float t[NF];
-          load_tap_row<NF, NC, 0, WIDE>(tp[i][j], dy, t);
+          load_tap_row<NF, NC, 0, WIDE>(bank + toff[i][j], dy, t);
 #pragma unroll
           for (int dx = 0; dx < NF; ++dx) {
 #pragma unroll
@@ -412,9 +459,9 @@ __global__ void __launch_bounds__(256 * G, 1)
       }
     }
 
-    // ---- store (rows y, y+1; cols x .. x+3)
+    // ---- store (rows y .. y+RY-1; cols x .. x+3)
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < RY; ++i) {
       const int yy = y + i;
       if (yy < a.o_r0 || yy >= a.o_r0 + a.o_rn || x >= a.W) continue;
       float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.W + x;

@@ -6,7 +6,7 @@ namespace tables {
 template <int NF, int NC, bool CH3 = false>
 static TmaVariant make_ph() {
   using SS = PhShape<NF, NC>;
-  return TmaVariant{NF, NC, 2, &k_stage_ph<NF, NC, CH3>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+  return TmaVariant{NF, NC, 2, 4, &k_stage_ph<NF, NC, CH3>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
                     SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, true, CH3, false};
 }
 const std::vector<TmaVariant>& ph_variants() {

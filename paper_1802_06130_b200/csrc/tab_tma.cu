@@ -6,16 +6,20 @@
 #endif
 namespace blade {
 namespace tables {
-template <int NF, int NC, bool CH3 = false, bool WIDE = false, int G = BLADE_TMA_GROUPS>
+template <int NF, int NC, bool CH3 = false, bool WIDE = false, int RY = 2, int G = BLADE_TMA_GROUPS>
 static TmaVariant make_tma() {
-  using SS = TmaShape<NF, NC, WIDE>;
-  return TmaVariant{NF, NC, G, &k_stage_tma<NF, NC, G, CH3, WIDE>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
-                    SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3, WIDE};
+  using SS = TmaShape<NF, NC, WIDE, RY>;
+  return TmaVariant{NF, NC, G, SS::BY, &k_stage_tma<NF, NC, G, CH3, WIDE, RY>, SS::stage_bytes, SS::TROWS,
+                    SS::TCOLS, SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3, WIDE};
 }
 const std::vector<TmaVariant>& tma_variants() {
   static const std::vector<TmaVariant> v = {
       make_tma<3, 0>(), make_tma<5, 0>(), make_tma<7, 0>(), make_tma<9, 0>(),
       make_tma<3, 3>(), make_tma<5, 5>(), make_tma<5, 3>(),
+      // 4 pixel rows per thread (fewer window wavefronts per pixel, 8 warps per SM)
+      make_tma<3, 0, false, false, 4>(), make_tma<5, 0, false, false, 4>(), make_tma<7, 0, false, false, 4>(),
+      make_tma<9, 0, false, false, 4>(), make_tma<3, 3, false, false, 4>(), make_tma<5, 5, false, false, 4>(),
+      make_tma<5, 3, false, false, 4>(),
       // per-channel YCbCr banks (NEXT f1): CTAs specialised by channel
       make_tma<3, 0, true>(), make_tma<5, 0, true>(), make_tma<7, 0, true>(), make_tma<9, 0, true>(),
       make_tma<3, 3, true>(), make_tma<5, 5, true>(), make_tma<5, 3, true>(),

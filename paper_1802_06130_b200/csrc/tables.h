@@ -28,6 +28,7 @@ const std::vector<StageVariant>& stage_variants();
 using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
 struct TmaVariant {
   int nf, nc, groups;
+  int by;  // warps per group (16 / pixel rows per thread); k_stage_ph: 4
   TmaKernel fn;
   int stage_bytes, trows, tcols, fcb, fr, ccb, cr, rf, rc, S;
   bool phase_split;  // k_stage_ph: CTAs specialised by output phase, one phase's bank each

@@ -417,3 +417,23 @@ def test_c5_paper_bucket_layout_parity(H, W, N):
     out, stats, worst = _full_parity(cfg, cfg.batch(), label=f"c5@{H}x{W}")
     h = _handle(cfg)
     assert h.map_dtype == torch.uint16
+
+
+# ------------------------------------------------------------------------- forced kernel variants
+
+@pytest.mark.parametrize("env", [{"BLADE_TMA_RY": "4"}, {"BLADE_TMA_RY": "2"}, {"BLADE_PDL": "0"}])
+def test_forced_variants_subprocess(env):
+    """The library picks kernel variants by level size (4- vs 2-row TMA stage threads) and
+    launches with programmatic dependent launch; the knobs are read once per process, so the
+    ragged / exact parity cases are re-run in a child process with each choice forced."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    cmd = [sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_parity.py"), "-q", "-x",
+           "-p", "no:cacheprovider", "-k",
+           "(ragged_shapes or c1_full or delta_bank or c3_frames_batched) and not forced_variants"]
+    r = subprocess.run(cmd, cwd=root, env={**os.environ, **env}, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
