@@ -10,11 +10,13 @@
 // tiles a fix-up pass overwrites them with the folded sample (R2), taken from the tile
 // itself or, for tiny levels, from global memory.
 //
-// Each thread computes a 2 x 4 pixel block (rows y, y+1; columns x..x+3): all four 2x2 output
-// phases, so phase(i, j) = 2 i + (j & 1) is static and the two coarse centres floor(x/2),
-// floor(x/2)+1 are shared by column pairs. Per input row the thread loads its window segment once
-// (LDS.128 / LDS.64, conflict-free) and the 8 pixels' taps (LDS.32, per-pixel addresses); the
-// three colour channels share every tap load (R13). FP32 FMA on the CUDA cores.
+// Each thread computes an RY x 4 pixel block (RY = 2 or 4 rows from an even row y; columns
+// x..x+3): all four 2x2 output phases, so phase(i, j) = 2 (i & 1) + (j & 1) is static and the two
+// coarse centres floor(x/2), floor(x/2)+1 are shared by column pairs. Per input row the thread
+// loads its window segment once (LDS.128 / LDS.64, conflict-free) and feeds it to up to RY pixel
+// rows; the taps are loaded per pixel (LDS.128 rows at per-pixel addresses) and shared by the
+// three colour channels (R13). FP32 FMA on the CUDA cores. RY = 4 (4 warps per group, 8 per SM)
+// is used on large, wide levels: 16% fewer shared-memory wavefronts per pixel.
 #pragma once
 #include <cuda.h>
 #include <cstdint>

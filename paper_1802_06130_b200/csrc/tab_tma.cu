@@ -20,6 +20,9 @@ const std::vector<TmaVariant>& tma_variants() {
       make_tma<3, 0, false, false, 4>(), make_tma<5, 0, false, false, 4>(), make_tma<7, 0, false, false, 4>(),
       make_tma<9, 0, false, false, 4>(), make_tma<3, 3, false, false, 4>(), make_tma<5, 5, false, false, 4>(),
       make_tma<5, 3, false, false, 4>(),
+      make_tma<3, 0, true, false, 4>(), make_tma<5, 0, true, false, 4>(), make_tma<7, 0, true, false, 4>(),
+      make_tma<9, 0, true, false, 4>(), make_tma<3, 3, true, false, 4>(), make_tma<5, 5, true, false, 4>(),
+      make_tma<5, 3, true, false, 4>(),
       // per-channel YCbCr banks (NEXT f1): CTAs specialised by channel
       make_tma<3, 0, true>(), make_tma<5, 0, true>(), make_tma<7, 0, true>(), make_tma<9, 0, true>(),
       make_tma<3, 3, true>(), make_tma<5, 5, true>(), make_tma<5, 3, true>(),
