@@ -159,17 +159,18 @@ def algorithmic_work(cfg, N):
     return out
 
 
-def stage_smem_bytes_per_px(cfg):
+def stage_smem_bytes_per_px(cfg, kind="k_stage_tma", ry=2):
     """Algorithmic (conflict-free) shared-memory bytes per output pixel of the stage kernel:
     every tap of the pixel's filter once (4 B), plus the window values a thread reads per pixel
-    (k_stage_tma: 2 x 4 pixels per thread share window rows; k_stage_ph: 2 x 2 sub-lattice)."""
+    (k_stage_tma: ry x 4 pixels per thread share window rows; k_stage_ph: 2 x 2 sub-lattice)."""
     nf = cfg.fine_size
     nc = cfg.coarse_size if cfg.levels > 1 else 0
     taps = 4 * (nf * nf + nc * nc)
-    if cfg.levels > 1 and nf >= 7:  # phase-split kernel, 2 x 2 sub-lattice pixels per thread
+    if kind == "k_stage_ph":  # phase-split kernel, 2 x 2 sub-lattice pixels per thread
         vals = (nf + 2) * (nf + 2) * 12 / 4 + (nc + 1) * (nc + 1) * 12 / 4
-    else:                           # 2 x 4 pixels per thread
-        vals = (nf + 1) * (nf + 3) * 12 / 8 + (nc * (nc + 1) * 12 / 8 if nc else 0)
+    else:                     # ry x 4 pixels per thread
+        vals = (nf + ry - 1) * (nf + 3) * 12 / (4 * ry) + \
+            ((nc + ry // 2 - 1) * (nc + 1) * 12 / (4 * ry) if nc else 0)
     return taps + vals
 
 
@@ -451,13 +452,18 @@ def main():
             # the unit that binds this kernel: shared memory. Conflict-free
             # algorithmic smem bytes / launch time vs 128 B/clk/SM; bank conflicts are the rest.
             px = w["flops"] / (6 * (cfg.fine_size ** 2 + (cfg.coarse_size ** 2 if cfg.levels > 1 else 0)))
-            sb = px * stage_smem_bytes_per_px(cfg)
+            n_launch = (min(args.chunk, n_local) if args.chunk else n_local) if shard.mode == "frames" else 1
+            skind, sry = h.stage_kernel(n_launch, H if shard.mode == "frames" else shard.out_rows, W, dom[1])
+            roof["kernel"] = f"{skind} level {dom[1]} ({sry} rows/thread)" if skind == "k_stage_tma" \
+                else f"{skind} level {dom[1]}"
+            sb = px * stage_smem_bytes_per_px(cfg, skind, sry)
             sp = n_sm * 128 * sm_max * 1e6 / 1e12  # TB/s
             roof["sram"] = {"achieved": sb / (dom_ms / 1e3) / 1e12, "peak": sp, "unit": "TB/s",
                             "frac": sb / (dom_ms / 1e3) / 1e12 / sp,
-                            "bytes_per_px": stage_smem_bytes_per_px(cfg),
+                            "bytes_per_px": stage_smem_bytes_per_px(cfg, skind, sry),
                             "note": "conflict-free model (taps 4 B each + window values); ncu "
-                                    "shows L1/TEX ~94% busy with 2.7-way tap-load bank conflicts"}
+                                    "shows L1/TEX ~91% busy, LDS.128 tap loads at ~2x their ideal "
+                                    "wavefronts (bank conflicts)"}
     else:
         ach = w["bytes"] / (dom_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": f"k_down level {dom[1]}", "achieved": ach, "peak": hbm_peak,

@@ -244,6 +244,13 @@ blade_status blade_ms_get_info(blade_ms_t h, blade_ms_info* info);
 /* Number of kernel launches one blade_ms_denoise(N, H, W) call issues. */
 blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t* count);
 
+/* Diagnostic: the stage kernel blade_ms_denoise(N, H, W) runs at stage `level` (0 .. n_stages-1)
+ * with 16-byte aligned buffers: *kind = 0 generic k_stage, 1 k_stage_tma, 2 k_stage_ph (phase-
+ * split); *rows_per_thread = output rows per thread of k_stage_tma (2 or 4; 2 otherwise). Used by
+ * bench.py's shared-memory roofline model and the tests. EINVAL for a bad level. */
+blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t level,
+                                   int32_t* kind, int32_t* rows_per_thread);
+
 /*
  * Per-kernel timing (measurement support for bench.py). While enabled, every launch the handle
  * enqueues is bracketed by two CUDA events recorded on the launching stream. blade_ms_profile_read

@@ -55,6 +55,7 @@ EXPORTS = ["blade_ms_create", "blade_ms_workspace_size", "blade_ms_denoise", "bl
            "blade_ms_train_layout", "blade_ms_train_workspace_size", "blade_ms_train_accumulate",
            "blade_ms_train_solve", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
            "blade_ms_selector", "blade_ms_pyramid", "blade_ms_get_info", "blade_ms_launch_count",
+           "blade_ms_stage_kernel",
            "blade_ms_set_profiling", "blade_ms_profile_read",
            "blade_ms_destroy", "blade_ms_status_string", "blade_ms_last_error"]
 
@@ -100,6 +101,7 @@ def lib():
     L.blade_ms_pyramid.argtypes = [P, P, i32, i32, i32, P, P, sz, P]
     L.blade_ms_get_info.argtypes = [P, ctypes.POINTER(_Info)]
     L.blade_ms_launch_count.argtypes = [P, i32, i32, i32, ctypes.POINTER(i32)]
+    L.blade_ms_stage_kernel.argtypes = [P, i32, i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.blade_ms_set_profiling.argtypes = [P, i32]
     L.blade_ms_profile_read.argtypes = [P, P, P]
     L.blade_ms_destroy.argtypes = [P]
@@ -203,6 +205,14 @@ class BladeMS:
         c = ctypes.c_int32()
         _check(lib().blade_ms_launch_count(self._h, N, H, W, ctypes.byref(c)))
         return c.value
+
+    STAGE_KINDS = ("k_stage", "k_stage_tma", "k_stage_ph")
+
+    def stage_kernel(self, N: int, H: int, W: int, level: int) -> tuple[str, int]:
+        """(kernel name, output rows per thread) of stage `level` for a denoise(N, H, W) call."""
+        k, r = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().blade_ms_stage_kernel(self._h, N, H, W, level, ctypes.byref(k), ctypes.byref(r)))
+        return self.STAGE_KINDS[k.value], r.value
 
     def fallback_count(self, N: int, H: int, W: int, workspace: torch.Tensor) -> list[int]:
         """Uncertified (fp64-recomputed) selector pixels per level of the last call that used

@@ -354,6 +354,18 @@ int tma_ry() {
   return v;
 }
 
+// Rows per thread of the TMA stage kernel for a level of width W whose computed rows span
+// `span`: large, wide levels (many tiles per SM, few border / partial tiles) take 4, others 2
+// (measured: c3 level 0 2.56 -> 2.36 ms, but level 1 (7.5 tiles wide) 0.75 -> 0.80 ms, and the
+// latency-bound small levels are slower with 8 warps per SM).
+bool use_ry4(const blade_ms* h, int N, int W, int span) {
+  if (!h->has_tma4 || tma_ry() == 2) return false;
+  if (tma_ry() == 4) return true;
+  const int tiles_x = (W + h->tma.tcols - 1) / h->tma.tcols;
+  const long long tiles = (long long)N * tiles_x * ((span + h->tma.trows - 1) / h->tma.trows);
+  return tiles_x >= 12 && tiles >= 8LL * h->num_sms;
+}
+
 // Kernel launch; with `pdl` the launch allows programmatic stream serialisation (PDL): the grid
 // may be scheduled while the previous kernel in the stream drains, and its kernels call pdl_wait()
 // before reading that kernel's outputs (kernels.cuh). BLADE_PDL=0 turns it off (A/B timing).
@@ -515,14 +527,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       }
     }
     if (use_tma) {
-      // large, wide levels (many tiles per SM, few border / partial tiles): 4 pixel rows per
-      // thread; otherwise 2 (measured: c3 level 0 2.56 -> 2.36 ms, but level 1 (7.5 tiles wide)
-      // 0.75 -> 0.80 ms and the latency-bound small levels slower with 8 warps per SM)
-      const int tiles_x = (p.W[l] + h->tma.tcols - 1) / h->tma.tcols;
-      const long long tiles_est = (long long)N * tiles_x * ((r.hi - y_base + h->tma.trows - 1) / h->tma.trows);
-      const bool ry4 = h->has_tma4 && tma_ry() != 2 &&
-                       (tma_ry() == 4 || (tiles_x >= 12 && tiles_est >= 8LL * h->num_sms));
-      const TmaVariant& tv = ry4 ? h->tma4 : h->tma;
+      const TmaVariant& tv = use_ry4(h, N, p.W[l], r.hi - y_base) ? h->tma4 : h->tma;
       StageTmaArgs a{};
       a.H = p.H[l];
       a.W = p.W[l];
@@ -990,6 +995,29 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
   const int L = h->cfg.levels;
   // k_down + k_down_fixup + k_stage per stage level (+ the YCbCr -> RGB conversion with per-channel banks)
   *count = N == 0 ? 0 : 3 * (L == 1 ? 1 : L - 1) + (h->cfg.n_filter_channels == 3 ? 1 : 0);
+  return BLADE_OK;
+}
+
+blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t level, int32_t* kind,
+                                   int32_t* rows_per_thread) {
+  if (!h || !kind || !rows_per_thread) return fail(BLADE_EINVAL, "NULL argument");
+  blade_status s = check_dims(N, H, W);
+  if (s != BLADE_OK) return s;
+  if (level < 0 || level >= h->n_stages) return fail(BLADE_EINVAL, "level %d outside 0..%d", level, h->n_stages - 1);
+  Plan p;
+  plan_rows(h, std::max(N, 1), H, W, 0, H, p);
+  const int L = p.L, l = level;
+  const bool tma = h->has_tma && p.W[l] % 16 == 0 && (L == 1 || p.W[l + 1] % 4 == 0);
+  if (!tma) {
+    *kind = 0;
+    *rows_per_thread = 2;
+  } else if (h->tma.phase_split) {
+    *kind = 2;
+    *rows_per_thread = 2;
+  } else {
+    *kind = 1;
+    *rows_per_thread = use_ry4(h, N, p.W[l], p.u[l].hi - (p.u[l].lo & ~1)) ? 4 : 2;
+  }
   return BLADE_OK;
 }
 

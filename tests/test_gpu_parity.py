@@ -437,3 +437,20 @@ def test_forced_variants_subprocess(env):
     r = subprocess.run(cmd, cwd=root, env={**os.environ, **env}, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_stage_kernel_selection():
+    """The variant each level runs (blade_ms_stage_kernel): the bench's c3 level 0 takes the
+    4-row TMA kernel, its 7.5-tile-wide level 1 the 2-row one; 7x7 / 9x9 pairs the phase-split
+    kernel; ragged widths the generic kernel."""
+    c3 = bs.load_config("c3")
+    h = _handle(c3)
+    assert h.stage_kernel(64, 1080, 1920, 0) == ("k_stage_tma", 4)
+    assert h.stage_kernel(64, 1080, 1920, 1) == ("k_stage_tma", 2)
+    assert h.stage_kernel(1, 512, 512, 0) == ("k_stage_tma", 2)
+    assert h.stage_kernel(1, 130, 259, 0)[0] == "k_stage"
+    assert _handle(bs.load_config("c2")).stage_kernel(1, 3000, 4000, 0)[0] == "k_stage_ph"
+    assert _handle(bs.load_config("c4")).stage_kernel(1, 6000, 8000, 0)[0] == "k_stage_ph"
+    from paper_1802_06130_b200.blade_ms import BladeError
+    with pytest.raises(BladeError):
+        h.stage_kernel(1, 64, 64, 2)
