@@ -251,7 +251,7 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
 
 // grid: ceil(n_tasks / WARPS) CTAs of 32 * WARPS threads; task = (frame, band, strip), strip fastest.
 template <bool HILO, bool DEC, bool FAST, bool WIDE>
-__global__ void __launch_bounds__(32 * down::WARPS, 3) k_down(const DownArgs a, const DownParams prm) {
+__global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const DownArgs a, const DownParams prm) {
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;  // bucket map entry
   using namespace down;
   constexpr int NP = HILO ? 6 : 3;  // planes per ring row (3 channels, x2 with lo)
