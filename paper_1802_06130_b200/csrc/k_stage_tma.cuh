@@ -410,6 +410,10 @@ __global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
 #pragma unroll
         for (int c = 0; c < PL; ++c) acc[i][j][c] = 0.0f;
 
+    // threads whose block lies wholly outside the image (the right part of a partial last tile
+    // column, rows past the last output row) issue no shared-memory traffic at all
+    const bool active = x < a.W && y < a.o_r0 + a.o_rn && y + RY > a.o_r0;
+    if (active) {
     if constexpr (NC > 0) {
       // coarse rows local ty RY/2 .. + NC + RY/2 - 1 (pixel row i sits on coarse row wr - i/2 of its
       // window); cols 2tx .. 2tx+NC
@@ -486,6 +490,7 @@ __global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
         }
       }
     }
+    }  // active
     group_sync();  // buffer b is free for the next TMA into it
     if (G == 2 && tid == 0 && tn < a.n_tiles) {
       fence_proxy_async();
