@@ -122,7 +122,12 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
     group_sync();
   }
 
-  // ---- this thread's 2 x 2 sub-lattice block: image pixels (Y0 + py + 4 ty + 2 i, X0 + PX + 4 tx + 2 j)
+  // ---- this thread's 2 x 2 sub-lattice block: image pixels (Y0 + py + 4 ty + 2 i, X0 + PX + 4 tx + 2 j);
+  //      a block wholly outside the image / the output rows issues no shared-memory traffic
+  {
+    const int y0 = Y0 + py + 4 * ty, x0 = X0 + PX + 4 * tx;
+    if (x0 >= a.W || y0 >= a.o_r0 + a.o_rn || y0 + 2 < a.o_r0) return;
+  }
   const float* tp[2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
