@@ -456,9 +456,9 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     const int span = R.hi - da.base;
     da.n_strips = (p.W[l] + down::STRIP - 1) / down::STRIP;
     // band height RB (even, 4..128): a task is RB + 6 input rows of one 64-column strip; pick
-    // the RB that minimises (RB + 6) x waves, waves = tasks / resident warp slots, counted in whole
-    // waves while the grid is short (< 2 waves: small images want thin bands, their halo rows are
-    // cheaper than idle SMs) and fractionally beyond (large batches want tall bands)
+    // the RB that minimises (RB + 6) x ceil(tasks / resident warp slots): small images want thin
+    // bands (their halo rows are cheaper than idle SMs), large batches tall ones, and no launch
+    // should end with a sliver of a wave
     const long long col_tasks = (long long)N * da.n_strips;
     const double slots = (double)h->down_slots[l > 0 ? 1 : 0];
     int RB = 128;
@@ -466,7 +466,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     for (int rb = 128; rb >= 4; rb -= 2) {
       const double tasks = (double)col_tasks * (double)((span + rb - 1) / rb);
       const double w = tasks / slots;
-      const double cost = (rb + 6) * (w < 2.0 ? std::ceil(w) : w);
+      const double cost = (rb + 6) * std::ceil(w);
       if (rb == 128 || cost < best) {
         best = cost;
         RB = rb;
