@@ -454,3 +454,40 @@ def test_stage_kernel_selection():
     from paper_1802_06130_b200.blade_ms import BladeError
     with pytest.raises(BladeError):
         h.stage_kernel(1, 64, 64, 2)
+
+
+# ------------------------------------------------------------------------- selector / layout variants
+
+_TS1, _TC1 = [0.12769653, 0.15104799], [0.06869324, 0.12480995]  # c1 stage-0 tertiles (fp32)
+LAYOUTS = {
+    # non-FAST bucket layouts: quadrant edges with 1 / 2 interior edges, the atan2 path (n_o % 4 != 0)
+    "8x4x2": dict(n_orient=8, n_strength=4, n_coherence=2, ts=[0.06, 0.11, 0.15], tc=[0.1]),
+    "12x2x3": dict(n_orient=12, n_strength=2, n_coherence=3, ts=[0.12], tc=_TC1),
+    "6x3x3_atan2": dict(n_orient=6, n_strength=3, n_coherence=3, ts=_TS1, tc=_TC1),
+    "1x1x1": dict(n_orient=1, n_strength=1, n_coherence=1, ts=[], tc=[]),       # one filter
+    "16x4x4_K256": dict(n_orient=16, n_strength=4, n_coherence=4, ts=[0.06, 0.11, 0.15],
+                        tc=[0.05, 0.09, 0.14]),                                   # largest uint8 K
+    "20x4x4_K320": dict(n_orient=20, n_strength=4, n_coherence=4, ts=[0.06, 0.11, 0.15],
+                        tc=[0.05, 0.09, 0.14]),                                   # uint16 maps
+    "nonpos_thresholds": dict(ts=[0.0, 0.12], tc=[-0.5, 0.1]),                  # t <= 0 [R6]
+    "window3": dict(window_size=3, window_sigma=0.8),
+    "window1": dict(window_size=1, window_sigma=1.0),
+    "one_phase": dict(n_phases=1),                                               # SPEC reading
+}
+
+
+@pytest.mark.parametrize("shape", [(2, 160, 256), (1, 97, 131)])
+@pytest.mark.parametrize("name", list(LAYOUTS))
+def test_selector_and_layout_variants(name, shape):
+    """Every parameter the ABI accepts besides the configs' own: bucket layouts that take the
+    generic (binary-search / quadrant-edge / atan2) selector paths, K = 1 and the uint8 / uint16
+    limits, non-positive thresholds, 3x3 and 1x1 structure-tensor windows, phase-free banks; on a
+    TMA-eligible and a ragged (generic stage kernel) shape, against the oracle."""
+    N, H, W = shape
+    over = dict(LAYOUTS[name])
+    ts, tc = over.pop("ts", None), over.pop("tc", None)
+    cfg = _cfg_like("c1", H, W, N, **over)
+    if ts is not None:
+        cfg.strength_thresholds = [list(ts)] * cfg.n_stages
+        cfg.coherence_thresholds = [list(tc)] * cfg.n_stages
+    _full_parity(cfg, cfg.batch(), label=f"{name}@{H}x{W}")
