@@ -491,3 +491,18 @@ def test_selector_and_layout_variants(name, shape):
         cfg.strength_thresholds = [list(ts)] * cfg.n_stages
         cfg.coherence_thresholds = [list(tc)] * cfg.n_stages
     _full_parity(cfg, cfg.batch(), label=f"{name}@{H}x{W}")
+
+
+@pytest.mark.parametrize("shape", [(2, 130, 256), (1, 77, 190)])
+@pytest.mark.parametrize("levels,nf,nc", [(2, 3, 3), (2, 5, 3), (3, 7, 5), (2, 9, 7), (1, 3, 0), (1, 5, 0),
+                                          (1, 9, 0), (4, 3, 3)])
+def test_footprint_variants(levels, nf, nc, shape):
+    """Every built footprint pair / single-level size beyond the configs' (5+5, 7+7, 9+9, 7 and the
+    wide 7+5), through the TMA (or phase-split) and generic stage kernels, against the oracle."""
+    N, H, W = shape
+    cfg = _cfg_like("c1", H, W, N, levels=levels, fine_size=nf, coarse_size=nc,
+                    n_phases=4 if levels > 1 else 1)
+    nst = max(levels - 1, 1)
+    cfg.strength_thresholds = [list(_TS1)] * nst
+    cfg.coherence_thresholds = [list(_TC1)] * nst
+    _full_parity(cfg, cfg.batch(), label=f"L{levels} {nf}+{nc}@{H}x{W}")
