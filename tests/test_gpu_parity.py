@@ -506,3 +506,36 @@ def test_footprint_variants(levels, nf, nc, shape):
     cfg.strength_thresholds = [list(_TS1)] * nst
     cfg.coherence_thresholds = [list(_TC1)] * nst
     _full_parity(cfg, cfg.batch(), label=f"L{levels} {nf}+{nc}@{H}x{W}")
+
+
+@pytest.mark.parametrize("name", ["c1", "c5"])
+def test_fixup_list_overflow_recomputes_everything(name):
+    """A frame whose top half is an exact 45-degree ramp puts every pixel there on an orientation
+    bin edge, so the fp32 certificate rejects far more pixels than the fix-up list holds (1/64 of
+    the level): the fix-up kernel must then recompute the WHOLE map in fp64. Check: the overflow
+    happened; on the natural bottom half the map obeys the parity rule; on the ramp every bucket
+    equals the oracle's or differs by one orientation bin (the decision sits exactly on an edge)."""
+    cfg = _cfg_like(name, 256, 384, 1)
+    x = cfg.batch()
+    H, W = 256, 384
+    yy, xx = np.mgrid[0:H // 2, 0:W]
+    x[0, :, :H // 2] = (0.25 + (xx + yy) * 2.0 ** -10).astype(np.float32)  # exact in fp32
+    h = _handle(cfg)
+    xt = torch.from_numpy(x).cuda()
+    ws = h.workspace(1, H, W)
+    maps = h.selector(xt, workspace=ws)
+    counts = h.fallback_count(1, H, W, ws)
+    assert counts[0] > H * W // 64, counts  # the list overflowed at level 0
+    gpu = maps[0][0].cpu().numpy().astype(np.int64)
+    ts, tc = cfg.thresholds()
+    ob, feats = oracle.selector(x[0].astype(np.float64), cfg.n_orient, cfg.n_strength, cfg.n_coherence,
+                                ts[0], tc[0], cfg.window_size, cfg.window_sigma, features=True)
+    lo = H // 2 + 4  # rows whose 5x5 window and gradients see only the natural half
+    check_buckets(gpu[lo:], ob[lo:], tuple(f[lo:] for f in feats), cfg.n_orient, ts[0], tc[0],
+                  f"{name} natural half after overflow")
+    per_o = cfg.n_strength * cfg.n_coherence
+    top = slice(2, H // 2 - 3)  # the pure ramp (away from the image border fold and the seam)
+    og, oo = gpu[top] // per_o, ob[top] // per_o
+    d = (og - oo) % cfg.n_orient
+    assert np.isin(d, [0, 1, cfg.n_orient - 1]).all()
+    assert (gpu[top] % per_o == ob[top] % per_o).all()  # strength / coherence bins agree
