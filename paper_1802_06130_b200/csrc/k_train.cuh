@@ -159,7 +159,12 @@ __global__ void __launch_bounds__(256) k_train_gram(const TrainArgs a) {
     }
   };
   const unsigned int hw = (unsigned int)a.H * (unsigned int)a.W;  // N H W < 2^32 (checked on the host)
-  __shared__ int pn[B], py[B], px[B];
+  __shared__ int pn[B];
+  // per batch pixel: folded row offsets (row * W, into the frame's plane) and folded columns of its
+  // fine and coarse windows, computed once per pixel instead of once per gathered sample
+  __shared__ int frow[B][NF], fcol[B][NF];
+  __shared__ int crow[B][NC > 0 ? NC : 1], ccol[B][NC > 0 ? NC : 1];
+  __shared__ int ctr[B];  // offset of the centre pixel in its plane
   for (int e = t; e < B * 3 * (NTP - NT - 1); e += TS::THREADS) {  // padding columns stay zero
     const int j = e / (3 * (NTP - NT - 1)), rem = e - j * 3 * (NTP - NT - 1);
     const int c = rem / (NTP - NT - 1), q = rem - c * (NTP - NT - 1);
@@ -174,33 +179,43 @@ __global__ void __launch_bounds__(256) k_train_gram(const TrainArgs a) {
       const unsigned int n = pix / hw, r = pix - n * hw;
       const unsigned int y = r / (unsigned int)a.W;
       pn[t] = (int)n;
-      py[t] = (int)y;
-      px[t] = (int)(r - y * (unsigned int)a.W);
+      ctr[t] = (int)r;
       segs[t] = train_seg<WIDE>(a, pix);
+      const int yy = (int)y, xx = (int)(r - y * (unsigned int)a.W);
+#pragma unroll
+      for (int d = 0; d < NF; ++d) {
+        frow[t][d] = fold_idx(yy + d - RF, a.H) * a.W;
+        fcol[t][d] = fold_idx(xx + d - RF, a.W);
+      }
+      if constexpr (NC > 0) {
+#pragma unroll
+        for (int d = 0; d < NC; ++d) {
+          crow[t][d] = fold_idx(yy / 2 + d - RC, a.H1) * a.W1;
+          ccol[t][d] = fold_idx(xx / 2 + d - RC, a.W1);
+        }
+      }
     }
     __syncthreads();
     // ---- gather the samples (fp64): fine taps, coarse taps, target (column NT); three
     //      branch-free loops so the lanes of a warp stay converged
+    const long long plane = (long long)a.H * a.W, plane1 = (long long)a.H1 * a.W1;
     for (int e = t; e < nb * 3 * NF * NF; e += TS::THREADS) {
       const int j = e / (3 * NF * NF), rem = e - j * (3 * NF * NF);
       const int c = rem / (NF * NF), tap = rem - c * (NF * NF);
-      const int dy = tap / NF - RF, dx = tap % NF - RF;
-      xs[j][c][tap] = (double)__ldg(a.z + (((long long)pn[j] * 3 + c) * a.H + fold_idx(py[j] + dy, a.H)) * a.W +
-                                    fold_idx(px[j] + dx, a.W));
+      const int dy = tap / NF, dx = tap - dy * NF;
+      xs[j][c][tap] = (double)__ldg(a.z + ((long long)pn[j] * 3 + c) * plane + frow[j][dy] + fcol[j][dx]);
     }
     if constexpr (NC > 0) {
       for (int e = t; e < nb * 3 * NC * NC; e += TS::THREADS) {
         const int j = e / (3 * NC * NC), rem = e - j * (3 * NC * NC);
         const int c = rem / (NC * NC), tc = rem - c * (NC * NC);
-        const int dy = tc / NC - RC, dx = tc % NC - RC;
-        xs[j][c][NF * NF + tc] =
-            (double)__ldg(a.u1 + (((long long)pn[j] * 3 + c) * a.H1 + fold_idx(py[j] / 2 + dy, a.H1)) * a.W1 +
-                          fold_idx(px[j] / 2 + dx, a.W1));
+        const int dy = tc / NC, dx = tc - dy * NC;
+        xs[j][c][NF * NF + tc] = (double)__ldg(a.u1 + ((long long)pn[j] * 3 + c) * plane1 + crow[j][dy] + ccol[j][dx]);
       }
     }
     for (int e = t; e < nb * 3; e += TS::THREADS) {
       const int j = e / 3, c = e - 3 * j;
-      xs[j][c][NT] = (double)__ldg(a.uc + (((long long)pn[j] * 3 + c) * a.H + py[j]) * a.W + px[j]);
+      xs[j][c][NT] = (double)__ldg(a.uc + ((long long)pn[j] * 3 + c) * plane + ctr[j]);
     }
     __syncthreads();
     // ---- accumulate (uniform over the CTA: segment changes flush)
