@@ -376,13 +376,27 @@ def main():
 
     if args.train:
         nt = cfg.fine_size ** 2 + (cfg.coarse_size ** 2 if cfg.levels > 1 else 0)
+        dfma_px = 3 * (((nt + 1 + 3) // 4) * (((nt + 1 + 3) // 4) + 1) // 2) * 16
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+            if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        fp64_peak = n_sm * 64 * 2 * sm_max * 1e6 / 1e12
         line = {"metric": "megapixels/sec of training data (stage-0 normal equations, f4)",
                 "value": value, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64 accumulation",
                 "data": "synthetic", "config": {"workload": cfg.name, "frames": cfg.N, "H": H, "W": W,
                                                  "taps": nt, "segments": cfg.n_phases * cfg.K},
-                "dfma_per_px": 3 * (((nt + 1 + 3) // 4) * (((nt + 1 + 3) // 4) + 1) // 2) * 16,
+                "dfma_per_px": dfma_px,
+                "roofline": {"bound": "alu", "kernel": "k_train_gram (+ selector, sort)",
+                             "achieved": value * 1e6 * dfma_px * 2 / 1e12, "peak": fp64_peak,
+                             "unit": "TFLOP/s", "frac": value * 1e6 * dfma_px * 2 / 1e12 / fp64_peak,
+                             "traffic": None,
+                             "peak_source": f"derived: {n_sm} SMs x 64 FP64 lanes x 2 x {sm_max:.0f} MHz",
+                             "note": "whole training step time (all kernels) against the FP64 pipe; "
+                                     "algorithmic DFMA = 3 channels x 16 per 4x4 block of the upper "
+                                     "block triangle of the (nt+1)-padded Gram"},
                 "clocks": clocks}
         if rank == 0:
             print(json.dumps(line), flush=True)
