@@ -488,7 +488,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
     auto fx = fixup_kernel(hilo, fast, wide);
-    LAUNCH("k_down_fixup", launch(fx, 4 * h->num_sms, 128, 0, st, true, da, h->down[l]));
+    LAUNCH("k_down_fixup", launch(fx, 8 * h->num_sms, 128, 0, st, true, da, h->down[l]));
   }
   if (!run_stages) return BLADE_OK;
 
