@@ -95,11 +95,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 3D tiled map over a [depth][rows][W] array of `esize`-byte elements.
 bool encode_3d(CUtensorMap* tm, const void* base, CUtensorMapDataType dt, int esize, int W, int rows,
-               int depth, int bw, int bh, int bd) {
+               int depth, int bw, int bh, int bd, int pitch = 0) {
   auto enc = get_encode();
   if (!enc) return false;
+  if (pitch <= 0) pitch = W;  // row pitch in elements (the rows of a map may be padded)
   const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)depth};
-  const cuuint64_t strides[2] = {(cuuint64_t)W * esize, (cuuint64_t)W * esize * rows};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * esize, (cuuint64_t)pitch * esize * rows};
   const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bd};
   const cuuint32_t es[3] = {1, 1, 1};
   return enc(tm, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -185,6 +186,7 @@ struct Plan {
   std::vector<Range> u;  // rows of u^l computed (= map rows), l <= L-2 (l = 0 if L == 1)
   size_t ws_bytes = 0;
   std::vector<size_t> z32_off, zlo_off, u_off, map_off, fb_off;
+  std::vector<int> map_pitch;  // entries per map row: W_l rounded up to 16 (16-B TMA rows)
   std::vector<unsigned int> fb_cap;
   size_t fbcnt_off = 0;
 };
@@ -233,6 +235,8 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
   p.zlo_off.assign(L, 0);
   p.u_off.assign(L, 0);
   p.map_off.assign(L, 0);
+  p.map_pitch.assign(L, 0);
+  for (int l = 0; l < L; ++l) p.map_pitch[l] = (p.W[l] + 15) & ~15;
   for (int l = 1; l < L; ++l) {
     p.z32_off[l] = off;
     off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
@@ -248,7 +252,7 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
   const int nsel = L == 1 ? 1 : L - 1;
   for (int l = 0; l < nsel; ++l) {
     p.map_off[l] = off;
-    off = align256(off + (size_t)map_es * N * p.u[l].n() * p.W[l]);
+    off = align256(off + (size_t)map_es * N * p.u[l].n() * p.map_pitch[l]);
   }
   // uncertified-pixel lists of the fp32 selector (DESIGN.md §6 H1): 1/64 of each level's map
   p.fb_off.assign(nsel, 0);
@@ -421,6 +425,8 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   std::vector<uint8_t*> maps(nsel);  // byte addresses of uint8 / uint16 maps
   for (int l = 0; l < nsel; ++l)
     maps[l] = (maps_out && maps_out[l]) ? static_cast<uint8_t*>(maps_out[l]) : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
+  std::vector<int> mpitch(nsel);  // caller-provided maps are dense [N][H][W]; workspace maps padded
+  for (int l = 0; l < nsel; ++l) mpitch[l] = (maps_out && maps_out[l]) ? p.W[l] : p.map_pitch[l];
 
   // ---- down pass: k_down(l) -> s^l, z^{l+1} (hi, and lo when level l+1 feeds a selector);
   //      k_down_fixup(l) recomputes the (rare) pixels whose fp32 orientation is uncertified
@@ -442,6 +448,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.in_plane = (long long)da.in_rows * p.W[l];
     da.in_frame = 3 * da.in_plane;
     da.map = maps[l];
+    da.map_pitch = mpitch[l];
     da.s_r0 = U.lo;
     da.s_rn = U.n();
     da.ohi = dec ? z32[l + 1].p : nullptr;
@@ -508,16 +515,18 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     const int clamp = (l == 0 && h->cfg.clamp_output) ? 1 : 0;
     ProfScope ps(h, st, 2, l);
     // TMA path: needs 16-B aligned buffers whose row pitches are 16-B multiples
-    bool use_tma = h->has_tma && p.W[l] % 16 == 0 && aligned16(zl.p) && aligned16(outv.p) &&
-                   aligned16(maps[l]) && (L == 1 || (p.W[l + 1] % 4 == 0 && aligned16(u1.p)));
+    const int map_es = h->K > 256 ? 2 : 1;
+    bool use_tma = h->has_tma && p.W[l] % 4 == 0 && (mpitch[l] * map_es) % 16 == 0 && aligned16(zl.p) &&
+                   aligned16(outv.p) && aligned16(maps[l]) &&
+                   (L == 1 || (p.W[l + 1] % 4 == 0 && aligned16(u1.p)));
     CUtensorMap tmz, tmu, tmm;
     if (use_tma) {
       const TmaVariant& tv = h->tma;
       use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb, tv.fr, 3) &&
                 (h->K > 256 ? encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p.W[l], r.n(), N, tv.tcols,
-                                        tv.trows, 1)
+                                        tv.trows, 1, mpitch[l])
                             : encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.W[l], r.n(), N, tv.tcols,
-                                        tv.trows, 1));
+                                        tv.trows, 1, mpitch[l]));
       if (use_tma) {
         if (L > 1)
           use_tma = encode_3d(&tmu, u1.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l + 1], u1.rows, N * 3, tv.ccb,
@@ -591,6 +600,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     a.map = maps[l];
     a.map_row0 = r.lo;
     a.map_rows = r.n();
+    a.map_pitch = mpitch[l];
     a.bank = bank;
     a.K = h->K;
     a.S = h->S;
@@ -1007,7 +1017,7 @@ blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W
   Plan p;
   plan_rows(h, std::max(N, 1), H, W, 0, H, p);
   const int L = p.L, l = level;
-  const bool tma = h->has_tma && p.W[l] % 16 == 0 && (L == 1 || p.W[l + 1] % 4 == 0);
+  const bool tma = h->has_tma && p.W[l] % 4 == 0 && (L == 1 || p.W[l + 1] % 4 == 0);
   if (!tma) {
     *kind = 0;
     *rows_per_thread = 2;
@@ -1284,6 +1294,7 @@ blade_status blade_ms_train_accumulate(blade_ms_t h, int32_t level, const float*
   da.in_plane = (long long)H * W;
   da.in_frame = 3 * da.in_plane;
   da.map = w + tp.map_off;
+  da.map_pitch = W;
   da.s_r0 = 0;
   da.s_rn = H;
   da.H1 = da.W1 = 1;

@@ -52,9 +52,10 @@ struct DownArgs {
   const float* zlo;  // level l lo plane (nullptr at l = 0)
   int H, W, in_row0, in_rows;
   long long in_plane, in_frame;
-  void* map;         // s^l rows [s_r0, s_r0 + s_rn), pitch W, frame stride s_rn * W; uint8
-                     // entries (K <= 256) or uint16 (WIDE, K <= 65536)
-  int s_r0, s_rn;
+  void* map;         // s^l rows [s_r0, s_r0 + s_rn), pitch map_pitch (>= W; a multiple of 16 in
+                     // the workspace so the stage can TMA it), frame stride s_rn * map_pitch;
+                     // uint8 entries (K <= 256) or uint16 (WIDE, K <= 65536)
+  int s_r0, s_rn, map_pitch;
   float* ohi;        // z^{l+1} hi: rows [d_buf_row0, + d_buf_rows), pitch W1 (nullptr: no dec)
   float* olo;        // z^{l+1} lo (nullptr: not needed, l + 1 is the coarsest level)
   int H1, W1, d_buf_row0, d_buf_rows, d_r0, d_rn;
@@ -333,11 +334,11 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
     lm[c][0] = lm[c][1] = lc[c][0] = lc[c][1] = lL[c] = lR[c] = 0.0f;
   }
 
-  MT* mapf = static_cast<MT*>(a.map) + (long long)n * a.s_rn * a.W;
+  MT* mapf = static_cast<MT*>(a.map) + (long long)n * a.s_rn * a.map_pitch;
   const long long oframe = (long long)n * 3 * a.d_buf_rows * a.W1;
   const int Xd = x >> 1;  // decimated column (x even)
   // 2-byte map stores when every map row starts 2-B aligned (x is even)
-  const bool map16 = (a.W & 1) == 0 && (reinterpret_cast<uintptr_t>(a.map) & (2 * sizeof(MT) - 1)) == 0;
+  const bool map16 = (a.map_pitch & 1) == 0 && (reinterpret_cast<uintptr_t>(a.map) & (2 * sizeof(MT) - 1)) == 0;
 
 #pragma unroll 2
   for (int i = 0; i < nrows; ++i) {
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
         }
       }
       if (emit && x < a.W) {
-        MT* mrow = mapf + (long long)(y - a.s_r0) * a.W + x;
+        MT* mrow = mapf + (long long)(y - a.s_r0) * a.map_pitch + x;
         if (map16 && x + 1 < a.W) {  // both entries in one store
           if constexpr (WIDE)
             *reinterpret_cast<uint32_t*>(mrow) = (uint32_t)bk[0] | ((uint32_t)bk[1] << 16);
@@ -564,7 +565,9 @@ __global__ void __launch_bounds__(128) k_down_fixup(const DownArgs a, const Down
       pb += __shfl_xor_sync(0xffffffffu, pb, o);
       pc += __shfl_xor_sync(0xffffffffu, pc, o);
     }
-    if (lane == 0) static_cast<MT*>(a.map)[e] = (MT)bucket_of<FAST>(pa, pb, pc, prm);
+    if (lane == 0)
+      static_cast<MT*>(a.map)[((unsigned long long)n * a.s_rn + (unsigned long long)(y - a.s_r0)) * a.map_pitch + xx] =
+          (MT)bucket_of<FAST>(pa, pb, pc, prm);
   }
 }
 

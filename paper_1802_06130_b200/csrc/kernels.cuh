@@ -68,8 +68,8 @@ struct StageArgs {
   LevelView z;         // z^l
   LevelView u1;        // u^{l+1} (unused when NC == 0)
   LevelView out;       // u^l (output rows [out_r0, out_r0 + out_rn))
-  const void* map;     // s^l, [N][map_rows][W] uint8 (uint16 when WIDE), row 0 = global row map_row0
-  int map_row0, map_rows;
+  const void* map;     // s^l, [N][map_rows][map_pitch] uint8 (uint16 when WIDE), row 0 = global row map_row0
+  int map_row0, map_rows, map_pitch;
   const float* bank;   // device bank of this stage: [phase][PS floats: K x S taps, padded]
   int K, S, PS;        // buckets, padded tap stride (odd), phase stride (multiple of 4)
   int n_phases;        // 1 or 4
@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
         const int yy = y0 + i * RS, xx = min(x + j, a.z.W - 1);
         int k = 0;
         if (row_ok[i])
-          k = static_cast<const MT*>(a.map)[(long long)n * a.map_rows * a.z.W + (long long)(yy - a.map_row0) * a.z.W + xx];
+          k = static_cast<const MT*>(a.map)[(long long)n * a.map_rows * a.map_pitch +
+                                            (long long)(yy - a.map_row0) * a.map_pitch + xx];
         int ps = 0;
         if (a.n_phases == 4) ps = RS == 2 ? j : 2 * (yy & 1) + j;
         tp[i][j] = bank + ps * a.PS + k * a.S;

@@ -121,7 +121,10 @@ def test_c4_full_size():
 # ------------------------------------------------------------------------- ragged / edge shapes
 
 @pytest.mark.parametrize("name,H,W,N", [("c1", 203, 333, 2), ("c1", 67, 129, 1), ("c2", 151, 97, 1),
-                                        ("c4", 77, 190, 1), ("c0", 45, 131, 3), ("c3", 130, 259, 2)])
+                                        ("c4", 77, 190, 1), ("c0", 45, 131, 3), ("c3", 130, 259, 2),
+                                        # widths 4 mod 16 / 8 mod 16: TMA stage with padded map rows
+                                        ("c1", 96, 392, 2), ("c4", 90, 200, 1), ("c2", 70, 500, 1),
+                                        ("c3", 64, 260, 2), ("c0", 40, 100, 2)])
 def test_ragged_shapes(name, H, W, N):
     cfg = _cfg_like(name, H, W, N)
     _full_parity(cfg, cfg.batch(), label=f"{name}@{H}x{W}")
@@ -449,6 +452,8 @@ def test_stage_kernel_selection():
     assert h.stage_kernel(64, 1080, 1920, 1) == ("k_stage_tma", 2)
     assert h.stage_kernel(1, 512, 512, 0) == ("k_stage_tma", 2)
     assert h.stage_kernel(1, 130, 259, 0)[0] == "k_stage"
+    assert h.stage_kernel(1, 130, 392, 0) == ("k_stage_tma", 2)  # W % 16 == 8: padded map rows
+    assert h.stage_kernel(1, 130, 260, 0)[0] == "k_stage"  # level 1 width 130: u^1 rows not 16-B
     assert _handle(bs.load_config("c2")).stage_kernel(1, 3000, 4000, 0)[0] == "k_stage_ph"
     assert _handle(bs.load_config("c4")).stage_kernel(1, 6000, 8000, 0)[0] == "k_stage_ph"
     from paper_1802_06130_b200.blade_ms import BladeError
