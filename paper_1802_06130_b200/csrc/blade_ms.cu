@@ -187,6 +187,7 @@ struct Plan {
   size_t ws_bytes = 0;
   std::vector<size_t> z32_off, zlo_off, u_off, map_off, fb_off;
   std::vector<int> map_pitch;  // entries per map row: W_l rounded up to 16 (16-B TMA rows)
+  std::vector<int> pitch;      // floats per workspace plane row at level l >= 1: W_l rounded up to 4
   std::vector<unsigned int> fb_cap;
   size_t fbcnt_off = 0;
 };
@@ -236,18 +237,22 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
   p.u_off.assign(L, 0);
   p.map_off.assign(L, 0);
   p.map_pitch.assign(L, 0);
-  for (int l = 0; l < L; ++l) p.map_pitch[l] = (p.W[l] + 15) & ~15;
+  p.pitch.assign(L, 0);
+  for (int l = 0; l < L; ++l) {
+    p.map_pitch[l] = (p.W[l] + 15) & ~15;
+    p.pitch[l] = l == 0 ? p.W[0] : (p.W[l] + 3) & ~3;  // 16-B rows: every level >= 1 is TMA-able
+  }
   for (int l = 1; l < L; ++l) {
     p.z32_off[l] = off;
-    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
+    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.pitch[l]);
   }
   for (int l = 1; l + 1 < L; ++l) {
     p.zlo_off[l] = off;
-    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.W[l]);
+    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.pitch[l]);
   }
   for (int l = 1; l + 1 < L; ++l) {
     p.u_off[l] = off;
-    off = align256(off + sizeof(float) * (size_t)N * 3 * p.u[l].n() * p.W[l]);
+    off = align256(off + sizeof(float) * (size_t)N * 3 * p.u[l].n() * p.pitch[l]);
   }
   const int nsel = L == 1 ? 1 : L - 1;
   for (int l = 0; l < nsel; ++l) {
@@ -268,14 +273,15 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
   p.ws_bytes = std::max<size_t>(off, 256);
 }
 
-LevelView make_view(float* base, int H, int W, Range r) {
+LevelView make_view(float* base, int H, int W, Range r, int pitch = 0) {
   LevelView v;
   v.p = base;
   v.H = H;
   v.W = W;
+  v.pitch = pitch > 0 ? pitch : W;
   v.row0 = r.lo;
   v.rows = r.n();
-  v.plane = (long long)r.n() * W;
+  v.plane = (long long)r.n() * v.pitch;
   v.frame = 3 * v.plane;
   return v;
 }
@@ -418,7 +424,10 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   for (int l = 1; l < L; ++l) {
     float* base = (levels_out && levels_out[l - 1]) ? levels_out[l - 1]
                                                     : reinterpret_cast<float*>(ws + p.z32_off[l]);
-    z32[l] = make_view(base, p.H[l], p.W[l], p.z[l]);
+    // caller-provided pyramid levels are dense (pitch W); the workspace's are padded (p.pitch);
+    // the lo plane shares the hi plane's pitch
+    const bool dense = levels_out && levels_out[l - 1];
+    z32[l] = make_view(base, p.H[l], p.W[l], p.z[l], dense ? p.W[l] : p.pitch[l]);
     if (l + 1 < L) zlo[l] = reinterpret_cast<float*>(ws + p.zlo_off[l]);
   }
   const int nsel = L == 1 ? 1 : L - 1;
@@ -445,7 +454,8 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.W = p.W[l];
     da.in_row0 = l == 0 ? in_view.row0 : p.z[l].lo;
     da.in_rows = l == 0 ? in_view.rows : p.z[l].n();
-    da.in_plane = (long long)da.in_rows * p.W[l];
+    da.in_pitch = l == 0 ? in_view.pitch : z32[l].pitch;
+    da.in_plane = (long long)da.in_rows * da.in_pitch;
     da.in_frame = 3 * da.in_plane;
     da.map = maps[l];
     da.map_pitch = mpitch[l];
@@ -455,6 +465,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.olo = (dec && l + 1 < L - 1) ? zlo[l + 1] : nullptr;
     da.H1 = dec ? p.H[l + 1] : 1;
     da.W1 = dec ? p.W[l + 1] : 1;
+    da.out_pitch = dec ? z32[l + 1].pitch : 1;
     da.d_buf_row0 = Z1.lo;
     da.d_buf_rows = Z1.n();
     da.d_r0 = Z1.lo;
@@ -507,22 +518,23 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     if (L > 1)
       u1 = (l + 1 == L - 1) ? z32[L - 1]
                             : make_view(reinterpret_cast<float*>(ws + p.u_off[l + 1]), p.H[l + 1], p.W[l + 1],
-                                        p.u[l + 1]);
+                                        p.u[l + 1], p.pitch[l + 1]);
     LevelView outv = (l == 0) ? out_view
-                              : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r);
+                              : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r, p.pitch[l]);
     const float* bank = h->d_bank + (size_t)l * h->cfg.n_filter_channels * h->cfg.n_phases * h->PS;
     const int y_base = r.lo & ~1;
     const int clamp = (l == 0 && h->cfg.clamp_output) ? 1 : 0;
     ProfScope ps(h, st, 2, l);
     // TMA path: needs 16-B aligned buffers whose row pitches are 16-B multiples
     const int map_es = h->K > 256 ? 2 : 1;
-    bool use_tma = h->has_tma && p.W[l] % 4 == 0 && (mpitch[l] * map_es) % 16 == 0 && aligned16(zl.p) &&
-                   aligned16(outv.p) && aligned16(maps[l]) &&
-                   (L == 1 || (p.W[l + 1] % 4 == 0 && aligned16(u1.p)));
+    bool use_tma = h->has_tma && zl.pitch % 4 == 0 && outv.pitch % 4 == 0 && (mpitch[l] * map_es) % 16 == 0 &&
+                   aligned16(zl.p) && aligned16(outv.p) && aligned16(maps[l]) &&
+                   (L == 1 || (u1.pitch % 4 == 0 && aligned16(u1.p)));
     CUtensorMap tmz, tmu, tmm;
     if (use_tma) {
       const TmaVariant& tv = h->tma;
-      use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb, tv.fr, 3) &&
+      use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb, tv.fr, 3,
+                          zl.pitch) &&
                 (h->K > 256 ? encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p.W[l], r.n(), N, tv.tcols,
                                         tv.trows, 1, mpitch[l])
                             : encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.W[l], r.n(), N, tv.tcols,
@@ -530,7 +542,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       if (use_tma) {
         if (L > 1)
           use_tma = encode_3d(&tmu, u1.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l + 1], u1.rows, N * 3, tv.ccb,
-                              tv.cr, 3);
+                              tv.cr, 3, u1.pitch);
         else
           tmu = tmz;
       }
@@ -566,6 +578,9 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
       a.tiles_y = (r.hi - y_base + tv.trows - 1) / tv.trows;
       a.n_tiles = N * a.tiles_x * a.tiles_y;
       a.clamp = clamp;
+      a.z_pitch = zl.pitch;
+      a.u_pitch = L > 1 ? u1.pitch : zl.pitch;
+      a.out_pitch = outv.pitch;
       if (tv.phase_split) {  // 4 phase-CTAs (x 3 channels) per tile group, 2 workers per CTA
         const int types = tv.ch3 ? 12 : 4;
         // one tile per worker group first: small levels spread over as many SMs as they have
@@ -1017,7 +1032,9 @@ blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W
   Plan p;
   plan_rows(h, std::max(N, 1), H, W, 0, H, p);
   const int L = p.L, l = level;
-  const bool tma = h->has_tma && p.W[l] % 4 == 0 && (L == 1 || p.W[l + 1] % 4 == 0);
+  // level 0 reads / writes the caller's dense buffers (pitch W); levels >= 1 and the coarse inputs
+  // live in the workspace with rows padded to 16 B
+  const bool tma = h->has_tma && (l > 0 || p.W[0] % 4 == 0);
   if (!tma) {
     *kind = 0;
     *rows_per_thread = 2;
@@ -1295,6 +1312,8 @@ blade_status blade_ms_train_accumulate(blade_ms_t h, int32_t level, const float*
   da.in_frame = 3 * da.in_plane;
   da.map = w + tp.map_off;
   da.map_pitch = W;
+  da.in_pitch = W;
+  da.out_pitch = 1;
   da.s_r0 = 0;
   da.s_rn = H;
   da.H1 = da.W1 = 1;

@@ -52,6 +52,7 @@ struct DownArgs {
   const float* zlo;  // level l lo plane (nullptr at l = 0)
   int H, W, in_row0, in_rows;
   long long in_plane, in_frame;
+  int in_pitch;      // floats per input row (>= W)
   void* map;         // s^l rows [s_r0, s_r0 + s_rn), pitch map_pitch (>= W; a multiple of 16 in
                      // the workspace so the stage can TMA it), frame stride s_rn * map_pitch;
                      // uint8 entries (K <= 256) or uint16 (WIDE, K <= 65536)
@@ -59,6 +60,7 @@ struct DownArgs {
   float* ohi;        // z^{l+1} hi: rows [d_buf_row0, + d_buf_rows), pitch W1 (nullptr: no dec)
   float* olo;        // z^{l+1} lo (nullptr: not needed, l + 1 is the coarsest level)
   int H1, W1, d_buf_row0, d_buf_rows, d_r0, d_rn;
+  int out_pitch;     // floats per z^{l+1} row (>= W1)
   int base, RB, n_strips, n_bands, n_tasks;
   unsigned long long* fb_list;  // uncertified map entries (flat index into map), capacity fb_cap
   unsigned int* fb_count;       // zeroed before the launch; may exceed fb_cap (overflow)
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
   const float* lbase = HILO ? a.zlo + (long long)n * a.in_frame : nullptr;
   const bool out_lane = lane >= LANE_LO && lane <= LANE_HI;
   // one 8-byte copy when the two columns are adjacent in memory and 8-B aligned (interior, W even)
-  const bool pair8 = fx1 == fx0 + 1 && ((fx0 | a.W | (int)(a.in_plane & 1)) & 1) == 0 &&
+  const bool pair8 = fx1 == fx0 + 1 && ((fx0 | a.in_pitch | (int)(a.in_plane & 1)) & 1) == 0 &&
                      ((reinterpret_cast<uintptr_t>(a.zhi) | reinterpret_cast<uintptr_t>(HILO ? a.zlo : a.zhi)) & 7) == 0;
   const bool all_pair8 = __all_sync(0xffffffffu, pair8);
 
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
     int br = fold_idx(r, a.H) - a.in_row0;
     br = min(max(br, 0), a.in_rows - 1);
     float* dst = ring + (i % RING) * NP * 64;
-    const long long ro = (long long)br * a.W;
+    const long long ro = (long long)br * a.in_pitch;
     if (all_pair8) {
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
   }
 
   MT* mapf = static_cast<MT*>(a.map) + (long long)n * a.s_rn * a.map_pitch;
-  const long long oframe = (long long)n * 3 * a.d_buf_rows * a.W1;
+  const long long oframe = (long long)n * 3 * a.d_buf_rows * a.out_pitch;
   const int Xd = x >> 1;  // decimated column (x even)
   // 2-byte map stores when every map row starts 2-B aligned (x is even)
   const bool map16 = (a.map_pitch & 1) == 0 && (reinterpret_cast<uintptr_t>(a.map) & (2 * sizeof(MT) - 1)) == 0;
@@ -404,13 +406,13 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
       if (!odd_r) {
         const int Yd = (r - 4) / 2;  // completed row (r even)
         if (out_lane && Yd >= a.d_r0 && Yd < a.d_r0 + a.d_rn && Xd < a.W1 && i >= 7) {
-          const long long o = oframe + (long long)(Yd - a.d_buf_row0) * a.W1 + Xd;
+          const long long o = oframe + (long long)(Yd - a.d_buf_row0) * a.out_pitch + Xd;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const double v = dacc[0][c];
             const float hi = (float)v;
-            a.ohi[o + (long long)c * a.d_buf_rows * a.W1] = hi;
-            if (a.olo) a.olo[o + (long long)c * a.d_buf_rows * a.W1] = (float)(v - (double)hi);
+            a.ohi[o + (long long)c * a.d_buf_rows * a.out_pitch] = hi;
+            if (a.olo) a.olo[o + (long long)c * a.d_buf_rows * a.out_pitch] = (float)(v - (double)hi);
           }
         }
 #pragma unroll
@@ -540,7 +542,7 @@ __global__ void __launch_bounds__(128) k_down_fixup(const DownArgs a, const Down
       auto Z = [&](int c, int yy, int xq) -> double {
         int br = fold_idx(yy, a.H) - a.in_row0;
         br = min(max(br, 0), a.in_rows - 1);
-        const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.W + fold_idx(xq, a.W);
+        const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.in_pitch + fold_idx(xq, a.W);
         double v = (double)a.zhi[o];
         if constexpr (HILO) v += (double)a.zlo[o];
         return v;

@@ -79,7 +79,7 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
             v = sfine[(c * SS::FR + ry) * SS::FCB + rx];
           } else {
             const int by = min(max(fy - a.z_row0, 0), a.z_rows - 1);
-            v = a.z[(((long long)n * 3 + c) * a.z_rows + by) * a.W + fx];
+            v = a.z[(((long long)n * 3 + c) * a.z_rows + by) * a.z_pitch + fx];
           }
           sfine[(c * SS::FR + r) * SS::FCB + q] = v;
         }
@@ -101,7 +101,7 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
             v = scoarse[(c * SS::CR + ry) * SS::CCB + rx];
           } else {
             const int by = min(max(fy - a.u_row0, 0), a.u_rows - 1);
-            v = a.u1[(((long long)n * 3 + c) * a.u_rows + by) * a.W1 + fx];
+            v = a.u1[(((long long)n * 3 + c) * a.u_rows + by) * a.u_pitch + fx];
           }
           scoarse[(c * SS::CR + r) * SS::CCB + q] = v;
         }
@@ -202,12 +202,12 @@ __device__ __forceinline__ void ph_tile(const StageTmaArgs& a, int n, int X0, in
     for (int j = 0; j < 2; ++j) {
       const int xx = X0 + PX + 4 * tx + 2 * j;
       if (xx >= a.W) continue;
-      float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.W + xx;
+      float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.out_pitch + xx;
 #pragma unroll
       for (int c = 0; c < PL; ++c) {
         float v = acc[i][j][c];
         if (a.clamp) v = fminf(fmaxf(v, 0.0f), 1.0f);
-        op[(long long)(CH3 ? chn : c) * a.out_rows * a.W] = v;
+        op[(long long)(CH3 ? chn : c) * a.out_rows * a.out_pitch] = v;
       }
     }
   }

@@ -218,6 +218,7 @@ struct StageTmaArgs {
   int tiles_x, tiles_y, n_tiles;
   int clamp;
   int u_rgb;           // CH3 (k_stage_ph): the coarse input is RGB z^{L-1}, not YCbCr planes
+  int z_pitch, u_pitch, out_pitch;  // floats per row of the z^l, u^{l+1} and output buffers
 };
 
 // G = 1: one 256-thread group, double-buffered tiles (TMA of tile i+1 overlaps tile i).
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
               v = sfine[(c * SS::FR + ry) * SS::FCB + rx];
             } else {
               const int by = min(max(fy - a.z_row0, 0), a.z_rows - 1);
-              v = a.z[(((long long)n * 3 + c) * a.z_rows + by) * a.W + fx];
+              v = a.z[(((long long)n * 3 + c) * a.z_rows + by) * a.z_pitch + fx];
             }
             sfine[(c * SS::FR + r) * SS::FCB + q] = v;
           }
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
                 v = scoarse[(c * SS::CR + ry) * SS::CCB + rx];
               } else {
                 const int by = min(max(fy - a.u_row0, 0), a.u_rows - 1);
-                v = a.u1[(((long long)n * 3 + c) * a.u_rows + by) * a.W1 + fx];
+                v = a.u1[(((long long)n * 3 + c) * a.u_rows + by) * a.u_pitch + fx];
               }
               scoarse[(c * SS::CR + r) * SS::CCB + q] = v;
             }
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
     for (int i = 0; i < RY; ++i) {
       const int yy = y + i;
       if (yy < a.o_r0 || yy >= a.o_r0 + a.o_rn || x >= a.W) continue;
-      float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.W + x;
+      float* op = a.out + ((long long)n * 3 * a.out_rows + (yy - a.out_row0)) * a.out_pitch + x;
 #pragma unroll
       for (int c = 0; c < PL; ++c) {
         float v0 = acc[i][0][c], v1 = acc[i][1][c], v2 = acc[i][2][c], v3 = acc[i][3][c];
@@ -480,7 +481,7 @@ __global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
           v2 = fminf(fmaxf(v2, 0.0f), 1.0f);
           v3 = fminf(fmaxf(v3, 0.0f), 1.0f);
         }
-        float* d = op + (long long)(CH3 ? chn : c) * a.out_rows * a.W;
+        float* d = op + (long long)(CH3 ? chn : c) * a.out_rows * a.out_pitch;
         if (x + 3 < a.W) {
           *reinterpret_cast<float4*>(d) = make_float4(v0, v1, v2, v3);  // W % 4 == 0 on this path
         } else {

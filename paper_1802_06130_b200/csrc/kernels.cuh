@@ -23,8 +23,9 @@ struct LevelView {
   float* p;         // frame 0, channel 0, buffer row 0
   int H, W;         // global level dims
   int row0, rows;   // the buffer holds global rows [row0, row0 + rows)
-  long long plane;  // floats per channel plane of the buffer (rows * W)
+  long long plane;  // floats per channel plane of the buffer (rows * pitch)
   long long frame;  // floats per frame of the buffer (3 * plane)
+  int pitch;        // floats per buffer row (>= W; padded to a multiple of 4 in the workspace)
 };
 
 // Programmatic dependent launch (sm_90+): the host launches every kernel of a cascade after the
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
       const float* zp = a.z.p + (long long)n * a.z.frame;
       for (int i = tid; i < SS::FR * SS::FC; i += SS::threads) {
         const int r = i / SS::FC, q = i - r * SS::FC;
-        const long long ro = (long long)view_row(a.z, Y0 - RF + r) * a.z.W + fold_idx(X0 - RF + q, a.z.W);
+        const long long ro = (long long)view_row(a.z, Y0 - RF + r) * a.z.pitch + fold_idx(X0 - RF + q, a.z.W);
         if constexpr (CH3) {
           sfine[r * SS::FCP + q] =
               rgb_to_ycc_ch(chn, __ldg(zp + ro), __ldg(zp + a.z.plane + ro), __ldg(zp + 2 * a.z.plane + ro));
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
       const int CY0 = Y0 / 2 - RC, CX0 = X0 / 2 - RC;
       for (int i = tid; i < SS::CR * SS::CC; i += SS::threads) {
         const int r = i / SS::CC, q = i - r * SS::CC;
-        const long long ro = (long long)view_row(a.u1, CY0 + r) * a.u1.W + fold_idx(CX0 + q, a.u1.W);
+        const long long ro = (long long)view_row(a.u1, CY0 + r) * a.u1.pitch + fold_idx(CX0 + q, a.u1.W);
         if constexpr (CH3) {
           scoarse[r * SS::CCP + q] =
               a.u_rgb ? rgb_to_ycc_ch(chn, __ldg(up + ro), __ldg(up + a.u1.plane + ro), __ldg(up + 2 * a.u1.plane + ro))
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       if (!row_ok[i]) continue;
-      const long long ro = (long long)(y0 + i * RS - a.out.row0) * a.out.W;
+      const long long ro = (long long)(y0 + i * RS - a.out.row0) * a.out.pitch;
 #pragma unroll
       for (int c = 0; c < PL; ++c) {
         float v0 = acc[i][0][c], v1 = acc[i][1][c];

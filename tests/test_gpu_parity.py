@@ -445,15 +445,17 @@ def test_forced_variants_subprocess(env):
 def test_stage_kernel_selection():
     """The variant each level runs (blade_ms_stage_kernel): the bench's c3 level 0 takes the
     4-row TMA kernel, its 7.5-tile-wide level 1 the 2-row one; 7x7 / 9x9 pairs the phase-split
-    kernel; ragged widths the generic kernel."""
+    kernel; a level-0 width that is not a multiple of 4 the generic kernel (levels >= 1 live in
+    the workspace with padded rows and always take TMA)."""
     c3 = bs.load_config("c3")
     h = _handle(c3)
     assert h.stage_kernel(64, 1080, 1920, 0) == ("k_stage_tma", 4)
     assert h.stage_kernel(64, 1080, 1920, 1) == ("k_stage_tma", 2)
     assert h.stage_kernel(1, 512, 512, 0) == ("k_stage_tma", 2)
-    assert h.stage_kernel(1, 130, 259, 0)[0] == "k_stage"
+    assert h.stage_kernel(1, 130, 259, 0)[0] == "k_stage"  # the caller's rows are not 16-B multiples
+    assert h.stage_kernel(1, 130, 259, 1) == ("k_stage_tma", 2)  # workspace levels are padded
     assert h.stage_kernel(1, 130, 392, 0) == ("k_stage_tma", 2)  # W % 16 == 8: padded map rows
-    assert h.stage_kernel(1, 130, 260, 0)[0] == "k_stage"  # level 1 width 130: u^1 rows not 16-B
+    assert h.stage_kernel(1, 130, 260, 0) == ("k_stage_tma", 2)  # level-1 width 130, padded to 132
     assert _handle(bs.load_config("c2")).stage_kernel(1, 3000, 4000, 0)[0] == "k_stage_ph"
     assert _handle(bs.load_config("c4")).stage_kernel(1, 6000, 8000, 0)[0] == "k_stage_ph"
     from paper_1802_06130_b200.blade_ms import BladeError
