@@ -188,6 +188,9 @@ struct Plan {
   std::vector<size_t> z32_off, zlo_off, u_off, map_off, fb_off;
   std::vector<int> map_pitch;  // entries per map row: W_l rounded up to 16 (16-B TMA rows)
   std::vector<int> pitch;      // floats per workspace plane row at level l >= 1: W_l rounded up to 4
+  size_t zcopy_off = 0;        // full-image calls with W % 4 != 0: a 16-B-row copy of the input
+  int zcopy_pitch = 0;         //   (written by k_down at level 0, read by the level-0 TMA stage)
+  size_t ocopy_off = 0;        //   and a 16-B-row staging buffer for the level-0 output
   std::vector<unsigned int> fb_cap;
   size_t fbcnt_off = 0;
 };
@@ -258,6 +261,14 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
   for (int l = 0; l < nsel; ++l) {
     p.map_off[l] = off;
     off = align256(off + (size_t)map_es * N * p.u[l].n() * p.map_pitch[l]);
+  }
+  p.zcopy_pitch = 0;
+  if (W % 4 != 0 && o0 == 0 && on == H) {  // full image whose rows the TMA engine cannot address
+    p.zcopy_pitch = (W + 3) & ~3;
+    p.zcopy_off = off;
+    off = align256(off + sizeof(float) * (size_t)N * 3 * H * p.zcopy_pitch);
+    p.ocopy_off = off;
+    off = align256(off + sizeof(float) * (size_t)N * 3 * H * p.zcopy_pitch);
   }
   // uncertified-pixel lists of the fp32 selector (DESIGN.md §6 H1): 1/64 of each level's map
   p.fb_off.assign(nsel, 0);
@@ -498,11 +509,14 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.fb_count = fb_cnt + l;
     da.fb_cap = p.fb_cap[l];
     da.N = N;
+    const bool zcopy = l == 0 && run_stages && h->has_tma && p.zcopy_pitch > 0;
+    da.zcopy = zcopy ? reinterpret_cast<float*>(ws + p.zcopy_off) : nullptr;
+    da.copy_pitch = zcopy ? p.zcopy_pitch : 0;
     ProfScope ps(h, st, 1, l);
     const bool hilo = l > 0;
     const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
     const bool wide = h->K > 256;
-    auto fn = down_kernel(hilo, dec, fast, wide);
+    auto fn = down_kernel(hilo, dec, fast, wide, zcopy);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
     auto fx = fixup_kernel(hilo, fast, wide);
@@ -514,6 +528,8 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   for (int l = nsel - 1; l >= 0; --l) {
     const Range r = p.u[l];
     LevelView zl = z32[l];
+    if (l == 0 && h->has_tma && p.zcopy_pitch > 0)  // the input copy k_down wrote (16-B rows)
+      zl = make_view(reinterpret_cast<float*>(ws + p.zcopy_off), p.H[0], p.W[0], Range{0, p.H[0]}, p.zcopy_pitch);
     LevelView u1{};
     if (L > 1)
       u1 = (l + 1 == L - 1) ? z32[L - 1]
@@ -521,6 +537,15 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
                                         p.u[l + 1], p.pitch[l + 1]);
     LevelView outv = (l == 0) ? out_view
                               : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r, p.pitch[l]);
+    const bool ostage = l == 0 && h->has_tma && p.zcopy_pitch > 0;  // level-0 output via 16-B rows
+    if (ostage)
+      outv = make_view(reinterpret_cast<float*>(ws + p.ocopy_off), p.H[0], p.W[0], Range{0, p.H[0]}, p.zcopy_pitch);
+    auto copy_out = [&]() {  // staged level-0 output -> the caller's dense rows
+      const long long total = (long long)N * 3 * p.H[0] * p.W[0];
+      const unsigned g = (unsigned)std::min<long long>((total + 255) / 256, 8LL * h->num_sms);
+      return launch(k_copy_rows<>, g, 256, 0, st, true, out_view.p, out_view.pitch,
+                    static_cast<const float*>(outv.p), outv.pitch, (long long)N * 3, p.H[0], p.W[0]);
+    };
     const float* bank = h->d_bank + (size_t)l * h->cfg.n_filter_channels * h->cfg.n_phases * h->PS;
     const int y_base = r.lo & ~1;
     const int clamp = (l == 0 && h->cfg.clamp_output) ? 1 : 0;
@@ -599,13 +624,14 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
         LAUNCH("k_stage_tma", launch(tv.fn, grid, dim3(32, tv.by * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
       }
       if (tv.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
-        const long long per_frame = (long long)r.n() * p.W[0];
+        const long long per_frame = (long long)r.n() * outv.pitch;
         const long long total = (long long)N * per_frame;
         const unsigned g2 = (unsigned)std::min<long long>((total + 255) / 256, 8LL * h->num_sms);
         LAUNCH("k_ycc_to_rgb", launch(k_ycc_to_rgb<>, g2, 256, 0, st, true,
-                                      outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane, outv.frame,
+                                      outv.p + (long long)(r.lo - outv.row0) * outv.pitch, outv.plane, outv.frame,
                                       per_frame, N, h->cfg.clamp_output));
       }
+      if (ostage) LAUNCH("k_copy_rows", copy_out());
       continue;
     }
     StageArgs a{};
@@ -637,13 +663,14 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     if (h->stage.ch3) a.clamp = 0;  // clamped after the colour conversion
     LAUNCH("k_stage", launch(h->stage.fn, (unsigned)grid, dim3(32, h->stage.by), h->stage_smem, st, true, a));
     if (h->stage.ch3 && l == 0) {  // u^0 is YCbCr planes: back to RGB in place (+ final clamp)
-      const long long per_frame = (long long)r.n() * p.W[0];
+      const long long per_frame = (long long)r.n() * outv.pitch;
       const long long total = (long long)N * per_frame;
       const unsigned g2 = (unsigned)std::min<long long>((total + 255) / 256, 8LL * h->num_sms);
       LAUNCH("k_ycc_to_rgb", launch(k_ycc_to_rgb<>, g2, 256, 0, st, true,
-                                    outv.p + (long long)(r.lo - outv.row0) * outv.W, outv.plane, outv.frame,
+                                    outv.p + (long long)(r.lo - outv.row0) * outv.pitch, outv.plane, outv.frame,
                                     per_frame, N, h->cfg.clamp_output));
     }
+    if (ostage) LAUNCH("k_copy_rows", copy_out());
   }
   return BLADE_OK;
 }
@@ -901,7 +928,8 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl)
       for (int dc = 0; dc < 2 && ce == cudaSuccess; ++dc)
         for (int sm = 0; sm < 3 && ce == cudaSuccess; ++sm)
-          ce = cudaFuncSetAttribute(down_kernel(hl, dc, sm == 1, sm == 2), cudaFuncAttributeMaxDynamicSharedMemorySize,
+          for (int cp = 0; cp < 2 && ce == cudaSuccess; ++cp)
+            ce = cudaFuncSetAttribute(down_kernel(hl, dc, sm == 1, sm == 2, cp && !hl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)down_smem(hl));
   }
   for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl) {
@@ -1016,10 +1044,11 @@ blade_status blade_ms_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t
 blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t* count) {
   if (!h || !count) return fail(BLADE_EINVAL, "NULL argument");
   (void)H;
-  (void)W;
   const int L = h->cfg.levels;
   // k_down + k_down_fixup + k_stage per stage level (+ the YCbCr -> RGB conversion with per-channel banks)
-  *count = N == 0 ? 0 : 3 * (L == 1 ? 1 : L - 1) + (h->cfg.n_filter_channels == 3 ? 1 : 0);
+  *count = N == 0 ? 0
+                  : 3 * (L == 1 ? 1 : L - 1) + (h->cfg.n_filter_channels == 3 ? 1 : 0) +
+                        (h->has_tma && W % 4 != 0 ? 1 : 0);  // level-0 output staged for 16-B rows
   return BLADE_OK;
 }
 
@@ -1034,7 +1063,7 @@ blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W
   const int L = p.L, l = level;
   // level 0 reads / writes the caller's dense buffers (pitch W); levels >= 1 and the coarse inputs
   // live in the workspace with rows padded to 16 B
-  const bool tma = h->has_tma && (l > 0 || p.W[0] % 4 == 0);
+  const bool tma = h->has_tma;  // level 0 with W % 4 != 0 reads k_down's 16-B-row input copy
   if (!tma) {
     *kind = 0;
     *rows_per_thread = 2;

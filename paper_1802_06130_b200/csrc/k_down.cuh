@@ -66,6 +66,8 @@ struct DownArgs {
   unsigned int* fb_count;       // zeroed before the launch; may exceed fb_cap (overflow)
   unsigned int fb_cap;
   int N;                        // frames of the launch
+  float* zcopy;                 // level 0 only (nullptr: off): a copy of the input rows with row pitch
+  int copy_pitch;               // copy_pitch (a multiple of 4) for the TMA stage, [N][3][H][copy_pitch]
 };
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
@@ -253,7 +255,9 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
 }
 
 // grid: ceil(n_tasks / WARPS) CTAs of 32 * WARPS threads; task = (frame, band, strip), strip fastest.
-template <bool HILO, bool DEC, bool FAST, bool WIDE>
+// COPY (level 0 only): also write the input rows into a.zcopy (16-B row pitch) for the TMA stage
+// when the caller's rows are not 16-B multiples.
+template <bool HILO, bool DEC, bool FAST, bool WIDE, bool COPY = false>
 __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const DownArgs a, const DownParams prm) {
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;  // bucket map entry
   using namespace down;
@@ -372,6 +376,15 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
       }
     }
     const int r = Yb - 3 + i;
+    if (COPY && out_lane && r >= Yb && r < Yb + a.RB && r < a.H && x < a.W) {
+      // the band's own rows, the strip's own columns: every input sample is written exactly once
+      float* cp = a.zcopy + ((long long)n * 3 * a.H + r) * a.copy_pitch + x;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        cp[(long long)c * a.H * a.copy_pitch] = hn[c][0];
+        if (x + 1 < a.W) cp[(long long)c * a.H * a.copy_pitch + 1] = hn[c][1];
+      }
+    }
 
     if constexpr (DEC) {
       // ---- decimation (fp64): horizontal 8 taps at column Xd of row r, then the vertical ring

@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
         }
         float* d = op + (long long)(CH3 ? chn : c) * a.out_rows * a.out_pitch;
         if (x + 3 < a.W) {
-          *reinterpret_cast<float4*>(d) = make_float4(v0, v1, v2, v3);  // W % 4 == 0 on this path
+          *reinterpret_cast<float4*>(d) = make_float4(v0, v1, v2, v3);  // output rows are 16-B multiples
         } else {
           d[0] = v0;
           if (x + 1 < a.W) d[1] = v1;

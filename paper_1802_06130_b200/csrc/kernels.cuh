@@ -308,6 +308,23 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
   }
 }
 
+// Plane-by-plane row copy between pitches: dst[p][y][x] = src[p][y][x], x < W, for `planes`
+// planes of H rows (the level-0 output of a full image whose rows are not 16-B multiples is
+// staged in the workspace with 16-B rows for the TMA stage kernel, then copied out).
+template <int = 0>
+__global__ void k_copy_rows(float* dst, int dst_pitch, const float* src, int src_pitch, long long planes, int H,
+                            int W) {
+  pdl_trigger();
+  pdl_wait();
+  const long long total = planes * H * (long long)W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / W;
+    const int x = (int)(i - row * W);
+    dst[row * dst_pitch + x] = src[row * src_pitch + x];
+  }
+}
+
 // YCbCr -> RGB in place over rows [0, rows) of a level view (exact inverse of rgb_to_ycc_ch up
 // to fp32 rounding; R25), with the optional final clamp.
 template <int = 0>

@@ -4,13 +4,14 @@
 namespace blade {
 namespace tables {
 template <bool FAST, bool WIDE>
-static DownKernel down_kernel_t(bool hilo, bool dec) {
+static DownKernel down_kernel_t(bool hilo, bool dec, bool copy) {
   if (hilo) return dec ? &k_down<true, true, FAST, WIDE> : &k_down<true, false, FAST, WIDE>;
+  if (copy) return dec ? &k_down<false, true, FAST, WIDE, true> : &k_down<false, false, FAST, WIDE, true>;
   return dec ? &k_down<false, true, FAST, WIDE> : &k_down<false, false, FAST, WIDE>;
 }
-DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide) {
-  if (wide) return down_kernel_t<false, true>(hilo, dec);  // FAST implies K = 144
-  return fast ? down_kernel_t<true, false>(hilo, dec) : down_kernel_t<false, false>(hilo, dec);
+DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy) {
+  if (wide) return down_kernel_t<false, true>(hilo, dec, copy);  // FAST implies K = 144
+  return fast ? down_kernel_t<true, false>(hilo, dec, copy) : down_kernel_t<false, false>(hilo, dec, copy);
 }
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide) {
   if (wide) return hilo ? &k_down_fixup<true, false, true> : &k_down_fixup<false, false, true>;

@@ -43,7 +43,7 @@ const std::vector<TmaVariant>& ph_variants();
 using DownKernel = void (*)(const DownArgs, const DownParams);
 // FAST: the configs' bucket layout (16 orientations x 3 strength x 3 coherence bins)
 // wide: uint16 bucket maps (K > 256, NEXT f2)
-DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide);
+DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy = false);
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide);
 
 // Training (NEXT f4): segmented fp64 SYRK of the normal equations.
