@@ -1533,7 +1533,11 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
   DeviceGuard guard(h->device);
   cudaStream_t st = (cudaStream_t)stream;
   // chunked frame pipeline: H2D (chunk i+1) || compute (chunk i) || D2H (chunk i-1)
-  const int nchunks = std::min<int>(N, 16);
+  static const int max_chunks = [] {  // BLADE_E2E_CHUNKS overrides (A/B timing: 16 / 32 / 64 chunks
+    const char* e = getenv("BLADE_E2E_CHUNKS");  // of a c3 batch: 34.8 / 34.6 / 35.9 ms, PCIe bound 31.7)
+    return e ? std::max(1, atoi(e)) : 32;
+  }();
+  const int nchunks = std::min<int>(N, max_chunks);
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> ev_in(nchunks, nullptr), ev_done(nchunks, nullptr);
   cudaEvent_t ev_start = nullptr;

@@ -23,3 +23,17 @@ def both():
 t_both = timed(both)
 print(f"H2D {gb / t_h2d:.1f} GB/s, D2H {gb / t_d2h:.1f} GB/s, concurrent H2D+D2H {2 * gb / t_both:.1f} GB/s "
       f"({t_both * 1e3:.1f} ms for {gb:.2f} GB each way)")
+
+# several copy streams per direction (one DMA engine per stream may not fill PCIe Gen5)
+for k in (2, 4):
+    ss = [torch.cuda.Stream() for _ in range(2 * k)]
+    step = n // k
+
+    def split():
+        for i in range(k):
+            with torch.cuda.stream(ss[i]):
+                d_a[i * step:(i + 1) * step].copy_(h_in[i * step:(i + 1) * step], non_blocking=True)
+            with torch.cuda.stream(ss[k + i]):
+                h_out[i * step:(i + 1) * step].copy_(d_b[i * step:(i + 1) * step], non_blocking=True)
+    t_k = timed(split)
+    print(f"{k} streams per direction: concurrent {2 * gb / t_k:.1f} GB/s ({t_k * 1e3:.1f} ms)")
