@@ -114,8 +114,10 @@ blade_status blade_ms_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t
  * Denoise a batch: in, out DEVICE fp32 [N][3][H][W] on the handle's device; N >= 0 (0 is a
  * no-op), H, W >= 1. `out` must not overlap `in` (EINVAL). workspace: device, >= the size
  * from blade_ms_workspace_size (ESHAPE otherwise), 16-byte aligned; on return it holds the
- * pyramid levels (fp32 and fp64 copies), intermediate stage outputs and bucket maps.
- * Output equals a per-frame loop bit-exactly.
+ * pyramid levels (fp32 hi / lo pairs carrying the fp64 decimation), intermediate stage outputs
+ * and bucket maps, with rows padded to 16-byte multiples (so every level can be read by TMA;
+ * a level-0 width that is not a multiple of 4 adds a padded copy of the input and a padded
+ * staging output). Output equals a per-frame loop bit-exactly.
  */
 blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t N, int32_t H,
                               int32_t W, void* workspace, size_t ws_bytes, void* cuda_stream);
@@ -238,7 +240,8 @@ typedef struct {
   int32_t device;
   size_t bank_bytes_device;    /* device copy of the relaid bank                          */
   size_t stage_smem_bytes;     /* dynamic shared memory of the stage kernel (K3)          */
-  int32_t stage_phase_groups;  /* 1: a CTA holds all phases; 2: CTAs specialised by row parity */
+  int32_t stage_phase_groups;  /* 1: a CTA holds all phases (TMA kernels; the phase-split kernel
+                                  holds one); 2: generic kernel, CTAs specialised by row parity */
 } blade_ms_info;
 blade_status blade_ms_get_info(blade_ms_t h, blade_ms_info* info);
 
