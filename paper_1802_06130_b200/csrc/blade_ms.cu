@@ -490,13 +490,19 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     // should end with a sliver of a wave
     const long long col_tasks = (long long)N * da.n_strips;
     const double slots = (double)h->down_slots[l > 0 ? 1 : 0];
-    int RB = 128;
+    // bands taller than 128 rows lose on c3 despite the model (1 wave of 1088-row tasks: k_down0
+    // 1.28 -> 1.38 ms): a single wave cannot rebalance uneven SMs
+    static const int rb_max = [] {  // BLADE_DOWN_RBMAX overrides the tallest band (A/B timing)
+      const char* e = getenv("BLADE_DOWN_RBMAX");
+      return e ? std::max(4, atoi(e)) & ~1 : 128;
+    }();
+    int RB = rb_max;
     double best = 0.0;
-    for (int rb = 128; rb >= 4; rb -= 2) {
+    for (int rb = rb_max; rb >= 4; rb -= 2) {
       const double tasks = (double)col_tasks * (double)((span + rb - 1) / rb);
       const double w = tasks / slots;
       const double cost = (rb + 6) * std::ceil(w);
-      if (rb == 128 || cost < best) {
+      if (rb == rb_max || cost < best) {
         best = cost;
         RB = rb;
       }
