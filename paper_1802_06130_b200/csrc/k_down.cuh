@@ -287,10 +287,18 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
                      ((reinterpret_cast<uintptr_t>(a.zhi) | reinterpret_cast<uintptr_t>(HILO ? a.zlo : a.zhi)) & 7) == 0;
   const bool all_pair8 = __all_sync(0xffffffffu, pair8);
 
+  // interior task: every input row it streams lies inside the image and the buffer (no fold)
+  const bool interior = Yb - 3 >= 0 && Yb - 3 + nrows <= a.H && Yb - 3 >= a.in_row0 &&
+                        Yb - 3 + nrows <= a.in_row0 + a.in_rows;
   auto issue = [&](int i) {
     const int r = Yb - 3 + i;
-    int br = fold_idx(r, a.H) - a.in_row0;
-    br = min(max(br, 0), a.in_rows - 1);
+    int br;
+    if (interior) {
+      br = r - a.in_row0;
+    } else {
+      br = fold_idx(r, a.H) - a.in_row0;
+      br = min(max(br, 0), a.in_rows - 1);
+    }
     float* dst = ring + (i % RING) * NP * 64;
     const long long ro = (long long)br * a.in_pitch;
     if (all_pair8) {
