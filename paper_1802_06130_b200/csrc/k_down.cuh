@@ -349,13 +349,16 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
   }
 
   MT* mapf = static_cast<MT*>(a.map) + (long long)n * a.s_rn * a.map_pitch;
-  const long long oframe = (long long)n * 3 * a.d_buf_rows * a.out_pitch;
+  const long long ostride = (long long)a.d_buf_rows * a.out_pitch;  // channel plane of z^{l+1}
+  const long long oframe = 3 * (long long)n * ostride;
   const int Xd = x >> 1;  // decimated column (x even)
   // 2-byte map stores when every map row starts 2-B aligned (x is even)
   const bool map16 = (a.map_pitch & 1) == 0 && (reinterpret_cast<uintptr_t>(a.map) & (2 * sizeof(MT) - 1)) == 0;
 
+  // map entry of this lane for the window row completing at iteration i (y = Yb - 6 + i)
+  MT* mrow_i = mapf + (long long)(Yb - 6 - a.s_r0) * a.map_pitch + x;
 #pragma unroll 2
-  for (int i = 0; i < nrows; ++i) {
+  for (int i = 0; i < nrows; ++i, mrow_i += a.map_pitch) {
     if (i + RING - 1 < nrows) issue(i + RING - 1);
     cp_async_commit();
     cp_async_wait<RING - 1>();
@@ -432,8 +435,8 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
           for (int c = 0; c < 3; ++c) {
             const double v = dacc[0][c];
             const float hi = (float)v;
-            a.ohi[o + (long long)c * a.d_buf_rows * a.out_pitch] = hi;
-            if (a.olo) a.olo[o + (long long)c * a.d_buf_rows * a.out_pitch] = (float)(v - (double)hi);
+            a.ohi[o + c * ostride] = hi;
+            if (a.olo) a.olo[o + c * ostride] = (float)(v - (double)hi);
           }
         }
 #pragma unroll
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
         }
       }
       if (emit && x < a.W) {
-        MT* mrow = mapf + (long long)(y - a.s_r0) * a.map_pitch + x;
+        MT* mrow = mrow_i;
         if (map16 && x + 1 < a.W) {  // both entries in one store
           if constexpr (WIDE)
             *reinterpret_cast<uint32_t*>(mrow) = (uint32_t)bk[0] | ((uint32_t)bk[1] << 16);
