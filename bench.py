@@ -486,7 +486,7 @@ def main():
     step_work = algorithmic_work(cfg, n_local) if shard.mode == "frames" else work
     step_bytes = sum(v["bytes"] for v in step_work.values())
     hbm_ach = step_bytes / (ms_per_step / 1e3) / 1e9  # per GPU
-    names = {"selector": "k_down", "stage": "k_stage", "decimate": "k_decimate"}
+    names = {"selector": "k_down", "stage": "k_stage", "decimate": "k_decimate", "fixup": "k_down_fixup"}
     breakdown = {f"{names.get(k[0], k[0])}{k[1]}": round(t, 4) for k, (t, c) in sorted(kern.items())}
 
     # ---- CPU baseline (rank 0, N=1 only)

@@ -258,13 +258,15 @@ blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W
 /*
  * Per-kernel timing (measurement support for bench.py). While enabled, every launch the handle
  * enqueues is bracketed by two CUDA events recorded on the launching stream. blade_ms_profile_read
- * synchronises on those events and returns, per kernel kind (0 = K1 decimate, 1 = K2 selector,
- * 2 = K3 stage) and level l (< 16), the summed milliseconds ms[kind * 16 + l] and the launch count
+ * synchronises on those events and returns, per kernel kind (0 = K1 decimate (fused into the
+ * selector: unused), 1 = K2 selector (k_down, fused decimation), 2 = K3 stage, 3 = the merged fp64
+ * fix-up of all levels, level 0) and level l (< 16), the summed milliseconds ms[kind * 16 + l] and
+ * the launch count
  * count[kind * 16 + l] since the last read, then clears the records. Enabling profiling makes the
  * handle stateful: do not enqueue from several threads while it is on.
  */
 blade_status blade_ms_set_profiling(blade_ms_t h, int32_t enable);
-blade_status blade_ms_profile_read(blade_ms_t h, double* ms /* [48] */, int32_t* count /* [48] */);
+blade_status blade_ms_profile_read(blade_ms_t h, double* ms /* [64] */, int32_t* count /* [64] */);
 
 /* Release the handle and its device bank. NULL is a no-op. */
 blade_status blade_ms_destroy(blade_ms_t h);

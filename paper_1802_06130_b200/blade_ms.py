@@ -268,15 +268,15 @@ class BladeMS:
     def set_profiling(self, enable: bool):
         _check(lib().blade_ms_set_profiling(self._h, int(enable)))
 
-    KINDS = ("decimate", "selector", "stage")
+    KINDS = ("decimate", "selector", "stage", "fixup")
 
     def profile_read(self) -> dict:
         """{(kind, level): (total_ms, launches)} since the last read (synchronises)."""
-        ms = np.zeros(48, np.float64)
-        cnt = np.zeros(48, np.int32)
+        ms = np.zeros(64, np.float64)
+        cnt = np.zeros(64, np.int32)
         _check(lib().blade_ms_profile_read(self._h, ms.ctypes.data, cnt.ctypes.data))
         return {(self.KINDS[i // 16], i % 16): (float(ms[i]), int(cnt[i]))
-                for i in range(48) if cnt[i]}
+                for i in range(64) if cnt[i]}
 
     def workspace(self, N: int, H: int, W: int) -> torch.Tensor:
         return torch.empty(self.workspace_size(N, H, W), dtype=torch.uint8,

@@ -387,6 +387,10 @@ bool use_ry4(const blade_ms* h, int N, int W, int span) {
   return tiles_x >= 12 && tiles >= 8LL * h->num_sms;
 }
 
+// The fp64 fix-ups of all selector levels run as one launch after the down pass on small calls
+// (launch-latency-bound: c1 -7 us per call), per level right after each k_down otherwise.
+bool fixups_merged(int nsel, long long N, long long H, long long W) { return nsel > 1 && N * H * W <= (4LL << 20); }
+
 // Kernel launch; with `pdl` the launch allows programmatic stream serialisation (PDL): the grid
 // may be scheduled while the previous kernel in the stream drains, and its kernels call pdl_wait()
 // before reading that kernel's outputs (kernels.cuh). BLADE_PDL=0 turns it off (A/B timing).
@@ -451,6 +455,8 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   // ---- down pass: k_down(l) -> s^l, z^{l+1} (hi, and lo when level l+1 feeds a selector);
   //      k_down_fixup(l) recomputes the (rare) pixels whose fp32 orientation is uncertified
   unsigned int* fb_cnt = reinterpret_cast<unsigned int*>(ws + p.fbcnt_off);
+  std::vector<DownArgs> fix_args;  // per level, for the merged fix-up launch
+  const bool merge_fix = fixups_merged(L == 1 ? 1 : L - 1, N, p.H[0], p.W[0]);
   CUDA_TRY(cudaMemsetAsync(fb_cnt, 0, sizeof(unsigned int) * nsel, st));
   for (int l = 0; l < nsel; ++l) {
     const Range U = p.u[l];
@@ -525,8 +531,30 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     auto fn = down_kernel(hilo, dec, fast, wide, zcopy);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
-    auto fx = fixup_kernel(hilo, fast, wide);
-    LAUNCH("k_down_fixup", launch(fx, 8 * h->num_sms, 128, 0, st, true, da, h->down[l]));
+    if (merge_fix) {
+      fix_args.push_back(da);
+    } else {
+      auto fx = fixup_kernel(hilo, fast, wide);
+      LAUNCH("k_down_fixup", launch(fx, 8 * h->num_sms, 128, 0, st, true, da, h->down[l]));
+    }
+  }
+  // ---- small (launch-latency-bound) calls: the fix-ups of every level in one launch per
+  //      kFixMax levels after the down pass (the stages need them, the next k_down does not; on
+  //      large batches the per-level fix-up right after its k_down is faster: 22 vs 70 us on c3)
+  if (merge_fix) {
+    const int l = nsel - 1;  // (LAUNCH's error message)
+    const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
+    ProfScope ps(h, st, 3, 0);  // kind 3: the merged fix-up
+    for (int l0 = 0; l0 < nsel; l0 += kFixMax) {
+      FixupMulti fm{};
+      fm.n = std::min(kFixMax, nsel - l0);
+      for (int q = 0; q < fm.n; ++q) {
+        fm.a[q] = fix_args[l0 + q];
+        fm.prm[q] = h->down[l0 + q];
+      }
+      LAUNCH("k_down_fixup_multi",
+             launch(fixup_multi_kernel(fast, h->K > 256), 8 * h->num_sms, 128, 0, st, true, fm));
+    }
   }
   if (!run_stages) return BLADE_OK;
 
@@ -976,7 +1004,7 @@ blade_status blade_ms_set_profiling(blade_ms_t h, int32_t enable) {
 blade_status blade_ms_profile_read(blade_ms_t h, double* ms, int32_t* count) {
   if (!h || !ms || !count) return fail(BLADE_EINVAL, "NULL argument");
   DeviceGuard guard(h->device);
-  for (int i = 0; i < 48; ++i) {
+  for (int i = 0; i < 64; ++i) {
     ms[i] = 0.0;
     count[i] = 0;
   }
@@ -1049,12 +1077,13 @@ blade_status blade_ms_workspace_size(blade_ms_t h, int32_t N, int32_t H, int32_t
 
 blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t* count) {
   if (!h || !count) return fail(BLADE_EINVAL, "NULL argument");
-  (void)H;
   const int L = h->cfg.levels;
-  // k_down + k_down_fixup + k_stage per stage level (+ the YCbCr -> RGB conversion with per-channel banks)
+  // k_down + k_stage per stage level, one merged fix-up per kFixMax levels (+ the YCbCr -> RGB
+  // conversion with per-channel banks, + the copy-out of a staged level-0 output)
+  const int nsel = L == 1 ? 1 : L - 1;
   *count = N == 0 ? 0
-                  : 3 * (L == 1 ? 1 : L - 1) + (h->cfg.n_filter_channels == 3 ? 1 : 0) +
-                        (h->has_tma && W % 4 != 0 ? 1 : 0);  // level-0 output staged for 16-B rows
+                  : 2 * nsel + (fixups_merged(nsel, N, H, W) ? (nsel + kFixMax - 1) / kFixMax : nsel) +
+                        (h->cfg.n_filter_channels == 3 ? 1 : 0) + (h->has_tma && W % 4 != 0 ? 1 : 0);
   return BLADE_OK;
 }
 

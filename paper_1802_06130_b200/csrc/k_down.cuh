@@ -597,4 +597,109 @@ __global__ void __launch_bounds__(128) k_down_fixup(const DownArgs a, const Down
   }
 }
 
+// All selector levels' fix-ups of one cascade in ONE launch (up to kFixMax levels): the lists
+// are only needed by the stages, which run after every k_down, so the per-level fix-up launches
+// merge into one after the down pass (one launch instead of L-1; c1: -7 us of 64).
+constexpr int kFixMax = 4;
+struct FixupMulti {
+  DownArgs a[kFixMax];
+  DownParams prm[kFixMax];
+  int n;  // levels in use
+};
+
+// The fields of one level a fix-up needs, read once per pixel from the (dynamically indexed)
+// kernel parameters into registers.
+struct FixLevel {
+  const float* zhi;
+  const float* zlo;
+  void* map;
+  const unsigned long long* fb_list;
+  long long in_frame, in_plane;
+  int H, W, in_row0, in_rows, in_pitch, s_r0, s_rn, map_pitch;
+  __device__ __forceinline__ explicit FixLevel(const DownArgs& a)
+      : zhi(a.zhi), zlo(a.zlo), map(a.map), fb_list(a.fb_list), in_frame(a.in_frame), in_plane(a.in_plane),
+        H(a.H), W(a.W), in_row0(a.in_row0), in_rows(a.in_rows), in_pitch(a.in_pitch), s_r0(a.s_r0), s_rn(a.s_rn),
+        map_pitch(a.map_pitch) {}
+};
+
+template <bool FAST, bool WIDE>
+__device__ __forceinline__ void fixup_pixel(const FixLevel& a, const DownParams& prm, unsigned long long i,
+                                            bool all, int lane) {
+  using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;
+  const unsigned long long per_frame = (unsigned long long)a.s_rn * a.W;
+  const unsigned long long e = all ? i : a.fb_list[i];
+  const int n = (int)(e / per_frame);
+  const unsigned long long r = e - (unsigned long long)n * per_frame;
+  const int y = a.s_r0 + (int)(r / a.W), xx = (int)(r % a.W);
+  const bool hilo = a.zlo != nullptr;
+  double pa = 0.0, pb = 0.0, pc = 0.0;
+  if (lane < 25) {
+    const int dy = lane / 5 - 2, dx = lane % 5 - 2;
+    auto Z = [&](int c, int yy, int xq) -> double {
+      int br = fold_idx(yy, a.H) - a.in_row0;
+      br = min(max(br, 0), a.in_rows - 1);
+      const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.in_pitch + fold_idx(xq, a.W);
+      double v = (double)a.zhi[o];
+      if (hilo) v += (double)a.zlo[o];
+      return v;
+    };
+    const int yy = y + dy, xq = xx + dx;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double gx = Z(c, yy, xq + 1) - Z(c, yy, xq - 1);
+      const double gy = Z(c, yy + 1, xq) - Z(c, yy - 1, xq);
+      pa = fma(gx, gx, pa);
+      pb = fma(gx, gy, pb);
+      pc = fma(gy, gy, pc);
+    }
+    const double wgt = prm.wp[dy + 2] * prm.wp[dx + 2];
+    pa *= wgt;
+    pb *= wgt;
+    pc *= wgt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pa += __shfl_xor_sync(0xffffffffu, pa, o);
+    pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  }
+  if (lane == 0)
+    static_cast<MT*>(a.map)[((unsigned long long)n * a.s_rn + (unsigned long long)(y - a.s_r0)) * a.map_pitch + xx] =
+        (MT)bucket_of<FAST>(pa, pb, pc, prm);
+}
+
+template <bool FAST, bool WIDE>
+__global__ void __launch_bounds__(128) k_down_fixup_multi(const __grid_constant__ FixupMulti m) {
+  pdl_trigger();
+  pdl_wait();
+  unsigned long long items[kFixMax];
+  bool all[kFixMax];
+  unsigned long long total = 0;
+#pragma unroll
+  for (int l = 0; l < kFixMax; ++l) {
+    items[l] = 0;
+    all[l] = false;
+    if (l < m.n) {
+      const unsigned int cnt = *m.a[l].fb_count;
+      all[l] = cnt > m.a[l].fb_cap;  // overflow: the whole map of that level
+      items[l] = all[l] ? (unsigned long long)m.a[l].N * m.a[l].s_rn * m.a[l].W : (unsigned long long)cnt;
+      total += items[l];
+    }
+  }
+  // one pass over the concatenated lists: every warp takes at most ceil(total / warps) pixels of
+  // any level (the calls this serves are small: one pixel latency per warp)
+  const int lane = threadIdx.x & 31;
+  const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < total;
+       i += warps) {
+    unsigned long long j = i;
+    int l = 0;
+    while (l + 1 < m.n && j >= items[l]) {  // warp-uniform
+      j -= items[l];
+      ++l;
+    }
+    fixup_pixel<FAST, WIDE>(FixLevel(m.a[l]), m.prm[l], j, all[l], lane);
+  }
+}
+
 }  // namespace blade

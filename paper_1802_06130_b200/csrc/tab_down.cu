@@ -18,5 +18,9 @@ DownKernel fixup_kernel(bool hilo, bool fast, bool wide) {
   if (hilo) return fast ? &k_down_fixup<true, true, false> : &k_down_fixup<true, false, false>;
   return fast ? &k_down_fixup<false, true, false> : &k_down_fixup<false, false, false>;
 }
+FixupMultiKernel fixup_multi_kernel(bool fast, bool wide) {
+  if (wide) return &k_down_fixup_multi<false, true>;
+  return fast ? &k_down_fixup_multi<true, false> : &k_down_fixup_multi<false, false>;
+}
 }  // namespace tables
 }  // namespace blade

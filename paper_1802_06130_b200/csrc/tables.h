@@ -45,6 +45,8 @@ using DownKernel = void (*)(const DownArgs, const DownParams);
 // wide: uint16 bucket maps (K > 256, NEXT f2)
 DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy = false);
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide);
+using FixupMultiKernel = void (*)(const FixupMulti);
+FixupMultiKernel fixup_multi_kernel(bool fast, bool wide);
 
 // Training (NEXT f4): segmented fp64 SYRK of the normal equations.
 using TrainKernel = void (*)(const TrainArgs);
