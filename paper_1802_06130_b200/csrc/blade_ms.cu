@@ -540,7 +540,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   }
   // ---- small (launch-latency-bound) calls: the fix-ups of every level in one launch per
   //      kFixMax levels after the down pass (the stages need them, the next k_down does not; on
-  //      large batches the per-level fix-up right after its k_down is faster: 22 vs 70 us on c3)
+  //      large batches the per-level fix-up right after its k_down is faster: 50 vs 70 us on c3)
   if (merge_fix) {
     const int l = nsel - 1;  // (LAUNCH's error message)
     const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
