@@ -39,7 +39,9 @@ FP32_LANES_PER_SM = 128  # B200: 4 SMSPs x 32 FP32 lanes (B200_PROFILING.md / gu
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks) of the run; without WORLD_SIZE in the environment and N > 1 "
+                         "the bench launches its own N ranks (torch.distributed.run, one per GPU)")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3")
@@ -55,6 +57,13 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0,
                     help="NEXT f3: frame-chunked schedule, chunks of this many frames (0 = off)")
     ap.add_argument("--streams", type=int, default=2, help="internal streams of the chunked schedule")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as a CUDA graph (auto: when the call is small enough to be "
+                         "launch-bound, <= 4 MP per rank)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU plumbing check of the multi-rank path (gloo, no GPU work, no kernels): "
+                         "self-launch, barrier, max-over-ranks timing and the rank-0 JSON line, "
+                         "marked dry_run; never a bench result")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU time of the oracle sample (cpu_baseline)")
@@ -64,6 +73,43 @@ def parse():
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def self_launch(args):
+    """--gpus N: under torchrun (WORLD_SIZE set) N must equal WORLD_SIZE; otherwise, for N > 1,
+    launch N ranks on this node with torch.distributed.run (127.0.0.1 rendezvous) running this
+    same command line, and return its exit code. None = run in this process."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None:
+        if args.gpus is not None and args.gpus != int(ws):
+            print(f"bench.py: --gpus {args.gpus} disagrees with WORLD_SIZE={ws}", file=sys.stderr)
+            return 2
+        return None
+    if args.gpus is None or args.gpus <= 1:
+        return None
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def init_dist(backend: str, local: int, world: int):
+    """Process group for world > 1. NCCL logs its communicator set-up (NCCL_DEBUG=INFO, INIT
+    subsystem) unless the caller chose otherwise, so the rank count is visible in the log."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return
+    if backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -245,17 +291,57 @@ def run_reference(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- dry run (CPU)
+
+def run_dry(args):
+    """The multi-rank plumbing of the blade arm on CPU (gloo): the same shard split, barrier,
+    max-over-ranks reduction and rank-0 line; the step is a 1 ms host sleep, not the hot path."""
+    import torch.distributed as dist
+    from paper_1802_06130_b200.shard import max_over_ranks, shard_for, units
+    rank, local, world = dist_env()
+    init_dist("gloo", local, world)
+    cfg = bs.load_config(args.config)
+    shard = shard_for(cfg, rank, world)
+    def barrier():
+        if world > 1:
+            dist.barrier()
+    for _ in range(args.warmup):
+        time.sleep(0.001)
+    barrier()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.001)
+    ms = (time.perf_counter() - t) * 1e3
+    barrier()
+    ms_max = max_over_ranks(ms)
+    total = sum(units(cfg, shard_for(cfg, r, world)) for r in range(world))
+    if rank == 0:
+        print(json.dumps({"metric": "megapixels/sec full multiscale denoise", "dry_run": True,
+                          "value": None, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms_max / max(args.steps, 1),
+                          "config": {"workload": cfg.name, "units_all_ranks": total,
+                                     "rank0_shard": shard.__dict__}}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 # ----------------------------------------------------------------------------- blade arm
 
 def main():
     args = parse()
+    rc = self_launch(args)
+    if rc is not None:
+        return rc
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     import torch
     import torch.distributed as dist
     rank, local, world = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    init_dist("nccl", local, world)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_1802_06130_b200 import BladeMS
@@ -267,6 +353,9 @@ def main():
     H, W = cfg.H, cfg.W
     h = BladeMS.from_config(cfg, taps=cfg.taps(channels=3 if args.ycc else 1), device=local)
     stream = torch.cuda.current_stream(dev)
+
+    def cur():  # the stream a step launches on (the capture stream while a graph is recorded)
+        return torch.cuda.current_stream(dev)
     if shard.mode == "frames":
         # ---- this rank's frames, generated on the host (seeded), copied once to HBM
         n_local, f0 = shard.frames, shard.frame0
@@ -282,12 +371,12 @@ def main():
                              dtype=torch.uint8, device=dev)
 
             def step():
-                h.denoise_pipelined(x, out, args.chunk, args.streams, ws, stream)
+                h.denoise_pipelined(x, out, args.chunk, args.streams, ws, cur())
         else:
             ws = h.workspace(n_local, H, W)
 
             def step():
-                h.denoise(x, out, ws, stream)
+                h.denoise(x, out, ws, cur())
 
         def e2e_step():
             h.denoise_host(x_host, out_host, d_in, out, ws, stream)
@@ -310,7 +399,7 @@ def main():
                          dtype=torch.uint8, device=dev)
 
         def step():
-            h.denoise_rows(x, shard.in_row0, shard.out_row0, shard.out_rows, H, out, ws, stream)
+            h.denoise_rows(x, shard.in_row0, shard.out_row0, shard.out_rows, H, out, ws, cur())
 
         out_host = torch.empty((3, shard.out_rows, W), dtype=torch.float32).pin_memory()
         d_in = torch.empty_like(x)
@@ -348,8 +437,24 @@ def main():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    for _ in range(args.warmup):
+    # ---- what one step touches, against the L2: small working sets are timed after an L2
+    #      flush, large ones back to back (their inputs exceed the L2)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    footprint = int(x.numel() * 4 + out.numel() * 4 + ws.numel())
+    small = footprint < 2 * l2
+    use_graph = (args.graph == "on" or (args.graph == "auto" and n_local * H * W <= (4 << 20))) \
+        and not args.train
+    run = step
+    if use_graph:  # the whole cascade as one CUDA graph (launch-bound small calls)
         step()
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        run = graph.replay
+
+    for _ in range(args.warmup):
+        run()
     barrier()
 
     sampler = ClockSampler(local)
@@ -359,20 +464,42 @@ def main():
     t0 = time.time()
     e0.record(stream)
     for _ in range(args.steps):
-        step()
+        run()
     e1.record(stream)
     torch.cuda.synchronize(dev)
     t1 = time.time()
     barrier()
+    warm_ms = e0.elapsed_time(e1)
+    flushed_ms = None
+    if small:
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        evs = []
+        for _ in range(args.steps):
+            flush.fill_(1)  # not timed: a 256 MB write evicts the previous step's lines
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            run()
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize(dev)
+        t1 = time.time()
+        flushed_ms = sum(a.elapsed_time(b) for a, b in evs)
+        barrier()
     time.sleep(0.1)
     sampler.stop()
     clocks = sampler.summary(t0, t1)
-    ms = e0.elapsed_time(e1)
+    ms = flushed_ms if small else warm_ms
     ms_max = max_over_ranks(ms, dev)
     ms_per_step = ms_max / args.steps
     total_px = cfg.N * H * W  # all ranks together (frames: the batch; bands: the whole image)
     assert world > 1 or units(cfg, shard) == total_px
     value = total_px / 1e6 / (ms_per_step / 1e3)
+    warm_step = max_over_ranks(warm_ms, dev) / args.steps
+    if small:
+        l2_note = (f"working set {footprint / 1e6:.1f} MB < 2 x L2 ({l2 / 1e6:.0f} MB): L2 flushed by a "
+                   f"256 MB write before every timed step (value); back-to-back rate in 'warm'")
+    else:
+        l2_note = f"working set {footprint / 1e9:.2f} GB per step > L2 ({l2 / 1e6:.0f} MB): no flush"
 
     if args.train:
         nt = cfg.fine_size ** 2 + (cfg.coarse_size ** 2 if cfg.levels > 1 else 0)
@@ -491,7 +618,7 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
             mps, dt, what, cores = oracle_sample_rate(cfg, args.cpu_seconds)
             cpu = {"value": mps, "unit": "MP/s", "cores": cores, "kind": "oracle",
@@ -516,9 +643,12 @@ def main():
                                        f"row bands over {world} GPU(s) with recomputed halo "
                                        f"(rank 0: out rows {shard.out_row0}+{shard.out_rows}, "
                                        f"in rows {shard.in_row0}+{shard.in_rows}), no collective"),
-                       "l2": "inputs larger than L2 (no flush)",
+                       "l2": l2_note,
+                       "cuda_graph": bool(use_graph),
                        "schedule": (f"frame chunks of {args.chunk} on {args.streams} streams (f3)"
                                     if args.chunk and shard.mode == "frames" else "whole batch per launch")},
+            "warm": {"value": total_px / 1e6 / (warm_step / 1e3), "ms_per_step": warm_step,
+                     "note": "back-to-back steps, no flush" + (" (L2-resident working set)" if small else "")},
             "roofline": roof,
             "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm_ach / hbm_peak,

@@ -30,9 +30,11 @@
  *     Asynchronous device faults surface at the caller's next synchronisation.
  *   - Thread safety: a handle's bank and plan are immutable after create; concurrent calls
  *     with distinct workspaces/outputs (on any streams) are safe, except while profiling is on
- *     (blade_ms_set_profiling). blade_ms_denoise_pipelined's internal streams are shared by
- *     the handle: concurrent pipelined calls stay correct but may serialise (and a caller's
- *     join may also wait for another call's chunks). destroy must not race pending work.
+ *     (blade_ms_set_profiling). blade_ms_denoise_pipelined's internal streams and fork/join
+ *     events are shared by the handle: concurrent pipelined calls are serialised on the host
+ *     (a per-handle mutex held from fork to join), so each call's chunks wait on its own
+ *     caller stream; their device work may serialise, and a caller's join may also wait for
+ *     another call's chunks queued before its own. destroy must not race pending work.
  *   - Non-finite PIXEL values are not checked (it would cost a pass); outputs are then
  *     unspecified. Non-finite TAPS and thresholds are rejected at create.
  */

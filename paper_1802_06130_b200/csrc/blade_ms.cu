@@ -175,6 +175,10 @@ struct blade_ms {
   cudaStream_t pipe[kMaxStreams] = {};
   cudaEvent_t pipe_fork = nullptr;
   cudaEvent_t pipe_join[kMaxStreams] = {};
+  // serialises whole pipelined calls on this handle: the fork / join events and the internal
+  // streams are handle-wide, so one call's record-then-wait pairs must not interleave with
+  // another's (a re-recorded pipe_fork would let a chunk wait on the wrong caller stream)
+  std::mutex pipe_mu;
 };
 
 namespace {
@@ -389,7 +393,17 @@ bool use_ry4(const blade_ms* h, int N, int W, int span) {
 
 // The fp64 fix-ups of all selector levels run as one launch after the down pass on small calls
 // (launch-latency-bound: c1 -7 us per call), per level right after each k_down otherwise.
-bool fixups_merged(int nsel, long long N, long long H, long long W) { return nsel > 1 && N * H * W <= (4LL << 20); }
+// BLADE_FIXUP_MERGE=0 / =1 forces the per-level / merged form on every call (A/B timing of the
+// threshold: scripts/fixup_ab.sh); default by size.
+bool fixups_merged(int nsel, long long N, long long H, long long W) {
+  static const int force = [] {
+    const char* e = getenv("BLADE_FIXUP_MERGE");
+    return e ? atoi(e) : -1;
+  }();
+  if (nsel <= 1) return false;
+  if (force == 0 || force == 1) return force == 1;
+  return N * H * W <= (4LL << 20);
+}
 
 // Kernel launch; with `pdl` the launch allows programmatic stream serialisation (PDL): the grid
 // may be scheduled while the previous kernel in the stream drains, and its kernels call pdl_wait()
@@ -1193,6 +1207,7 @@ blade_status blade_ms_denoise_pipelined(blade_ms_t h, const float* in, float* ou
   cudaStream_t st = (cudaStream_t)stream;
   const int nchunks = (N + chunk - 1) / chunk;
   const int ns = std::min(n_streams, nchunks);
+  std::lock_guard<std::mutex> lock(h->pipe_mu);  // fork .. join of this call, atomically
   cudaError_t ce = cudaEventRecord(h->pipe_fork, st);
   for (int i = 0; i < ns && ce == cudaSuccess; ++i) ce = cudaStreamWaitEvent(h->pipe[i], h->pipe_fork, 0);
   if (ce != cudaSuccess) return fail(BLADE_ECUDA, "fork: %s", cudaGetErrorString(ce));

@@ -546,3 +546,102 @@ def test_fixup_list_overflow_recomputes_everything(name):
     d = (og - oo) % cfg.n_orient
     assert np.isin(d, [0, 1, cfg.n_orient - 1]).all()
     assert (gpu[top] % per_o == ob[top] % per_o).all()  # strength / coherence bins agree
+
+
+# ------------------------------------------------------------------ forced-selector parity mode
+
+def _forced_parity(cfg, x_np, taps=None, label="", frames=None):
+    """SURVEY.md §8(c) parity rule 2(a): the oracle's stages (Eq. 9, fp64) consume the GPU's OWN
+    bucket maps, so the comparison covers every output pixel, including the dependency cones of
+    near-boundary bucket mismatches that the free mode excludes. Every pixel within 1e-4."""
+    taps = cfg.taps() if taps is None else taps
+    t4 = taps[:, 0] if taps.ndim == 5 else taps
+    h = _handle(cfg, taps)
+    x = torch.from_numpy(x_np).cuda()
+    out = h.denoise(x)
+    maps = h.selector(x)
+    torch.cuda.synchronize()
+    sel = list(range(x_np.shape[0])) if frames is None else list(frames)
+    L = cfg.levels
+    worst = 0.0
+    for n in sel:
+        lv = oracle.pyramid(x_np[n], L)
+        gm = [maps[l][n].cpu().numpy().astype(np.int32) for l in range(len(maps))]
+        if L == 1:
+            ref = oracle.stage(lv[0], None, gm[0], t4[0], cfg.n_phases, cfg.fine_size, 0)
+        else:
+            ref = lv[L - 1]
+            for l in range(L - 2, -1, -1):
+                ref = oracle.stage(lv[l], ref, gm[l], t4[l], cfg.n_phases, cfg.fine_size, cfg.coarse_size)
+        err = float(np.abs(out[n].cpu().numpy().astype(np.float64) - ref).max())
+        assert err <= OUT_ATOL, f"{label} frame {n}: forced-selector max |gpu - oracle| = {err}"
+        worst = max(worst, err)
+    return worst
+
+
+@pytest.mark.parametrize("name,N,frames", [("c0", 1, None), ("c1", 1, None), ("c3", 2, None), ("c2", 1, None),
+                                           ("c4", 1, None), ("c5", 2, None)])
+def test_forced_selector_every_pixel(name, N, frames):
+    """Forced-selector mode on every config at full size (c3 / c5: 2 frames of the recipe)."""
+    cfg = bs.load_config(name)
+    _forced_parity(cfg, cfg.batch(N=N), label=f"{name} forced", frames=frames)
+
+
+def test_forced_selector_bench_batch_sampled_frames():
+    """Forced-selector mode in the bench's launch configuration (the whole 64-frame c3 batch)."""
+    cfg = bs.load_config("c3")
+    _forced_parity(cfg, cfg.batch(), label="c3 bench batch forced", frames=(5, 63))
+
+
+@pytest.mark.parametrize("name,H,W,N", [("c1", 67, 129, 2), ("c4", 203, 333, 1), ("c2", 9, 17, 1)])
+def test_forced_selector_ragged(name, H, W, N):
+    cfg = _cfg_like(name, H, W, N)
+    _forced_parity(cfg, cfg.batch(), label=f"{name}@{H}x{W} forced")
+
+
+# ------------------------------------------------------------------ deep pyramids (merged fix-up)
+
+@pytest.mark.parametrize("levels,H,W", [(7, 256, 256), (6, 130, 200), (12, 300, 260)])
+def test_deep_pyramid_merged_fixup(levels, H, W):
+    """levels >= 6 on a small image: more than kFixMax = 4 selector levels, so the merged fp64
+    fix-up runs as ceil(nsel / 4) launches; the launch count says so and every level's map and
+    the output obey the parity rule (the nsel > 4 path was untested)."""
+    cfg = _cfg_like("c1", H, W, 1, levels=levels)
+    nst = levels - 1
+    cfg.strength_thresholds = [list(_TS1)] * nst
+    cfg.coherence_thresholds = [list(_TC1)] * nst
+    h = _handle(cfg)
+    nsel = levels - 1
+    assert h.launch_count(1, H, W) == 2 * nsel + (nsel + 3) // 4, h.launch_count(1, H, W)
+    _full_parity(cfg, cfg.batch(), label=f"L{levels}@{H}x{W}")
+
+
+def test_deep_pyramid_merged_fixup_overflow():
+    """The merged fix-up with 6 selector levels where level 0's list overflows (half the frame an
+    exact 45-degree ramp): the whole level-0 map is recomputed in fp64 inside the merged launch;
+    the natural half obeys the parity rule at every level that sees only natural rows."""
+    H, W, levels = 256, 384, 7
+    cfg = _cfg_like("c1", H, W, 1, levels=levels)
+    cfg.strength_thresholds = [list(_TS1)] * (levels - 1)
+    cfg.coherence_thresholds = [list(_TC1)] * (levels - 1)
+    x = cfg.batch()
+    yy, xx = np.mgrid[0:H // 2, 0:W]
+    x[0, :, :H // 2] = (0.25 + (xx + yy) * 2.0 ** -10).astype(np.float32)
+    h = _handle(cfg)
+    xt = torch.from_numpy(x).cuda()
+    ws = h.workspace(1, H, W)
+    maps = h.selector(xt, workspace=ws)
+    counts = h.fallback_count(1, H, W, ws)
+    assert counts[0] > H * W // 64, counts
+    ts, tc = cfg.thresholds()
+    ob, feats = oracle.selector(x[0].astype(np.float64), cfg.n_orient, cfg.n_strength, cfg.n_coherence,
+                                ts[0], tc[0], cfg.window_size, cfg.window_sigma, features=True)
+    lo = H // 2 + 4
+    gpu = maps[0][0].cpu().numpy().astype(np.int64)
+    check_buckets(gpu[lo:], ob[lo:], tuple(f[lo:] for f in feats), cfg.n_orient, ts[0], tc[0],
+                  "L7 natural half after overflow")
+    per_o = cfg.n_strength * cfg.n_coherence
+    top = slice(2, H // 2 - 3)
+    d = (gpu[top] // per_o - ob[top] // per_o) % cfg.n_orient
+    assert np.isin(d, [0, 1, cfg.n_orient - 1]).all()
+    assert (gpu[top] % per_o == ob[top] % per_o).all()

@@ -4,8 +4,12 @@ cone written from the paper's definitions, and a world_size-2 gloo process group
 bench's max-over-ranks reduction and shard planning (the data path itself has no collective)."""
 from __future__ import annotations
 
+import json
 import os
 import socket
+import subprocess
+import sys
+from pathlib import Path
 
 import pytest
 import torch
@@ -14,6 +18,8 @@ import torch.multiprocessing as mp
 
 import blade_synth as bs
 from paper_1802_06130_b200.shard import max_over_ranks, shard_for, split_even, units
+
+ROOT = Path(__file__).resolve().parents[1]
 
 
 def _fold(i: int, n: int) -> int:
@@ -133,3 +139,33 @@ def test_gloo_world2_shards_and_max_reduction():
     # the two bands' input halos overlap (recomputed, not exchanged)
     assert b[1].in_row0 < b[0].out_rows < b[0].in_row0 + b[0].in_rows
     assert sum(units(c3, s) for s in f) == c3.N * c3.H * c3.W
+
+
+def _bench_json(stdout: str) -> dict:
+    lines = [ln for ln in stdout.splitlines() if ln.startswith("{")]
+    assert lines, stdout
+    return json.loads(lines[-1])
+
+
+def test_bench_self_launches_world2_dry_run():
+    """bench.py --gpus 2 with no WORLD_SIZE launches its own 2 ranks (torch.distributed.run,
+    127.0.0.1) and the world-2 path (gloo here: barrier, max-over-ranks time, rank-0 line)
+    prints n_gpus: 2 (--gpus was parsed and ignored)."""
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _bench_json(r.stdout)
+    assert d["n_gpus"] == 2 and d["dry_run"] is True
+    c3 = bs.load_config("c3")
+    assert d["config"]["units_all_ranks"] == c3.N * c3.H * c3.W
+    assert d["config"]["rank0_shard"]["frames"] == c3.N // 2
+
+
+def test_bench_rejects_gpus_world_size_mismatch():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4", "--dry-run"],
+                       capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 2 and "disagrees" in r.stderr
