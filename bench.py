@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0,
                     help="NEXT f3: frame-chunked schedule, chunks of this many frames (0 = off)")
     ap.add_argument("--streams", type=int, default=2, help="internal streams of the chunked schedule")
+    ap.add_argument("--halo", default="recompute", choices=["recompute", "exchange"],
+                    help="row-band configs (c4) at N > 1: recompute each band's dependency cone, or "
+                         "exchange per-level halo rows with the neighbour ranks (NEXT f3)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: when the call is small enough to be "
                          "launch-bound, <= 4 MP per rank)")
@@ -390,26 +393,41 @@ def main():
         io_in = io_out = n_local * 3 * H * W * 4
     else:
         # ---- this rank's row band of the one image: input rows of its dependency cone
+        #      (--halo recompute), or own rows +- a small halo with per-level halo exchange
+        #      between neighbour ranks (--halo exchange, NEXT f3; NCCL P2P)
         n_local = 1
+        if args.halo == "exchange":
+            from paper_1802_06130_b200.xband import denoise_band_dist
+            lay = h.xband_layout(H, W, shard.out_row0, shard.out_rows)
+            in_row0, in_rows = lay["in_row0"], lay["in_rows"]
+            ws = torch.empty(lay["ws_bytes"], dtype=torch.uint8, device=dev)
+
+            def run_band(src):
+                denoise_band_dist(h, src, lay, out, ws, shard.out_row0, H, rank, world, cur())
+        else:
+            in_row0, in_rows = shard.in_row0, shard.in_rows
+            ws = torch.empty(h.band_workspace_size(H, W, shard.out_row0, shard.out_rows),
+                             dtype=torch.uint8, device=dev)
+
+            def run_band(src):
+                h.denoise_rows(src, in_row0, shard.out_row0, shard.out_rows, H, out, ws, cur())
         x_host = torch.from_numpy(np.ascontiguousarray(
-            cfg.frame(0, row0=shard.in_row0, rows=shard.in_rows))).pin_memory()
+            cfg.frame(0, row0=in_row0, rows=in_rows))).pin_memory()
         x = x_host.to(dev)
         out = torch.empty((3, shard.out_rows, W), dtype=torch.float32, device=dev)
-        ws = torch.empty(h.band_workspace_size(H, W, shard.out_row0, shard.out_rows),
-                         dtype=torch.uint8, device=dev)
 
         def step():
-            h.denoise_rows(x, shard.in_row0, shard.out_row0, shard.out_rows, H, out, ws, cur())
+            run_band(x)
 
         out_host = torch.empty((3, shard.out_rows, W), dtype=torch.float32).pin_memory()
         d_in = torch.empty_like(x)
 
         def e2e_step():
             d_in.copy_(x_host, non_blocking=True)
-            h.denoise_rows(d_in, shard.in_row0, shard.out_row0, shard.out_rows, H, out, ws, stream)
+            run_band(d_in)
             out_host.copy_(out, non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
-        io_in = 3 * shard.in_rows * W * 4
+        io_in = 3 * in_rows * W * 4
         io_out = 3 * shard.out_rows * W * 4
 
     if args.train:
@@ -443,7 +461,7 @@ def main():
     footprint = int(x.numel() * 4 + out.numel() * 4 + ws.numel())
     small = footprint < 2 * l2
     use_graph = (args.graph == "on" or (args.graph == "auto" and n_local * H * W <= (4 << 20))) \
-        and not args.train
+        and not args.train and not (args.halo == "exchange" and world > 1)
     run = step
     if use_graph:  # the whole cascade as one CUDA graph (launch-bound small calls)
         step()
@@ -640,9 +658,12 @@ def main():
                        "filter_channels": "Y,Cb,Cr (f1)" if args.ycc else "shared R,G,B",
                        "parallelism": (f"frames split over {world} GPU(s), no collective"
                                        if shard.mode == "frames" else
-                                       f"row bands over {world} GPU(s) with recomputed halo "
-                                       f"(rank 0: out rows {shard.out_row0}+{shard.out_rows}, "
-                                       f"in rows {shard.in_row0}+{shard.in_rows}), no collective"),
+                                       (f"row bands over {world} GPU(s) with recomputed halo "
+                                        f"(rank 0: out rows {shard.out_row0}+{shard.out_rows}, "
+                                        f"in rows {shard.in_row0}+{shard.in_rows}), no collective"
+                                        if args.halo == "recompute" else
+                                        f"row bands over {world} GPU(s), per-level halo rows "
+                                        f"exchanged with the neighbour ranks (NCCL P2P)")),
                        "l2": l2_note,
                        "cuda_graph": bool(use_graph),
                        "schedule": (f"frame chunks of {args.chunk} on {args.streams} streams (f3)"

@@ -222,6 +222,54 @@ blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t i
                                    size_t ws_bytes, void* cuda_stream);
 
 /*
+ * NEXT f3 (b): row bands whose neighbours EXCHANGE halo rows between pyramid levels instead of
+ * each recomputing its whole dependency cone (§5: time linear in
+ * the pixels). Band b owns output rows [out_row0, out_row0 + out_rows) = own^0 and, at every
+ * level, own^{l+1} = [ceil(own^l.lo / 2), ceil(own^l.hi / 2)) — so bands that partition the
+ * image partition every level — and computes only those rows; the halo_z rows of z^l and halo_u
+ * rows of u^l around them come from the neighbour bands.
+ *
+ * blade_ms_xband_layout (host only, no handle): the band's plan. Steps s = 0 .. n_steps-1 with
+ * n = max(levels - 1, 1): s < n is the down pass at level l = s (selector map s^l of own^l and
+ * z^{l+1} of own^{l+1}), s >= n the up pass at level l = 2n-1-s (stage l of own^l; l = 0 writes
+ * out_band). After step s, for side 0 (the band above, rows < own) and side 1 (below),
+ * send[s][side] names this band's own boundary rows the neighbour needs and recv[s][side] the
+ * halo rows to be filled from it (rows == 0: nothing to move). A region is `planes` runs of
+ * `rows` x `pitch` fp32 values, global rows [row0, row0 + rows), starting `offset` bytes into
+ * the band's workspace, `plane_stride` bytes apart. The band's send[s][1] and the band below's
+ * recv[s][0] cover the same global rows (likewise send[s][0] / the band above's recv[s][1]).
+ * in_row0 / in_rows: the level-0 input rows the band reads (own^0 +- halo_z, clamped);
+ * ws_bytes: its workspace. EUNSUPPORTED when some level of a band (other than the whole image)
+ * owns fewer than halo_z rows. K = bucket count (map entry size).
+ *
+ * blade_ms_xband_step: runs step s of the band on `stream` (asynchronous). The caller moves the
+ * recv regions of step s-1 in before calling it (NCCL send/recv between GPUs, a device copy
+ * between bands on one GPU). Concatenated band outputs equal blade_ms_denoise of the whole
+ * frame bit-exactly (the same kernels compute every row from the same inputs). Argument errors
+ * as blade_ms_denoise_rows.
+ */
+#define BLADE_MAX_LEVELS 12
+typedef struct {
+  int64_t offset;        /* bytes into the band's workspace                                  */
+  int64_t plane_stride;  /* bytes between planes                                             */
+  int32_t row0, rows;    /* global rows [row0, row0 + rows) of the level                      */
+  int32_t pitch, planes; /* fp32 values per row; planes (3 channels; 6 = hi + lo of z^l)       */
+} blade_region;
+typedef struct {
+  int32_t levels, n_steps, halo_z, halo_u;
+  int32_t own_lo[BLADE_MAX_LEVELS], own_hi[BLADE_MAX_LEVELS];
+  int32_t in_row0, in_rows;
+  uint64_t ws_bytes;
+  blade_region send[2 * BLADE_MAX_LEVELS][2], recv[2 * BLADE_MAX_LEVELS][2];
+} blade_xband_layout;
+blade_status blade_ms_xband_layout(const blade_ms_config* cfg, int32_t K, int32_t H, int32_t W,
+                                   int32_t out_row0, int32_t out_rows, blade_xband_layout* layout);
+blade_status blade_ms_xband_step(blade_ms_t h, int32_t step, const float* in_band, int32_t in_row0,
+                                 int32_t in_rows, float* out_band, int32_t out_row0,
+                                 int32_t out_rows, int32_t H_full, int32_t W, void* workspace,
+                                 size_t ws_bytes, void* cuda_stream);
+
+/*
  * Diagnostic: the bucket maps s^l (device, [N][H_l][W_l]; uint8 entries when K <= 256, uint16
  * when K > 256 — the paper's 16 x 16 x 16 layout, NEXT f2) for every selector level
  * l = 0 .. n_stages-1 (maps_per_level[l]; a NULL entry skips that level). Also leaves the

@@ -49,13 +49,29 @@ class _Info(ctypes.Structure):
                 ("stage_phase_groups", ctypes.c_int32)]
 
 
+class _Region(ctypes.Structure):
+    _fields_ = [("offset", ctypes.c_int64), ("plane_stride", ctypes.c_int64), ("row0", ctypes.c_int32),
+                ("rows", ctypes.c_int32), ("pitch", ctypes.c_int32), ("planes", ctypes.c_int32)]
+
+
+MAX_LEVELS = 12  # BLADE_MAX_LEVELS
+
+
+class _XLayout(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_int32), ("n_steps", ctypes.c_int32), ("halo_z", ctypes.c_int32),
+                ("halo_u", ctypes.c_int32), ("own_lo", ctypes.c_int32 * MAX_LEVELS),
+                ("own_hi", ctypes.c_int32 * MAX_LEVELS), ("in_row0", ctypes.c_int32),
+                ("in_rows", ctypes.c_int32), ("ws_bytes", ctypes.c_uint64),
+                ("send", (_Region * 2) * (2 * MAX_LEVELS)), ("recv", (_Region * 2) * (2 * MAX_LEVELS))]
+
+
 EXPORTS = ["blade_ms_create", "blade_ms_workspace_size", "blade_ms_denoise", "blade_ms_denoise_host",
            "blade_ms_pipeline_workspace_size", "blade_ms_denoise_pipelined",
            "blade_ms_band_rows", "blade_ms_band_plan", "blade_ms_fallback_count",
            "blade_ms_train_layout", "blade_ms_train_workspace_size", "blade_ms_train_accumulate",
            "blade_ms_train_solve", "blade_ms_band_workspace_size", "blade_ms_denoise_rows",
            "blade_ms_selector", "blade_ms_pyramid", "blade_ms_get_info", "blade_ms_launch_count",
-           "blade_ms_stage_kernel",
+           "blade_ms_stage_kernel", "blade_ms_xband_layout", "blade_ms_xband_step",
            "blade_ms_set_profiling", "blade_ms_profile_read",
            "blade_ms_destroy", "blade_ms_status_string", "blade_ms_last_error"]
 
@@ -97,6 +113,9 @@ def lib():
     L.blade_ms_train_solve.argtypes = [P, P, P, ctypes.c_double, ctypes.c_uint64, P]
     L.blade_ms_band_workspace_size.argtypes = [P, i32, i32, i32, i32, ctypes.POINTER(sz)]
     L.blade_ms_denoise_rows.argtypes = [P, P, i32, i32, P, i32, i32, i32, i32, P, sz, P]
+    L.blade_ms_xband_layout.argtypes = [ctypes.POINTER(_Config), i32, i32, i32, i32, i32,
+                                        ctypes.POINTER(_XLayout)]
+    L.blade_ms_xband_step.argtypes = [P, i32, P, i32, i32, P, i32, i32, i32, i32, P, sz, P]
     L.blade_ms_selector.argtypes = [P, P, i32, i32, i32, P, P, sz, P]
     L.blade_ms_pyramid.argtypes = [P, P, i32, i32, i32, P, P, sz, P]
     L.blade_ms_get_info.argtypes = [P, ctypes.POINTER(_Info)]
@@ -141,6 +160,36 @@ def band_plan(levels: int, fine_size: int, coarse_size: int, window_size: int, H
     return a.value, b.value
 
 
+def _region(r: _Region) -> dict:
+    return {"offset": r.offset, "plane_stride": r.plane_stride, "row0": r.row0, "rows": r.rows,
+            "pitch": r.pitch, "planes": r.planes}
+
+
+def xband_layout(levels: int, fine_size: int, coarse_size: int, window_size: int, K: int, H: int,
+                 W: int, out_row0: int, out_rows: int) -> dict:
+    """blade_ms_xband_layout (host only): the plan of a row band that exchanges per-level halo
+    rows with its neighbours (NEXT f3): own rows per level, input rows, workspace bytes, steps
+    and, per step and side (0 = band above, 1 = below), the send / recv workspace regions."""
+    cfg = _Config(levels, fine_size, coarse_size if levels > 1 else 0, 4 if levels > 1 else 1, 1,
+                  window_size, 1.5, 0)
+    x = _XLayout()
+    _check(lib().blade_ms_xband_layout(ctypes.byref(cfg), K, H, W, out_row0, out_rows, ctypes.byref(x)))
+    n = x.n_steps
+    return {"levels": x.levels, "n_steps": n, "halo_z": x.halo_z, "halo_u": x.halo_u,
+            "own": [(x.own_lo[l], x.own_hi[l]) for l in range(x.levels)],
+            "in_row0": x.in_row0, "in_rows": x.in_rows, "ws_bytes": int(x.ws_bytes),
+            "send": [[_region(x.send[s][d]) for d in range(2)] for s in range(n)],
+            "recv": [[_region(x.recv[s][d]) for d in range(2)] for s in range(n)]}
+
+
+def region_view(ws: torch.Tensor, r: dict) -> torch.Tensor:
+    """[planes, rows, pitch] fp32 view of a region of a uint8 workspace tensor."""
+    f = ws.view(torch.float32)
+    assert r["offset"] % 4 == 0 and r["plane_stride"] % 4 == 0
+    return torch.as_strided(f, (r["planes"], r["rows"], r["pitch"]),
+                            (r["plane_stride"] // 4, r["pitch"], 1), r["offset"] // 4)
+
+
 class BladeMS:
     """Handle over blade_ms_create / blade_ms_denoise / blade_ms_destroy."""
 
@@ -166,6 +215,7 @@ class BladeMS:
         self.levels = levels
         self.n_stages = max(levels - 1, 1)
         self.K = n_orient * n_strength * n_coherence
+        self.fine_size, self.coarse_size, self.window_size = fine_size, coarse_size, window_size
         self.map_dtype = torch.uint16 if self.K > 256 else torch.uint8
 
     @classmethod
@@ -397,3 +447,18 @@ class BladeMS:
                                            _ptr(workspace), workspace.numel(),
                                            _stream_ptr(stream)))
         return out_band
+
+    # ------------------------------------------------------------------ bands with halo exchange
+    def xband_layout(self, H: int, W: int, out_row0: int, out_rows: int) -> dict:
+        return xband_layout(self.levels, self.fine_size, self.coarse_size, self.window_size, self.K,
+                            H, W, out_row0, out_rows)
+
+    def xband_step(self, step: int, in_band: torch.Tensor, in_row0: int, out_band: torch.Tensor,
+                   out_row0: int, H: int, workspace: torch.Tensor, stream=None):
+        """Step `step` of a halo-exchange band (blade_ms_xband_step); in_band [3, rows, W]
+        holds global rows from in_row0, out_band [3, out_rows, W]."""
+        _, in_rows, W = in_band.shape
+        out_rows = out_band.shape[1]
+        _check(lib().blade_ms_xband_step(self._h, step, _ptr(in_band), in_row0, in_rows,
+                                         _ptr(out_band), out_row0, out_rows, H, W,
+                                         _ptr(workspace), workspace.numel(), _stream_ptr(stream)))

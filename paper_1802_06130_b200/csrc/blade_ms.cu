@@ -186,8 +186,10 @@ namespace {
 struct Plan {
   int L = 0, N = 0;
   std::vector<int> H, W;
-  std::vector<Range> z;  // rows of z^l materialised (level 0: needed input rows)
-  std::vector<Range> u;  // rows of u^l computed (= map rows), l <= L-2 (l = 0 if L == 1)
+  std::vector<Range> z;   // rows of the z^l buffer (level 0: needed input rows)
+  std::vector<Range> zc;  // rows of z^l computed by the down pass, l >= 1 (= z unless exchanged)
+  std::vector<Range> u;   // rows of u^l computed (= map rows), l <= L-2 (l = 0 if L == 1)
+  std::vector<Range> ub;  // rows of the u^l buffer, 1 <= l <= L-2 (= u unless exchanged)
   size_t ws_bytes = 0;
   std::vector<size_t> z32_off, zlo_off, u_off, map_off, fb_off;
   std::vector<int> map_pitch;  // entries per map row: W_l rounded up to 16 (16-B TMA rows)
@@ -201,6 +203,7 @@ struct Plan {
 
 // Dependency cone of output rows [o0, o0+on) of the final output.
 void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int on, Plan& p, int map_es = 1);
+void plan_layout(Plan& p, int map_es, int W, bool full_image);
 void plan_rows(const blade_ms* h, int N, int H, int W, int o0, int on, Plan& p) {
   plan_rows_cfg(h->cfg, N, H, W, o0, on, p, h->K > 256 ? 2 : 1);
 }
@@ -238,6 +241,15 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
       p.z[l - 1] = hull(p.z[l - 1], fold_hull(dlo, dhi, p.H[l - 1]));
     }
   }
+  p.zc = p.z;
+  p.ub = p.u;
+  plan_layout(p, map_es, W, o0 == 0 && on == H);
+}
+
+// Workspace layout of a plan whose row ranges are set (Plan::z, zc, u, ub): level planes, maps,
+// fix-up lists. full_image: the call covers every row (the 16-B-row input copy is possible).
+void plan_layout(Plan& p, int map_es, int W, bool full_image) {
+  const int L = p.L, N = p.N, H = p.H[0];
   size_t off = 0;
   p.z32_off.assign(L, 0);
   p.zlo_off.assign(L, 0);
@@ -249,17 +261,21 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
     p.map_pitch[l] = (p.W[l] + 15) & ~15;
     p.pitch[l] = l == 0 ? p.W[0] : (p.W[l] + 3) & ~3;  // 16-B rows: every level >= 1 is TMA-able
   }
+  // z^l hi planes, directly followed by its lo planes (levels that feed a selector): the six
+  // planes of a level are one uniform-stride run (one region for a halo exchange)
   for (int l = 1; l < L; ++l) {
+    const size_t planes = sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.pitch[l];
     p.z32_off[l] = off;
-    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.pitch[l]);
-  }
-  for (int l = 1; l + 1 < L; ++l) {
-    p.zlo_off[l] = off;
-    off = align256(off + sizeof(float) * (size_t)N * 3 * p.z[l].n() * p.pitch[l]);
+    if (l + 1 < L) {
+      p.zlo_off[l] = off + planes;
+      off = align256(off + 2 * planes);
+    } else {
+      off = align256(off + planes);
+    }
   }
   for (int l = 1; l + 1 < L; ++l) {
     p.u_off[l] = off;
-    off = align256(off + sizeof(float) * (size_t)N * 3 * p.u[l].n() * p.pitch[l]);
+    off = align256(off + sizeof(float) * (size_t)N * 3 * p.ub[l].n() * p.pitch[l]);
   }
   const int nsel = L == 1 ? 1 : L - 1;
   for (int l = 0; l < nsel; ++l) {
@@ -267,7 +283,7 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
     off = align256(off + (size_t)map_es * N * p.u[l].n() * p.map_pitch[l]);
   }
   p.zcopy_pitch = 0;
-  if (W % 4 != 0 && o0 == 0 && on == H) {  // full image whose rows the TMA engine cannot address
+  if (W % 4 != 0 && full_image) {  // full image whose rows the TMA engine cannot address
     p.zcopy_pitch = (W + 3) & ~3;
     p.zcopy_off = off;
     off = align256(off + sizeof(float) * (size_t)N * 3 * H * p.zcopy_pitch);
@@ -286,6 +302,54 @@ void plan_rows_cfg(const blade_ms_config& cfg, int N, int H, int W, int o0, int 
   p.fbcnt_off = off;
   off = align256(off + sizeof(unsigned int) * 16);
   p.ws_bytes = std::max<size_t>(off, 256);
+}
+
+// NEXT f3 (b): the plan of one row band whose neighbours EXCHANGE halo rows between levels
+// (DESIGN.md §10c): the band owns rows own^0 = [o0, o0 + on) and own^{l+1} = [ceil(lo/2),
+// ceil(hi/2)) (a partition of every level when the bands partition the image), computes only
+// those (z^{l+1} by its k_down, u^l and s^l by its stage / selector), and holds hz rows of z^l
+// and hu rows of u^l around them, received from the neighbours. hz covers everything a level's
+// kernels read around own rows: the selector (gradient + window: ws/2 + 1), the decimation
+// (2y-3 .. 2y+4: 4), the fine taps (rf) and, through z^{L-1} = u^{L-1}, the coarse taps of the
+// next finer stage (floor(y/2) +- rc: rc + 1). Returns false when a level of a proper band owns
+// fewer than hz rows (its halo would need rows of a non-adjacent band).
+bool plan_xband(const blade_ms_config& cfg, int map_es, int H, int W, int o0, int on, Plan& p, int& hz, int& hu,
+                std::vector<Range>& own) {
+  const int L = cfg.levels;
+  p.L = L;
+  p.N = 1;
+  p.H.assign(L, 0);
+  p.W.assign(L, 0);
+  p.H[0] = H;
+  p.W[0] = W;
+  for (int l = 1; l < L; ++l) {
+    p.H[l] = (p.H[l - 1] + 1) / 2;
+    p.W[l] = (p.W[l - 1] + 1) / 2;
+  }
+  const int rf = cfg.fine_size / 2, rc = L > 1 ? cfg.coarse_size / 2 : 0;
+  hu = L > 1 ? rc + 1 : 0;
+  hz = std::max(std::max(rf, cfg.window_size / 2 + 1), std::max(L > 1 ? 4 : 0, hu));
+  own.assign(L, Range{});
+  own[0] = Range{o0, o0 + on};
+  for (int l = 1; l < L; ++l) own[l] = Range{(own[l - 1].lo + 1) / 2, (own[l - 1].hi + 1) / 2};
+  const bool whole = o0 == 0 && on == H;
+  for (int l = 0; l < L; ++l)
+    if (!whole && own[l].n() < hz) return false;
+  p.z.assign(L, Range{});
+  p.zc.assign(L, Range{});
+  p.u.assign(L, Range{});
+  p.ub.assign(L, Range{});
+  for (int l = 0; l < L; ++l) {
+    p.z[l] = fold_hull((long long)own[l].lo - hz, (long long)own[l].hi + hz, p.H[l]);
+    p.zc[l] = own[l];
+  }
+  const int nsel = L == 1 ? 1 : L - 1;
+  for (int l = 0; l < nsel; ++l) {
+    p.u[l] = own[l];
+    p.ub[l] = l == 0 ? own[0] : fold_hull((long long)own[l].lo - hu, (long long)own[l].hi + hu, p.H[l]);
+  }
+  plan_layout(p, map_es, W, false);
+  return true;
 }
 
 LevelView make_view(float* base, int H, int W, Range r, int pitch = 0) {
@@ -440,42 +504,58 @@ cudaError_t launch(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
     LAUNCH_CHECK(name);                                                                          \
   } while (0)
 
-// Enqueue the cascade for plan p. in_view: level-0 input (fp32, rows >= p.z[0]); out_view: final
-// output rows p.u[0]. levels_out (diagnostic) receives z^l (fp32) for l >= 1; maps_out the maps.
-blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view, char* ws,
-                     cudaStream_t st, bool run_stages, void* const* maps_out,
-                     float* const* levels_out) {
-  const int L = p.L, N = p.N;
-  if (N == 0) return BLADE_OK;
-  std::vector<LevelView> z32(L);
-  std::vector<float*> zlo(L, nullptr);
-  z32[0] = in_view;
+// Buffers of one cascade call for plan p (views of the workspace, or of caller-provided
+// pyramid levels / maps for the diagnostics).
+struct Bufs {
+  std::vector<LevelView> z32;   // z^l (level 0: the input view)
+  std::vector<float*> zlo;      // lo planes of z^l, 1 <= l <= L-2
+  std::vector<uint8_t*> maps;   // byte addresses of the uint8 / uint16 maps
+  std::vector<int> mpitch;      // entries per map row
+  unsigned int* fb_cnt = nullptr;
+};
+
+Bufs make_bufs(const Plan& p, LevelView in_view, char* ws, void* const* maps_out, float* const* levels_out) {
+  const int L = p.L;
+  Bufs b;
+  b.z32.resize(L);
+  b.zlo.assign(L, nullptr);
+  b.z32[0] = in_view;
   for (int l = 1; l < L; ++l) {
     float* base = (levels_out && levels_out[l - 1]) ? levels_out[l - 1]
                                                     : reinterpret_cast<float*>(ws + p.z32_off[l]);
     // caller-provided pyramid levels are dense (pitch W); the workspace's are padded (p.pitch);
     // the lo plane shares the hi plane's pitch
     const bool dense = levels_out && levels_out[l - 1];
-    z32[l] = make_view(base, p.H[l], p.W[l], p.z[l], dense ? p.W[l] : p.pitch[l]);
-    if (l + 1 < L) zlo[l] = reinterpret_cast<float*>(ws + p.zlo_off[l]);
+    b.z32[l] = make_view(base, p.H[l], p.W[l], p.z[l], dense ? p.W[l] : p.pitch[l]);
+    if (l + 1 < L) b.zlo[l] = reinterpret_cast<float*>(ws + p.zlo_off[l]);
   }
   const int nsel = L == 1 ? 1 : L - 1;
-  std::vector<uint8_t*> maps(nsel);  // byte addresses of uint8 / uint16 maps
-  for (int l = 0; l < nsel; ++l)
-    maps[l] = (maps_out && maps_out[l]) ? static_cast<uint8_t*>(maps_out[l]) : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
-  std::vector<int> mpitch(nsel);  // caller-provided maps are dense [N][H][W]; workspace maps padded
-  for (int l = 0; l < nsel; ++l) mpitch[l] = (maps_out && maps_out[l]) ? p.W[l] : p.map_pitch[l];
-
-  // ---- down pass: k_down(l) -> s^l, z^{l+1} (hi, and lo when level l+1 feeds a selector);
-  //      k_down_fixup(l) recomputes the (rare) pixels whose fp32 orientation is uncertified
-  unsigned int* fb_cnt = reinterpret_cast<unsigned int*>(ws + p.fbcnt_off);
-  std::vector<DownArgs> fix_args;  // per level, for the merged fix-up launch
-  const bool merge_fix = fixups_merged(L == 1 ? 1 : L - 1, N, p.H[0], p.W[0]);
-  CUDA_TRY(cudaMemsetAsync(fb_cnt, 0, sizeof(unsigned int) * nsel, st));
+  b.maps.resize(nsel);
+  b.mpitch.resize(nsel);
   for (int l = 0; l < nsel; ++l) {
+    b.maps[l] = (maps_out && maps_out[l]) ? static_cast<uint8_t*>(maps_out[l]) : reinterpret_cast<uint8_t*>(ws + p.map_off[l]);
+    b.mpitch[l] = (maps_out && maps_out[l]) ? p.W[l] : p.map_pitch[l];  // caller maps are dense
+  }
+  b.fb_cnt = reinterpret_cast<unsigned int*>(ws + p.fbcnt_off);
+  return b;
+}
+
+// Down pass at level l: k_down(l) -> s^l (rows p.u[l]) and z^{l+1} (rows p.zc[l+1] of the buffer
+// p.z[l+1]); unless `fix_args` collects it for the merged launch, k_down_fixup(l) recomputes the
+// (rare) pixels whose fp32 orientation is uncertified. The level's fix-up counter must be zero.
+blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView in_view, char* ws,
+                        cudaStream_t st, bool run_stages, int l, std::vector<DownArgs>* fix_args) {
+  const int L = p.L, N = p.N;
+  const std::vector<LevelView>& z32 = B.z32;
+  const std::vector<float*>& zlo = B.zlo;
+  const std::vector<uint8_t*>& maps = B.maps;
+  const std::vector<int>& mpitch = B.mpitch;
+  unsigned int* fb_cnt = B.fb_cnt;
+  {
     const Range U = p.u[l];
     const bool dec = L > 1;
-    Range Z1 = dec ? p.z[l + 1] : Range{0, 0};
+    const Range Z1 = dec ? p.zc[l + 1] : Range{0, 0};  // rows of z^{l+1} computed
+    const Range Z1b = dec ? p.z[l + 1] : Range{0, 0};  // rows of its buffer
     Range R = U;
     if (dec) R = hull(R, Range{2 * Z1.lo, 2 * Z1.hi});
     DownArgs da{};
@@ -497,8 +577,8 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     da.H1 = dec ? p.H[l + 1] : 1;
     da.W1 = dec ? p.W[l + 1] : 1;
     da.out_pitch = dec ? z32[l + 1].pitch : 1;
-    da.d_buf_row0 = Z1.lo;
-    da.d_buf_rows = Z1.n();
+    da.d_buf_row0 = Z1b.lo;
+    da.d_buf_rows = Z1b.n();
     da.d_r0 = Z1.lo;
     da.d_rn = Z1.n();
     da.base = R.lo & ~1;
@@ -545,17 +625,24 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     auto fn = down_kernel(hilo, dec, fast, wide, zcopy);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
-    if (merge_fix) {
-      fix_args.push_back(da);
+    if (fix_args) {
+      fix_args->push_back(da);
     } else {
       auto fx = fixup_kernel(hilo, fast, wide);
       LAUNCH("k_down_fixup", launch(fx, 8 * h->num_sms, 128, 0, st, true, da, h->down[l]));
     }
   }
+  return BLADE_OK;
+}
+
+// The merged fix-up of every selector level (small, launch-latency-bound calls): one launch per
+// kFixMax levels after the down pass.
+blade_status merged_fixups(const blade_ms* h, const std::vector<DownArgs>& fix_args, cudaStream_t st) {
+  const int nsel = (int)fix_args.size();
   // ---- small (launch-latency-bound) calls: the fix-ups of every level in one launch per
   //      kFixMax levels after the down pass (the stages need them, the next k_down does not; on
   //      large batches the per-level fix-up right after its k_down is faster: 50 vs 70 us on c3)
-  if (merge_fix) {
+  {
     const int l = nsel - 1;  // (LAUNCH's error message)
     const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
     ProfScope ps(h, st, 3, 0);  // kind 3: the merged fix-up
@@ -570,10 +657,19 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
              launch(fixup_multi_kernel(fast, h->K > 256), 8 * h->num_sms, 128, 0, st, true, fm));
     }
   }
-  if (!run_stages) return BLADE_OK;
+  return BLADE_OK;
+}
 
-  // ---- up pass: stage(l)
-  for (int l = nsel - 1; l >= 0; --l) {
+// Up pass at level l: stage(l) -> u^l for rows p.u[l] (l = 0: into out_view; l >= 1: into the
+// workspace buffer of rows p.ub[l]), reading z^l, u^{l+1} (buffer rows p.ub[l+1], or z^{L-1})
+// and s^l.
+blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView out_view, char* ws,
+                      cudaStream_t st, int l) {
+  const int L = p.L, N = p.N;
+  const std::vector<LevelView>& z32 = B.z32;
+  const std::vector<uint8_t*>& maps = B.maps;
+  const std::vector<int>& mpitch = B.mpitch;
+  {
     const Range r = p.u[l];
     LevelView zl = z32[l];
     if (l == 0 && h->has_tma && p.zcopy_pitch > 0)  // the input copy k_down wrote (16-B rows)
@@ -582,9 +678,9 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     if (L > 1)
       u1 = (l + 1 == L - 1) ? z32[L - 1]
                             : make_view(reinterpret_cast<float*>(ws + p.u_off[l + 1]), p.H[l + 1], p.W[l + 1],
-                                        p.u[l + 1], p.pitch[l + 1]);
+                                        p.ub[l + 1], p.pitch[l + 1]);
     LevelView outv = (l == 0) ? out_view
-                              : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], r, p.pitch[l]);
+                              : make_view(reinterpret_cast<float*>(ws + p.u_off[l]), p.H[l], p.W[l], p.ub[l], p.pitch[l]);
     const bool ostage = l == 0 && h->has_tma && p.zcopy_pitch > 0;  // level-0 output via 16-B rows
     if (ostage)
       outv = make_view(reinterpret_cast<float*>(ws + p.ocopy_off), p.H[0], p.W[0], Range{0, p.H[0]}, p.zcopy_pitch);
@@ -680,7 +776,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
                                       per_frame, N, h->cfg.clamp_output));
       }
       if (ostage) LAUNCH("k_copy_rows", copy_out());
-      continue;
+      return BLADE_OK;
     }
     StageArgs a{};
     a.z = zl;
@@ -720,6 +816,28 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
     }
     if (ostage) LAUNCH("k_copy_rows", copy_out());
   }
+  return BLADE_OK;
+}
+
+// Enqueue the cascade for plan p. in_view: level-0 input (fp32, rows >= p.z[0]); out_view: final
+// output rows p.u[0]. levels_out (diagnostic) receives z^l (fp32) for l >= 1; maps_out the maps.
+blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view, char* ws,
+                     cudaStream_t st, bool run_stages, void* const* maps_out, float* const* levels_out) {
+  const int L = p.L, N = p.N;
+  if (N == 0) return BLADE_OK;
+  const Bufs B = make_bufs(p, in_view, ws, maps_out, levels_out);
+  const int nsel = L == 1 ? 1 : L - 1;
+  std::vector<DownArgs> fix_args;  // per level, for the merged fix-up launch
+  const bool merge_fix = fixups_merged(nsel, N, p.H[0], p.W[0]);
+  CUDA_TRY(cudaMemsetAsync(B.fb_cnt, 0, sizeof(unsigned int) * nsel, st));
+  blade_status s;
+  for (int l = 0; l < nsel; ++l)
+    if ((s = down_level(h, p, B, in_view, ws, st, run_stages, l, merge_fix ? &fix_args : nullptr)) != BLADE_OK)
+      return s;
+  if (merge_fix && (s = merged_fixups(h, fix_args, st)) != BLADE_OK) return s;
+  if (!run_stages) return BLADE_OK;
+  for (int l = nsel - 1; l >= 0; --l)
+    if ((s = up_level(h, p, B, out_view, ws, st, l)) != BLADE_OK) return s;
   return BLADE_OK;
 }
 
@@ -1564,6 +1682,118 @@ blade_status blade_ms_denoise_rows(blade_ms_t h, const float* in_band, int32_t i
   LevelView inv = make_view(const_cast<float*>(in_band), H, W, Range{in_row0, in_row0 + in_rows});
   LevelView outv = make_view(out_band, H, W, Range{out_row0, out_row0 + out_rows});
   return enqueue(h, p, inv, outv, (char*)ws, (cudaStream_t)stream, true, nullptr, nullptr);
+}
+
+static blade_status xband_layout_impl(const blade_ms_config& cfg, int map_es, int32_t H, int32_t W, int32_t o0,
+                                      int32_t on, blade_xband_layout* out, Plan* plan_out) {
+  if (H < 1 || W < 1 || (long long)H * W > (1LL << 31) || o0 < 0 || on < 1 || o0 + on > H)
+    return fail(BLADE_EINVAL, "bad band [%d, %d) of %d x %d", o0, o0 + on, H, W);
+  Plan p;
+  int hz = 0, hu = 0;
+  std::vector<Range> own;
+  if (!plan_xband(cfg, map_es, H, W, o0, on, p, hz, hu, own))
+    return fail(BLADE_EUNSUPPORTED, "band [%d, %d) owns fewer than %d rows at some level (use fewer bands or "
+                "blade_ms_denoise_rows)", o0, o0 + on, hz);
+  if (out) {
+    std::memset(out, 0, sizeof(*out));
+    const int L = p.L, nsel = L == 1 ? 1 : L - 1;
+    out->levels = L;
+    out->n_steps = 2 * nsel;
+    out->halo_z = hz;
+    out->halo_u = hu;
+    for (int l = 0; l < L; ++l) {
+      out->own_lo[l] = own[l].lo;
+      out->own_hi[l] = own[l].hi;
+    }
+    out->in_row0 = p.z[0].lo;
+    out->in_rows = p.z[0].n();
+    out->ws_bytes = p.ws_bytes;
+    // regions exchanged after each step: rows [row0, row0 + rows) of `planes` planes
+    auto region = [&](size_t base, Range buf, int pitch, int planes, int row0, int rows) {
+      blade_region r{};
+      if (rows <= 0) return r;
+      r.row0 = row0;
+      r.rows = rows;
+      r.pitch = pitch;
+      r.planes = planes;
+      r.plane_stride = (int64_t)sizeof(float) * buf.n() * pitch;
+      r.offset = (int64_t)base + (int64_t)sizeof(float) * (row0 - buf.lo) * pitch;
+      return r;
+    };
+    for (int st = 0; st < out->n_steps; ++st) {
+      size_t base = 0;
+      Range buf{}, mine{};
+      int planes = 0, pitch = 0;
+      if (L > 1 && st < nsel) {  // after down(l = st): z^{l+1} (hi, and lo when it feeds a selector)
+        const int l1 = st + 1;
+        base = p.z32_off[l1];
+        buf = p.z[l1];
+        mine = p.zc[l1];
+        planes = l1 + 1 < L ? 6 : 3;
+        pitch = p.pitch[l1];
+      } else if (L > 1 && st >= nsel && 2 * nsel - 1 - st >= 1) {  // after up(l >= 1): u^l
+        const int l = 2 * nsel - 1 - st;
+        base = p.u_off[l];
+        buf = p.ub[l];
+        mine = p.u[l];
+        planes = 3;
+        pitch = p.pitch[l];
+      } else {
+        continue;  // nothing to exchange
+      }
+      const int above = mine.lo - buf.lo, below = buf.hi - mine.hi;
+      out->recv[st][0] = region(base, buf, pitch, planes, buf.lo, above);
+      out->send[st][0] = region(base, buf, pitch, planes, mine.lo, above);
+      out->recv[st][1] = region(base, buf, pitch, planes, mine.hi, below);
+      out->send[st][1] = region(base, buf, pitch, planes, mine.hi - below, below);
+    }
+  }
+  if (plan_out) *plan_out = p;
+  return BLADE_OK;
+}
+
+blade_status blade_ms_xband_layout(const blade_ms_config* cfg, int32_t K, int32_t H, int32_t W, int32_t out_row0,
+                                   int32_t out_rows, blade_xband_layout* layout) {
+  if (!cfg || !layout) return fail(BLADE_EINVAL, "NULL argument");
+  if (cfg->levels < 1 || cfg->levels > BLADE_MAX_LEVELS || cfg->fine_size < 1 || cfg->fine_size > 9 ||
+      !(cfg->fine_size & 1) ||
+      (cfg->levels > 1 && (cfg->coarse_size < 1 || cfg->coarse_size > 9 || !(cfg->coarse_size & 1))) ||
+      cfg->window_size < 1 || cfg->window_size > 5 || !(cfg->window_size & 1) || K < 1 || K > 65536)
+    return fail(BLADE_EINVAL, "bad config");
+  return xband_layout_impl(*cfg, K > 256 ? 2 : 1, H, W, out_row0, out_rows, layout, nullptr);
+}
+
+blade_status blade_ms_xband_step(blade_ms_t h, int32_t step, const float* in_band, int32_t in_row0, int32_t in_rows,
+                                 float* out_band, int32_t out_row0, int32_t out_rows, int32_t H, int32_t W, void* ws,
+                                 size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!h) return fail(BLADE_EINVAL, "handle is NULL");
+  blade_status s = check_dims(1, H, W);
+  if (s != BLADE_OK) return s;
+  Plan p;
+  if ((s = xband_layout_impl(h->cfg, h->K > 256 ? 2 : 1, H, W, out_row0, out_rows, nullptr, &p)) != BLADE_OK)
+    return s;
+  const int L = p.L, nsel = L == 1 ? 1 : L - 1;
+  if (step < 0 || step >= 2 * nsel) return fail(BLADE_EINVAL, "step %d outside 0..%d", step, 2 * nsel - 1);
+  if (!in_band || !out_band) return fail(BLADE_EINVAL, "NULL band pointer");
+  if (in_row0 < 0 || in_rows < 1 || in_row0 > p.z[0].lo || in_row0 + in_rows < p.z[0].hi || in_row0 + in_rows > H)
+    return fail(BLADE_ESHAPE, "input band [%d, %d) does not cover the needed rows [%d, %d)", in_row0,
+                in_row0 + in_rows, p.z[0].lo, p.z[0].hi);
+  if ((s = common_checks(h, in_band, 1, ws, ws_bytes, p)) != BLADE_OK) return s;
+  if ((s = check_dev_ptr(h, out_band, "out_band")) != BLADE_OK) return s;
+  if (ranges_overlap(in_band, sizeof(float) * 3 * (size_t)in_rows * W, out_band, sizeof(float) * 3 * (size_t)out_rows * W))
+    return fail(BLADE_EINVAL, "out_band overlaps in_band");
+  DeviceGuard guard(h->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  LevelView inv = make_view(const_cast<float*>(in_band), H, W, Range{in_row0, in_row0 + in_rows});
+  LevelView outv = make_view(out_band, H, W, Range{out_row0, out_row0 + out_rows});
+  const Bufs B = make_bufs(p, inv, (char*)ws, nullptr, nullptr);
+  if (step < nsel) {
+    const int l = step;
+    CUDA_TRY(cudaMemsetAsync(B.fb_cnt + l, 0, sizeof(unsigned int), st));
+    return down_level(h, p, B, inv, (char*)ws, st, true, l, nullptr);
+  }
+  return up_level(h, p, B, outv, (char*)ws, st, 2 * nsel - 1 - step);
 }
 
 blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* out_host, int32_t N, int32_t H,

@@ -645,3 +645,39 @@ def test_deep_pyramid_merged_fixup_overflow():
     d = (gpu[top] // per_o - ob[top] // per_o) % cfg.n_orient
     assert np.isin(d, [0, 1, cfg.n_orient - 1]).all()
     assert (gpu[top] % per_o == ob[top] % per_o).all()
+
+
+# ------------------------------------------------------------------ NEXT f3 (b): halo-exchange bands
+
+@pytest.mark.parametrize("name,H,W,G", [("c4", 900, 260, 2), ("c4", 1200, 333, 8), ("c2", 333, 260, 3),
+                                        ("c1", 257, 100, 5), ("c3", 400, 1918, 4), ("c0", 64, 64, 4),
+                                        ("c5", 512, 384, 3)])
+def test_xband_bands_bit_identical(name, H, W, G):
+    """Bands that exchange per-level halo rows (blade_ms_xband_step + device copies between the
+    bands' workspaces, the single-GPU form of the NCCL exchange) reproduce the whole-frame
+    blade_ms_denoise bit-exactly, for every config recipe (c0: L = 1, nothing to exchange)."""
+    from paper_1802_06130_b200.xband import denoise_bands_local
+    cfg = _cfg_like(name, H, W, 1)
+    h = _handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    full = h.denoise(x)[0]
+    got = denoise_bands_local(h, x, G)
+    torch.cuda.synchronize()
+    assert torch.equal(got, full)
+
+
+def test_xband_step_argument_errors():
+    from paper_1802_06130_b200.blade_ms import BladeError
+    cfg = _cfg_like("c4", 900, 260, 1)
+    h = _handle(cfg)
+    lay = h.xband_layout(900, 260, 300, 300)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    ws = torch.empty(lay["ws_bytes"], dtype=torch.uint8, device="cuda")
+    out = torch.empty((3, 300, 260), device="cuda")
+    band = x[0, :, lay["in_row0"]:lay["in_row0"] + lay["in_rows"]].contiguous()
+    with pytest.raises(BladeError):  # step out of range
+        h.xband_step(lay["n_steps"], band, lay["in_row0"], out, 300, 900, ws)
+    with pytest.raises(BladeError):  # input band misses needed rows
+        h.xband_step(0, band[:, 2:].contiguous(), lay["in_row0"] + 2, out, 300, 900, ws)
+    with pytest.raises(BladeError):  # workspace too small
+        h.xband_step(0, band, lay["in_row0"], out, 300, 900, ws[: lay["ws_bytes"] // 2])
