@@ -40,9 +40,18 @@ struct DownParams {
   float ecos[16], esin[16];  // interior edges 2 pi j / n_o, j = 1 .. n_o/4 - 1
 };
 
+// BLADE_DOWN_PACK (A/B builds, profiles/r02_down_pack.txt): 0 = scalar fp32 window arithmetic,
+// 1 (default) = the vertical window ring
+// as packed fp32x2 FMAs, 2 = products and horizontal window packed too (all bit-identical).
+#ifndef BLADE_DOWN_PACK
+#define BLADE_DOWN_PACK 1
+#endif
 namespace down {
 constexpr int WARPS = 4;        // independent warps per CTA
-constexpr int RING = 8;         // rows in flight per lane (cp.async ring)
+#ifndef BLADE_DOWN_RING
+#define BLADE_DOWN_RING 8
+#endif
+constexpr int RING = BLADE_DOWN_RING;  // rows in flight per lane (cp.async ring)
 constexpr int STRIP = 56;       // output columns per strip
 constexpr int LANE_LO = 2, LANE_HI = 29;
 }  // namespace down
@@ -333,12 +342,13 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
   // fp32 gradient rows (own columns of rows c-1, c; row c at columns x-1, x+2); hi and lo parts
   float hm[3][2], hc[3][2], hL[3], hR[3];
   float lm[3][2], lc[3][2], lL[3], lR[3];
-  float vA[4][2], vB[4][2], vC[4][2];  // pending window rows y = c-1 .. c+2 (after the shift)
+  // pending window rows y = c-1 .. c+2 (after the shift); (x, y) = the lane's two columns, so the
+  // window arithmetic runs as packed fp32x2 FMAs (FFMA2; element-wise identical to fmaf)
+  float2 vA[4], vB[4], vC[4];
   double dacc[4][3];                   // pending decimated rows (4) x channels
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) vA[k][j] = vB[k][j] = vC[k][j] = 0.0f;
+    vA[k] = vB[k] = vC[k] = make_float2(0.0f, 0.0f);
 #pragma unroll
     for (int c = 0; c < 3; ++c) dacc[k][c] = 0.0;
   }
@@ -451,7 +461,25 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
 
     if (i >= 2) {
       // ---- fp32 products at row c = r - 1 for columns x, x+1 (unscaled gradients 2g; at l >= 1
-      //      (hi1 - hi0) + (lo1 - lo0), relative error ~2u of the exact fp64-level difference)
+      //      (hi1 - hi0) + (lo1 - lo0), relative error ~2u of the exact fp64-level difference).
+      //      Packed over the column pair: __ffma2_rn / __fmul2_rn / __fadd2_rn round each element
+      //      exactly as fmaf / * / + do, so the results are those of the scalar form.
+#if BLADE_DOWN_PACK >= 2
+      const float2 m1 = make_float2(-1.0f, -1.0f);
+      float2 A = make_float2(0.0f, 0.0f), B = A, C = A;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float2 gx = __ffma2_rn(make_float2(hL[c], hc[c][0]), m1, make_float2(hc[c][1], hR[c]));
+        float2 gy = __ffma2_rn(make_float2(hm[c][0], hm[c][1]), m1, make_float2(hn[c][0], hn[c][1]));
+        if constexpr (HILO) {
+          gx = __fadd2_rn(gx, __ffma2_rn(make_float2(lL[c], lc[c][0]), m1, make_float2(lc[c][1], lR[c])));
+          gy = __fadd2_rn(gy, __ffma2_rn(make_float2(lm[c][0], lm[c][1]), m1, make_float2(ln[c][0], ln[c][1])));
+        }
+        A = __ffma2_rn(gx, gx, A);
+        B = __ffma2_rn(gx, gy, B);
+        C = __ffma2_rn(gy, gy, C);
+      }
+#else
       float A0 = 0.0f, B0 = 0.0f, C0 = 0.0f, A1 = 0.0f, B1 = 0.0f, C1 = 0.0f;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -470,52 +498,69 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
         B1 = fmaf(gx1, gy1, B1);
         C1 = fmaf(gy1, gy1, C1);
       }
-      // ---- horizontal window: products at x-2, x-1 (lane-1) and x+2, x+3 (lane+1); w symmetric
-      const float Am2 = __shfl_up_sync(0xffffffffu, A0, 1), Am1 = __shfl_up_sync(0xffffffffu, A1, 1);
-      const float Ap2 = __shfl_down_sync(0xffffffffu, A0, 1), Ap3 = __shfl_down_sync(0xffffffffu, A1, 1);
-      const float Bm2 = __shfl_up_sync(0xffffffffu, B0, 1), Bm1 = __shfl_up_sync(0xffffffffu, B1, 1);
-      const float Bp2 = __shfl_down_sync(0xffffffffu, B0, 1), Bp3 = __shfl_down_sync(0xffffffffu, B1, 1);
-      const float Cm2 = __shfl_up_sync(0xffffffffu, C0, 1), Cm1 = __shfl_up_sync(0xffffffffu, C1, 1);
-      const float Cp2 = __shfl_down_sync(0xffffffffu, C0, 1), Cp3 = __shfl_down_sync(0xffffffffu, C1, 1);
-      const float hA[2] = {fmaf(w0, Am2 + Ap2, fmaf(w1, Am1 + A1, w2 * A0)), fmaf(w0, Am1 + Ap3, fmaf(w1, A0 + Ap2, w2 * A1))};
-      const float hB[2] = {fmaf(w0, Bm2 + Bp2, fmaf(w1, Bm1 + B1, w2 * B0)), fmaf(w0, Bm1 + Bp3, fmaf(w1, B0 + Bp2, w2 * B1))};
-      const float hC[2] = {fmaf(w0, Cm2 + Cp2, fmaf(w1, Cm1 + C1, w2 * C0)), fmaf(w0, Cm1 + Cp3, fmaf(w1, C0 + Cp2, w2 * C1))};
+      const float2 A = make_float2(A0, A1), B = make_float2(B0, B1), C = make_float2(C0, C1);
+#endif
+      // ---- horizontal window: products at x-2, x-1 (lane-1) and x+2, x+3 (lane+1); w symmetric:
+      //      h[j] = w0 (p[j-2] + p[j+2]) + (w1 (p[j-1] + p[j+1]) + w2 p[j])
+      const float2 w0v = make_float2(w0, w0), w1v = make_float2(w1, w1), w2v = make_float2(w2, w2);
+      auto hwin = [&](float2 P) {
+        const float2 M = make_float2(__shfl_up_sync(0xffffffffu, P.x, 1), __shfl_up_sync(0xffffffffu, P.y, 1));
+        const float2 Q = make_float2(__shfl_down_sync(0xffffffffu, P.x, 1), __shfl_down_sync(0xffffffffu, P.y, 1));
+#if BLADE_DOWN_PACK >= 2
+        const float2 s2 = __fadd2_rn(M, Q);                                         // (m2+p2, m1+p3)
+        const float2 s1 = __fadd2_rn(make_float2(M.y, P.x), make_float2(P.y, Q.x));  // (m1+p1, p0+p2)
+        return __ffma2_rn(w0v, s2, __ffma2_rn(w1v, s1, __fmul2_rn(w2v, P)));
+#else
+        return make_float2(fmaf(w0, M.x + Q.x, fmaf(w1, M.y + P.y, w2 * P.x)),
+                           fmaf(w0, M.y + Q.y, fmaf(w1, P.x + Q.x, w2 * P.y)));
+#endif
+      };
+      const float2 hA = hwin(A), hB = hwin(B), hC = hwin(C);
       // ---- vertical window: pending rows y = c-2 .. c+2 get weight w[c - y + 2]
       const int y = r - 3;  // = c - 2: completes now
-      const bool emit = i >= 6 && out_lane && y >= a.s_r0 && y < a.s_r0 + a.s_rn;
-      int bk[2];
-      bool need_fb = false;
+#if BLADE_DOWN_PACK >= 1
+      const float2 fa = __ffma2_rn(w0v, hA, vA[0]), fb = __ffma2_rn(w0v, hB, vB[0]), fc = __ffma2_rn(w0v, hC, vC[0]);
+      vA[0] = __ffma2_rn(w1v, hA, vA[1]); vB[0] = __ffma2_rn(w1v, hB, vB[1]); vC[0] = __ffma2_rn(w1v, hC, vC[1]);
+      vA[1] = __ffma2_rn(w2v, hA, vA[2]); vB[1] = __ffma2_rn(w2v, hB, vB[2]); vC[1] = __ffma2_rn(w2v, hC, vC[2]);
+      vA[2] = __ffma2_rn(w1v, hA, vA[3]); vB[2] = __ffma2_rn(w1v, hB, vB[3]); vC[2] = __ffma2_rn(w1v, hC, vC[3]);
+      vA[3] = __fmul2_rn(w0v, hA);        vB[3] = __fmul2_rn(w0v, hB);        vC[3] = __fmul2_rn(w0v, hC);
+#else
+      auto f2 = [](float w, float2 h, float2 v) { return make_float2(fmaf(w, h.x, v.x), fmaf(w, h.y, v.y)); };
+      const float2 fa = f2(w0, hA, vA[0]), fb = f2(w0, hB, vB[0]), fc = f2(w0, hC, vC[0]);
+      vA[0] = f2(w1, hA, vA[1]); vB[0] = f2(w1, hB, vB[1]); vC[0] = f2(w1, hC, vC[1]);
+      vA[1] = f2(w2, hA, vA[2]); vB[1] = f2(w2, hB, vB[2]); vC[1] = f2(w2, hC, vC[2]);
+      vA[2] = f2(w1, hA, vA[3]); vB[2] = f2(w1, hB, vB[3]); vC[2] = f2(w1, hC, vC[3]);
+      vA[3] = make_float2(w0 * hA.x, w0 * hA.y); vB[3] = make_float2(w0 * hB.x, w0 * hB.y);
+      vC[3] = make_float2(w0 * hC.x, w0 * hC.y);
+#endif
+      // the first six rows of a task are its top halo: their window sums are incomplete and never
+      // emitted, so their buckets are not evaluated (warp-uniform)
+      if (i >= 6) {
+        const bool emit = out_lane && y >= a.s_r0 && y < a.s_r0 + a.s_rn;
+        bool safe0 = true, safe1 = true;
+        const int bk0 = bucket32<FAST>(fa.x, fb.x, fc.x, prm, safe0);
+        const int bk1 = bucket32<FAST>(fa.y, fb.y, fc.y, prm, safe1);
+        const bool need_fb = emit && ((x < a.W && !safe0) || (x + 1 < a.W && !safe1));
+        if (need_fb) {  // rare: queue the uncertified pixel(s) for the fp64 fix-up kernel
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float fa = fmaf(w0, hA[j], vA[0][j]), fb = fmaf(w0, hB[j], vB[0][j]), fc = fmaf(w0, hC[j], vC[0][j]);
-        bool safe = true;
-        bk[j] = bucket32<FAST>(fa, fb, fc, prm, safe);
-        need_fb |= emit && x + j < a.W && !safe;
-        (void)safe;
-        vA[0][j] = fmaf(w1, hA[j], vA[1][j]); vB[0][j] = fmaf(w1, hB[j], vB[1][j]); vC[0][j] = fmaf(w1, hC[j], vC[1][j]);
-        vA[1][j] = fmaf(w2, hA[j], vA[2][j]); vB[1][j] = fmaf(w2, hB[j], vB[2][j]); vC[1][j] = fmaf(w2, hC[j], vC[2][j]);
-        vA[2][j] = fmaf(w1, hA[j], vA[3][j]); vB[2][j] = fmaf(w1, hB[j], vB[3][j]); vC[2][j] = fmaf(w1, hC[j], vC[3][j]);
-        vA[3][j] = w0 * hA[j];                vB[3][j] = w0 * hB[j];                vC[3][j] = w0 * hC[j];
-      }
-      if (need_fb) {  // rare: queue the uncertified pixel(s) for the fp64 fix-up kernel
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (x + j >= a.W) continue;
-          const unsigned int slot = atomicAdd(a.fb_count, 1u);
-          if (slot < a.fb_cap)
-            a.fb_list[slot] = ((unsigned long long)n * a.s_rn + (unsigned long long)(y - a.s_r0)) * a.W + x + j;
+          for (int j = 0; j < 2; ++j) {
+            if (x + j >= a.W) continue;
+            const unsigned int slot = atomicAdd(a.fb_count, 1u);
+            if (slot < a.fb_cap)
+              a.fb_list[slot] = ((unsigned long long)n * a.s_rn + (unsigned long long)(y - a.s_r0)) * a.W + x + j;
+          }
         }
-      }
-      if (emit && x < a.W) {
-        MT* mrow = mrow_i;
-        if (map16 && x + 1 < a.W) {  // both entries in one store
-          if constexpr (WIDE)
-            *reinterpret_cast<uint32_t*>(mrow) = (uint32_t)bk[0] | ((uint32_t)bk[1] << 16);
-          else
-            *reinterpret_cast<uint16_t*>(mrow) = (uint16_t)(bk[0] | (bk[1] << 8));
-        } else {
-          mrow[0] = (MT)bk[0];
-          if (x + 1 < a.W) mrow[1] = (MT)bk[1];
+        if (emit && x < a.W) {
+          MT* mrow = mrow_i;
+          if (map16 && x + 1 < a.W) {  // both entries in one store
+            if constexpr (WIDE)
+              *reinterpret_cast<uint32_t*>(mrow) = (uint32_t)bk0 | ((uint32_t)bk1 << 16);
+            else
+              *reinterpret_cast<uint16_t*>(mrow) = (uint16_t)(bk0 | (bk1 << 8));
+          } else {
+            mrow[0] = (MT)bk0;
+            if (x + 1 < a.W) mrow[1] = (MT)bk1;
+          }
         }
       }
     }

@@ -230,8 +230,16 @@ struct StageTmaArgs {
 // (the coarse patch only when it is the RGB z^{L-1}; else plane chn of the YCbCr u^{l+1} is read).
 // WIDE (NEXT f2, K > 256): uint16 bucket tiles and the bank read from global memory (the paper's
 // 16 x 16 x 16 layout is 4.8 MB per stage: L2-resident, not shared-memory resident).
+// BLADE_STAGE_MAXNREG (A/B builds): cap the registers instead of the launch bounds, so that a
+// k_down CTA fits next to the stage CTA on one SM (co-scheduled down / up passes).
+#ifdef BLADE_STAGE_MAXNREG
+#define BLADE_STAGE_BOUNDS(threads) \
+  __maxnreg__((threads) <= 256 ? BLADE_STAGE_MAXNREG : (65536 / (threads)) & ~7)
+#else
+#define BLADE_STAGE_BOUNDS(threads) __launch_bounds__(threads, 1)
+#endif
 template <int NF, int NC, int G, bool CH3, bool WIDE = false, int RY = 2>
-__global__ void __launch_bounds__(32 * (16 / RY) * G, 1)
+__global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
     k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
   using SS = TmaShape<NF, NC, WIDE, RY>;
