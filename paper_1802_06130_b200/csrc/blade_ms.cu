@@ -479,6 +479,25 @@ bool pdl_enabled() {
   }();
   return on;
 }
+// Shared-memory carveout of the launches of the current (small) call: consecutive kernels with
+// different L1 / shared-memory splits make the SMs reconfigure between launches, which small,
+// latency-bound calls feel (c1 flushed 63 -> 58 us, c0 24.6 -> 23.5 us; large batches keep the
+// driver's per-kernel choice: c3's k_down1 is 4% slower with the maximal carveout).
+// profiles/r02_carveout.txt. Set by CarveScope for the duration of one enqueue.
+thread_local int g_carveout = -1;
+struct CarveScope {
+  int saved;
+  explicit CarveScope(int v) : saved(g_carveout) { g_carveout = v; }
+  ~CarveScope() { g_carveout = saved; }
+};
+int small_call_carveout(long long N, long long H, long long W) {
+  static const int force = [] {  // BLADE_CARVEOUT=<percent> forces one on every call (A/B timing)
+    const char* e = getenv("BLADE_CARVEOUT");
+    return e ? atoi(e) : -2;
+  }();
+  if (force >= -1) return force;
+  return N * H * W <= (4LL << 20) ? 100 : -1;
+}
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
                    Args&&... args) {
@@ -487,11 +506,20 @@ cudaError_t launch(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
   lc.blockDim = block;
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl && pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (g_carveout >= 0) {
+    at[na].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+    at[na].val.sharedMemCarveout = (unsigned)g_carveout;
+    ++na;
+  }
   lc.attrs = at;
-  lc.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  lc.numAttrs = na;
   return cudaLaunchKernelEx(&lc, fn, std::forward<Args>(args)...);
 }
 #define LAUNCH(name, expr)                                                                       \
@@ -826,6 +854,7 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   const int L = p.L, N = p.N;
   if (N == 0) return BLADE_OK;
   const Bufs B = make_bufs(p, in_view, ws, maps_out, levels_out);
+  const CarveScope carve(small_call_carveout(N, p.u[0].n(), p.W[0]));
   const int nsel = L == 1 ? 1 : L - 1;
   std::vector<DownArgs> fix_args;  // per level, for the merged fix-up launch
   const bool merge_fix = fixups_merged(nsel, N, p.H[0], p.W[0]);
@@ -1535,38 +1564,61 @@ blade_status blade_ms_train_accumulate(blade_ms_t h, int32_t level, const float*
   LAUNCH_CHECK("k_down (training selector)");
   fixup_kernel(false, fast, wide)<<<4 * h->num_sms, 128, 0, st>>>(da, h->down[l]);
   LAUNCH_CHECK("k_down_fixup (training selector)");
-  // ---- counting sort of the pixels by (phase, bucket), then the segmented fp64 SYRK
-  TrainArgs ta{};
-  ta.z = z;
-  ta.uc = u_clean;
-  ta.u1 = u_coarse;
-  ta.map = w + tp.map_off;
-  ta.N = N;
-  ta.H = H;
-  ta.W = W;
-  ta.H1 = (H + 1) / 2;
-  ta.W1 = (W + 1) / 2;
-  ta.n_phases = h->cfg.n_phases;
-  ta.K = h->K;
-  ta.n_seg = n_seg;
-  ta.count = reinterpret_cast<unsigned int*>(w + tp.cnt_off);
-  ta.cursor = reinterpret_cast<unsigned int*>(w + tp.cur_off);
-  ta.sorted = reinterpret_cast<unsigned int*>(w + tp.sorted_off);
-  ta.E = E;
-  ta.count_out = reinterpret_cast<unsigned long long*>(count);
-  ta.pix_per_cta = 512;
-  CUDA_TRY(cudaMemsetAsync(ta.count, 0, sizeof(unsigned int) * n_seg, st));
+  // ---- counting sort of the pixels by (phase, bucket), then the segmented fp64 SYRK, per group
+  //      of frames whose inputs (z, clean target, coarse input) fit in about half the L2: the
+  //      sorted order scatters every segment's pixels over the group's frames, so the Gram
+  //      kernel's patch gathers hit L2 only while the group stays resident (BLADE_TRAIN_GROUP =
+  //      frames per group overrides; 0 = all frames in one group)
+  const long long frame_bytes = (long long)H * W * 3 * 4 * 2 + (u_coarse ? (long long)((H + 1) / 2) * ((W + 1) / 2) * 12 : 0);
+  static const int group_env = [] {
+    const char* e = getenv("BLADE_TRAIN_GROUP");
+    return e ? atoi(e) : -1;
+  }();
+  int fg = group_env >= 0 ? group_env : (int)std::max<long long>(1, (64LL << 20) / std::max<long long>(frame_bytes, 1));
+  if (fg <= 0 || fg > N) fg = N;
+  static const bool use_mma = [] {  // BLADE_TRAIN_MMA=0: the DFMA accumulation (A/B timing)
+    const char* e = getenv("BLADE_TRAIN_MMA");
+    return !(e && e[0] == '0');
+  }();
   CUDA_TRY(cudaFuncSetAttribute(train_hist(wide), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(unsigned int) * n_seg)));
-  const unsigned g_px = (unsigned)std::min<long long>((px + 255) / 256, 4LL * h->num_sms);
-  train_hist(wide)<<<g_px, 256, sizeof(unsigned int) * n_seg, st>>>(ta);
-  LAUNCH_CHECK("k_train_hist");
-  train_scan()<<<1, 1024, 0, st>>>(ta);
-  LAUNCH_CHECK("k_train_scan");
-  train_scatter(wide)<<<g_px, 256, 0, st>>>(ta);
-  LAUNCH_CHECK("k_train_scatter");
-  v->gram<<<(unsigned)((px + ta.pix_per_cta - 1) / ta.pix_per_cta), 256, 0, st>>>(ta);
-  LAUNCH_CHECK("k_train_gram");
+  CUDA_TRY(cudaFuncSetAttribute(train_scatter(wide), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(2 * sizeof(unsigned int) * n_seg)));
+  const long long plane = (long long)H * W, plane1 = (long long)((H + 1) / 2) * ((W + 1) / 2);
+  for (int f0 = 0; f0 < N; f0 += fg) {
+    const int nf = std::min(fg, N - f0);
+    const long long gpx = (long long)nf * H * W;
+    TrainArgs ta{};
+    ta.z = z + (long long)f0 * 3 * plane;
+    ta.uc = u_clean + (long long)f0 * 3 * plane;
+    ta.u1 = u_coarse ? u_coarse + (long long)f0 * 3 * plane1 : nullptr;
+    ta.map = w + tp.map_off + (size_t)(wide ? 2 : 1) * f0 * plane;
+    ta.N = nf;
+    ta.H = H;
+    ta.W = W;
+    ta.H1 = (H + 1) / 2;
+    ta.W1 = (W + 1) / 2;
+    ta.n_phases = h->cfg.n_phases;
+    ta.K = h->K;
+    ta.n_seg = n_seg;
+    ta.count = reinterpret_cast<unsigned int*>(w + tp.cnt_off);
+    ta.cursor = reinterpret_cast<unsigned int*>(w + tp.cur_off);
+    ta.sorted = reinterpret_cast<unsigned int*>(w + tp.sorted_off);
+    ta.E = E;
+    ta.count_out = reinterpret_cast<unsigned long long*>(count);
+    ta.pix_per_cta = 512;
+    CUDA_TRY(cudaMemsetAsync(ta.count, 0, sizeof(unsigned int) * n_seg, st));
+    const unsigned g_px = (unsigned)std::min<long long>((gpx + 255) / 256, 4LL * h->num_sms);
+    train_hist(wide)<<<g_px, 256, sizeof(unsigned int) * n_seg, st>>>(ta);
+    LAUNCH_CHECK("k_train_hist");
+    train_scan()<<<1, 1024, 0, st>>>(ta);
+    LAUNCH_CHECK("k_train_scan");
+    const unsigned g_sc = (unsigned)std::min<long long>((gpx + 8191) / 8192, 2LL * h->num_sms);
+    train_scatter(wide)<<<g_sc, 512, 2 * sizeof(unsigned int) * n_seg, st>>>(ta);
+    LAUNCH_CHECK("k_train_scatter");
+    (use_mma ? v->gram : v->gram_dfma)<<<(unsigned)((gpx + ta.pix_per_cta - 1) / ta.pix_per_cta), 256, 0, st>>>(ta);
+    LAUNCH_CHECK("k_train_gram");
+  }
   return BLADE_OK;
 }
 

@@ -83,12 +83,34 @@ __global__ void __launch_bounds__(1024) k_train_scan(const TrainArgs a) {
   }
 }
 
+// Counting-sort scatter by chunks of consecutive pixels: a CTA counts its chunk's pixels per
+// segment in shared memory, reserves one contiguous run per segment with a single global atomic,
+// then places the chunk's pixels inside those runs (shared-memory atomics). One global atomic per
+// (chunk, segment) instead of per pixel; a segment's list is a sequence of per-chunk runs.
 template <bool WIDE>
-__global__ void __launch_bounds__(256) k_train_scatter(const TrainArgs a) {
+__global__ void __launch_bounds__(512) k_train_scatter(const TrainArgs a) {
+  extern __shared__ unsigned int sc[];  // [n_seg] chunk counts / placement cursors, [n_seg] bases
+  unsigned int* cnt = sc;
+  unsigned int* base = sc + a.n_seg;
+  constexpr int CHUNK = 8192;
   const long long total = (long long)a.N * a.H * a.W;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const unsigned int pos = atomicAdd(&a.cursor[train_seg<WIDE>(a, (unsigned int)i)], 1u);
-    a.sorted[pos] = (unsigned int)i;
+  for (long long c0 = (long long)blockIdx.x * CHUNK; c0 < total; c0 += (long long)gridDim.x * CHUNK) {
+    const long long c1 = min(total, c0 + CHUNK);
+    for (int i = threadIdx.x; i < a.n_seg; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) atomicAdd(&cnt[train_seg<WIDE>(a, (unsigned int)i)], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.n_seg; i += blockDim.x) {
+      const unsigned int n = cnt[i];
+      base[i] = n ? atomicAdd(&a.cursor[i], n) : 0u;
+      cnt[i] = 0;
+    }
+    __syncthreads();
+    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      const int sg = train_seg<WIDE>(a, (unsigned int)i);
+      a.sorted[base[sg] + atomicAdd(&cnt[sg], 1u)] = (unsigned int)i;
+    }
+    __syncthreads();
   }
 }
 
@@ -249,4 +271,164 @@ __global__ void __launch_bounds__(256) k_train_gram(const TrainArgs a) {
   flush();
 }
 
+
+// ---- k_train_gram_mma: the same accumulation on the FP64 tensor cores (DMMA, mma.sync
+// m8n8k4 .f64). The batch's samples (pixel j, channel c) are the K dimension: for an 8 x 8 block
+// (I, J) of the upper block triangle, D += A B with A[r][k] = x_k[8I + r], B[k][c] = x_k[8J + c]
+// over steps of 4 samples. One warp owns every 8th block; its fragments are loaded straight
+// from the shared sample rows (stride NTPX doubles: the 16 lanes of a half warp hit distinct
+// bank pairs). Samples of another segment inside a 4-sample step are masked to zero, so every
+// MMA adds only the current segment's samples; the segment changes flush with fp64 atomics as
+// before. Entries written: (r, c) with r / 8 <= c / 8 (a superset of E's upper 4 x 4-block
+// triangle contract); rows / columns >= NTP do not exist in E and are skipped.
+template <int NF, int NC>
+struct TrainMmaShape {
+  static constexpr int NT = NF * NF + NC * NC;
+  static constexpr int NTP = (NT + 1 + 3) & ~3;     // E's row pitch (TrainShape)
+  static constexpr int NTP8 = (NT + 1 + 7) & ~7;    // 8-aligned columns of a sample row
+  // sample-row stride in doubles, = 4 (mod 8): the 4 rows x 4 columns a half warp's fragment
+  // loads touch land on 16 distinct 8-byte bank pairs
+  static constexpr int NTPX = NTP8 + 4;
+  static constexpr int NB = NTP8 / 8;
+  static constexpr int UB = NB * (NB + 1) / 2;      // upper 8 x 8 blocks
+  static constexpr int WARPS = 8;
+  static constexpr int BPW = (UB + WARPS - 1) / WARPS;  // blocks per warp
+  static constexpr int BATCH = NTPX <= 64 ? 24 : 16;    // pixels per gather (<= 48 KB static smem)
+};
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int NF, int NC, bool WIDE>
+__global__ void __launch_bounds__(256) k_train_gram_mma(const TrainArgs a) {
+  using TS = TrainMmaShape<NF, NC>;
+  constexpr int NTP = TS::NTP, NTPX = TS::NTPX, NT = TS::NT, B = TS::BATCH;
+  constexpr int RF = NF / 2, RC = NC / 2;
+  static_assert(NTPX % 8 == 4, "sample stride");
+  __shared__ double xs[B * 3][NTPX];
+  __shared__ int segs[B];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int g = lane >> 2, q = lane & 3;  // MMA fragment coordinates
+  // this warp's blocks: b = warp, warp + 8, ...; block index -> (I, J), I <= J
+  int bI[TS::BPW], bJ[TS::BPW];
+  bool act[TS::BPW];
+#pragma unroll
+  for (int k = 0; k < TS::BPW; ++k) {
+    int blk = warp + k * TS::WARPS;
+    act[k] = blk < TS::UB;
+    int r = 0;
+    while (act[k] && blk >= TS::NB - r) {
+      blk -= TS::NB - r;
+      ++r;
+    }
+    bI[k] = r;
+    bJ[k] = r + blk;
+  }
+  double acc[TS::BPW][2];
+#pragma unroll
+  for (int k = 0; k < TS::BPW; ++k) acc[k][0] = acc[k][1] = 0.0;
+
+  const long long total = (long long)a.N * a.H * a.W;
+  const long long r0 = (long long)blockIdx.x * a.pix_per_cta;
+  const long long r1 = min(total, r0 + a.pix_per_cta);
+  int cur = -1;
+  auto flush = [&]() {
+    if (cur < 0) return;
+    double* Es = a.E + (long long)cur * NTP * NTP;
+#pragma unroll
+    for (int k = 0; k < TS::BPW; ++k) {
+      if (!act[k]) continue;
+      const int row = 8 * bI[k] + g, col = 8 * bJ[k] + 2 * q;
+      if (row < NTP) {
+        if (col < NTP) atomicAdd(Es + row * NTP + col, acc[k][0]);
+        if (col + 1 < NTP) atomicAdd(Es + row * NTP + col + 1, acc[k][1]);
+      }
+      acc[k][0] = acc[k][1] = 0.0;
+    }
+  };
+  const unsigned int hw = (unsigned int)a.H * (unsigned int)a.W;
+  __shared__ int pn[B];
+  __shared__ int frow[B][NF], fcol[B][NF];
+  __shared__ int crow[B][NC > 0 ? NC : 1], ccol[B][NC > 0 ? NC : 1];
+  __shared__ int ctr[B];
+  for (int e = t; e < B * 3 * (NTPX - NT - 1); e += 256) {  // padding columns stay zero
+    const int j = e / (NTPX - NT - 1), c = e - j * (NTPX - NT - 1);
+    xs[j][NT + 1 + c] = 0.0;
+  }
+  for (long long b0 = r0; b0 < r1; b0 += B) {
+    const int nb = (int)min((long long)B, r1 - b0);
+    __syncthreads();  // previous batch consumed
+    if (t < nb) {
+      const unsigned int pix = a.sorted[b0 + t];
+      const unsigned int n = pix / hw, r = pix - n * hw;
+      const unsigned int y = r / (unsigned int)a.W;
+      pn[t] = (int)n;
+      ctr[t] = (int)r;
+      segs[t] = train_seg<WIDE>(a, pix);
+      const int yy = (int)y, xx = (int)(r - y * (unsigned int)a.W);
+#pragma unroll
+      for (int d = 0; d < NF; ++d) {
+        frow[t][d] = fold_idx(yy + d - RF, a.H) * a.W;
+        fcol[t][d] = fold_idx(xx + d - RF, a.W);
+      }
+      if constexpr (NC > 0) {
+#pragma unroll
+        for (int d = 0; d < NC; ++d) {
+          crow[t][d] = fold_idx(yy / 2 + d - RC, a.H1) * a.W1;
+          ccol[t][d] = fold_idx(xx / 2 + d - RC, a.W1);
+        }
+      }
+    }
+    __syncthreads();
+    const long long plane = (long long)a.H * a.W, plane1 = (long long)a.H1 * a.W1;
+    for (int e = t; e < nb * 3 * NF * NF; e += 256) {
+      const int j = e / (3 * NF * NF), rem = e - j * (3 * NF * NF);
+      const int c = rem / (NF * NF), tap = rem - c * (NF * NF);
+      const int dy = tap / NF, dx = tap - dy * NF;
+      xs[3 * j + c][tap] = (double)__ldg(a.z + ((long long)pn[j] * 3 + c) * plane + frow[j][dy] + fcol[j][dx]);
+    }
+    if constexpr (NC > 0) {
+      for (int e = t; e < nb * 3 * NC * NC; e += 256) {
+        const int j = e / (3 * NC * NC), rem = e - j * (3 * NC * NC);
+        const int c = rem / (NC * NC), tc = rem - c * (NC * NC);
+        const int dy = tc / NC, dx = tc - dy * NC;
+        xs[3 * j + c][NF * NF + tc] = (double)__ldg(a.u1 + ((long long)pn[j] * 3 + c) * plane1 + crow[j][dy] + ccol[j][dx]);
+      }
+    }
+    for (int e = t; e < nb * 3; e += 256) {
+      const int j = e / 3, c = e - 3 * j;
+      xs[e][NT] = (double)__ldg(a.uc + ((long long)pn[j] * 3 + c) * plane + ctr[j]);
+    }
+    __syncthreads();
+    // ---- runs of one segment within the batch (uniform over the CTA)
+    const int ns = 3 * nb;
+    int pos = 0;
+    while (pos < ns) {
+      const int sg = segs[pos / 3];
+      if (sg != cur) {
+        flush();
+        cur = sg;
+      }
+      int end = pos + 3;
+      while (end < ns && segs[end / 3] == sg) end += 3;
+      for (int k0 = pos & ~3; k0 < end; k0 += 4) {
+        const int smp = k0 + q;
+        const bool ok = smp >= pos && smp < end;
+        const double* xr = &xs[ok ? smp : 0][0];
+#pragma unroll
+        for (int k = 0; k < TS::BPW; ++k) {
+          if (!act[k]) continue;  // warp-uniform
+          const double av = ok ? xr[8 * bI[k] + g] : 0.0;
+          const double bv = ok ? xr[8 * bJ[k] + g] : 0.0;
+          dmma_884(acc[k][0], acc[k][1], av, bv);
+        }
+      }
+      pos = end;
+    }
+  }
+  flush();
+}
 }  // namespace blade

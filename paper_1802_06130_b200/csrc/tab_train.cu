@@ -5,7 +5,8 @@ namespace blade {
 namespace tables {
 template <int NF, int NC, bool WIDE>
 static TrainVariant make_train() {
-  return TrainVariant{NF, NC, TrainShape<NF, NC>::NTP, &k_train_gram<NF, NC, WIDE>, WIDE};
+  return TrainVariant{NF, NC, TrainShape<NF, NC>::NTP, &k_train_gram_mma<NF, NC, WIDE>, WIDE,
+                      &k_train_gram<NF, NC, WIDE>};
 }
 const std::vector<TrainVariant>& train_variants() {
   static const std::vector<TrainVariant> v = {

@@ -52,8 +52,9 @@ FixupMultiKernel fixup_multi_kernel(bool fast, bool wide);
 using TrainKernel = void (*)(const TrainArgs);
 struct TrainVariant {
   int nf, nc, ntp;
-  TrainKernel gram;
+  TrainKernel gram;      // FP64 tensor-core (DMMA) accumulation
   bool wide;
+  TrainKernel gram_dfma; // the same on the FP64 CUDA cores (BLADE_TRAIN_MMA=0)
 };
 const std::vector<TrainVariant>& train_variants();
 TrainKernel train_hist(bool wide);
