@@ -164,6 +164,10 @@ struct blade_ms {
   TmaVariant tma{};
   bool has_tma4 = false;  // the 4-rows-per-thread variant of the same shape (large levels)
   TmaVariant tma4{};
+  // fused selector at level 0 (the 4-row TMA stage computes s^0 itself; k_down only decimates)
+  bool has_fsel = false;
+  size_t fsel_smem = 0;
+  StageFixKernel sfix = nullptr;
   size_t tma_smem = 0;
   // profiling (blade_ms_set_profiling): event pairs around each launch
   struct ProfRec { int kind, level; cudaEvent_t e0, e1; };
@@ -540,6 +544,7 @@ struct Bufs {
   std::vector<uint8_t*> maps;   // byte addresses of the uint8 / uint16 maps
   std::vector<int> mpitch;      // entries per map row
   unsigned int* fb_cnt = nullptr;
+  bool fuse0 = false;           // level 0 runs the fused-selector stage (decimation-only k_down)
 };
 
 Bufs make_bufs(const Plan& p, LevelView in_view, char* ws, void* const* maps_out, float* const* levels_out) {
@@ -568,11 +573,50 @@ Bufs make_bufs(const Plan& p, LevelView in_view, char* ws, void* const* maps_out
   return b;
 }
 
+bool use_ry4(const blade_ms* h, int N, int W, int span);
+// BLADE_FUSE_SEL=1 turns the fused level-0 selector on (A/B builds; default off: measured slower,
+// profiles/r02_fused_selector.txt — the stage's 8 warps per SM cannot hide the selector's
+// dependent ALU chains under its shared-memory time: c3 stage0 2.36 -> 3.61 ms against k_down0
+// 1.23 -> 0.56 ms)
+bool fuse_sel_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BLADE_FUSE_SEL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+// Level-0 views of a call (the TMA stage reads the 16-B-row input copy / writes the staging output
+// when the caller's rows are ragged) and whether the fused-selector stage runs there: the same
+// conditions as up_level's TMA path for the 4-row variant.
+struct Level0Views {
+  LevelView zl, outv;
+  bool ostage = false;
+};
+Level0Views level0_views(const blade_ms* h, const Plan& p, LevelView in_view, LevelView out_view, char* ws) {
+  Level0Views v{in_view, out_view, false};
+  if (h->has_tma && p.zcopy_pitch > 0) {
+    v.zl = make_view(reinterpret_cast<float*>(ws + p.zcopy_off), p.H[0], p.W[0], Range{0, p.H[0]}, p.zcopy_pitch);
+    v.outv = make_view(reinterpret_cast<float*>(ws + p.ocopy_off), p.H[0], p.W[0], Range{0, p.H[0]}, p.zcopy_pitch);
+    v.ostage = true;
+  }
+  return v;
+}
+bool fused_level0(const blade_ms* h, const Plan& p, const Bufs& B, LevelView in_view, LevelView out_view, char* ws,
+                  bool run_stages) {
+  if (!h->has_fsel || !run_stages || p.L < 2 || !fuse_sel_enabled()) return false;
+  const Level0Views v = level0_views(h, p, in_view, out_view, ws);
+  const LevelView u1 = p.L == 2 ? B.z32[1] : make_view(reinterpret_cast<float*>(ws + p.u_off[1]), p.H[1], p.W[1], p.ub[1], p.pitch[1]);
+  const int y_base = p.u[0].lo & ~1;
+  return use_ry4(h, p.N, p.W[0], p.u[0].hi - y_base) && v.zl.pitch % 4 == 0 && v.outv.pitch % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(v.zl.p) & 15) == 0 && (reinterpret_cast<uintptr_t>(v.outv.p) & 15) == 0 &&
+         u1.pitch % 4 == 0 && (reinterpret_cast<uintptr_t>(u1.p) & 15) == 0;
+}
+
 // Down pass at level l: k_down(l) -> s^l (rows p.u[l]) and z^{l+1} (rows p.zc[l+1] of the buffer
 // p.z[l+1]); unless `fix_args` collects it for the merged launch, k_down_fixup(l) recomputes the
 // (rare) pixels whose fp32 orientation is uncertified. The level's fix-up counter must be zero.
 blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView in_view, char* ws,
-                        cudaStream_t st, bool run_stages, int l, std::vector<DownArgs>* fix_args) {
+                        cudaStream_t st, bool run_stages, int l, std::vector<std::pair<int, DownArgs>>* fix_args) {
   const int L = p.L, N = p.N;
   const std::vector<LevelView>& z32 = B.z32;
   const std::vector<float*>& zlo = B.zlo;
@@ -650,11 +694,14 @@ blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelVi
     const bool hilo = l > 0;
     const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
     const bool wide = h->K > 256;
-    auto fn = down_kernel(hilo, dec, fast, wide, zcopy);
+    const bool fused = l == 0 && B.fuse0;  // the level-0 stage computes s^0: decimation only
+    auto fn = fused ? dec_kernel(zcopy) : down_kernel(hilo, dec, fast, wide, zcopy);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
-    if (fix_args) {
-      fix_args->push_back(da);
+    if (fused) {
+      // no map, no fix-up list at this level
+    } else if (fix_args) {
+      fix_args->emplace_back(l, da);
     } else {
       auto fx = fixup_kernel(hilo, fast, wide);
       LAUNCH("k_down_fixup", launch(fx, 8 * h->num_sms, 128, 0, st, true, da, h->down[l]));
@@ -665,8 +712,9 @@ blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelVi
 
 // The merged fix-up of every selector level (small, launch-latency-bound calls): one launch per
 // kFixMax levels after the down pass.
-blade_status merged_fixups(const blade_ms* h, const std::vector<DownArgs>& fix_args, cudaStream_t st) {
+blade_status merged_fixups(const blade_ms* h, const std::vector<std::pair<int, DownArgs>>& fix_args, cudaStream_t st) {
   const int nsel = (int)fix_args.size();
+  if (nsel == 0) return BLADE_OK;
   // ---- small (launch-latency-bound) calls: the fix-ups of every level in one launch per
   //      kFixMax levels after the down pass (the stages need them, the next k_down does not; on
   //      large batches the per-level fix-up right after its k_down is faster: 50 vs 70 us on c3)
@@ -678,8 +726,8 @@ blade_status merged_fixups(const blade_ms* h, const std::vector<DownArgs>& fix_a
       FixupMulti fm{};
       fm.n = std::min(kFixMax, nsel - l0);
       for (int q = 0; q < fm.n; ++q) {
-        fm.a[q] = fix_args[l0 + q];
-        fm.prm[q] = h->down[l0 + q];
+        fm.a[q] = fix_args[l0 + q].second;
+        fm.prm[q] = h->down[fix_args[l0 + q].first];
       }
       LAUNCH("k_down_fixup_multi",
              launch(fixup_multi_kernel(fast, h->K > 256), 8 * h->num_sms, 128, 0, st, true, fm));
@@ -702,6 +750,7 @@ blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView
     LevelView zl = z32[l];
     if (l == 0 && h->has_tma && p.zcopy_pitch > 0)  // the input copy k_down wrote (16-B rows)
       zl = make_view(reinterpret_cast<float*>(ws + p.zcopy_off), p.H[0], p.W[0], Range{0, p.H[0]}, p.zcopy_pitch);
+    const bool fused = l == 0 && B.fuse0;  // this stage computes s^0 (fused selector)
     LevelView u1{};
     if (L > 1)
       u1 = (l + 1 == L - 1) ? z32[L - 1]
@@ -724,18 +773,20 @@ blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView
     ProfScope ps(h, st, 2, l);
     // TMA path: needs 16-B aligned buffers whose row pitches are 16-B multiples
     const int map_es = h->K > 256 ? 2 : 1;
-    bool use_tma = h->has_tma && zl.pitch % 4 == 0 && outv.pitch % 4 == 0 && (mpitch[l] * map_es) % 16 == 0 &&
-                   aligned16(zl.p) && aligned16(outv.p) && aligned16(maps[l]) &&
-                   (L == 1 || (u1.pitch % 4 == 0 && aligned16(u1.p)));
+    bool use_tma = h->has_tma && zl.pitch % 4 == 0 && outv.pitch % 4 == 0 &&
+                   (fused || ((mpitch[l] * map_es) % 16 == 0 && aligned16(maps[l]))) && aligned16(zl.p) &&
+                   aligned16(outv.p) && (L == 1 || (u1.pitch % 4 == 0 && aligned16(u1.p)));
     CUtensorMap tmz, tmu, tmm;
     if (use_tma) {
       const TmaVariant& tv = h->tma;
-      use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb, tv.fr, 3,
-                          zl.pitch) &&
-                (h->K > 256 ? encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p.W[l], r.n(), N, tv.tcols,
-                                        tv.trows, 1, mpitch[l])
-                            : encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.W[l], r.n(), N, tv.tcols,
-                                        tv.trows, 1, mpitch[l]));
+      use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb,
+                          fused ? h->tma4.fsel_fr : tv.fr, 3, zl.pitch) &&
+                (fused ? true
+                 : h->K > 256 ? encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p.W[l], r.n(), N, tv.tcols,
+                                          tv.trows, 1, mpitch[l])
+                              : encode_3d(&tmm, maps[l], CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, p.W[l], r.n(), N, tv.tcols,
+                                          tv.trows, 1, mpitch[l]));
+      if (fused) tmm = tmz;  // unused by the fused kernel
       if (use_tma) {
         if (L > 1)
           use_tma = encode_3d(&tmu, u1.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l + 1], u1.rows, N * 3, tv.ccb,
@@ -745,7 +796,7 @@ blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView
       }
     }
     if (use_tma) {
-      const TmaVariant& tv = use_ry4(h, N, p.W[l], r.hi - y_base) ? h->tma4 : h->tma;
+      const TmaVariant& tv = (fused || use_ry4(h, N, p.W[l], r.hi - y_base)) ? h->tma4 : h->tma;
       StageTmaArgs a{};
       a.H = p.H[l];
       a.W = p.W[l];
@@ -791,6 +842,53 @@ blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView
         a.u_rgb = (L > 1 && l + 1 == L - 1) ? 1 : 0;
         a.clamp = 0;  // clamped after the colour conversion
         LAUNCH("k_stage_tma", launch(tv.fn, 3 * per_ch, dim3(32, tv.by * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
+      } else if (fused) {
+        // fused selector: k_down's level-0 selector arithmetic inside the stage; the uncertified
+        // pixels are then recomputed (fp64 bucket + Eq. 9) by k_stage_fixup
+        const DownParams& dp = h->down[0];
+        a.sw0 = (float)dp.wp[0];
+        a.sw1 = (float)dp.wp[1];
+        a.sw2 = (float)dp.wp[2];
+        a.ts2[0] = dp.ts2[0];
+        a.ts2[1] = dp.ts2[1];
+        a.kc2[0] = dp.kc2[0];
+        a.kc2[1] = dp.kc2[1];
+        a.tc_nonpos = dp.tc_nonpos;
+        a.fb_list = reinterpret_cast<unsigned long long*>(ws + p.fb_off[0]);
+        a.fb_count = B.fb_cnt;
+        a.fb_cap = p.fb_cap[0];
+        const int grid = std::min(h->num_sms, a.n_tiles);
+        LAUNCH("k_stage_tma(fused selector)", launch(tv.fsel_fn, grid, dim3(32, tv.by * tv.groups), h->fsel_smem, st,
+                                                     true, tmz, tmu, tmm, a));
+        StageFixArgs fa{};
+        fa.z = zl.p;
+        fa.z_row0 = zl.row0;
+        fa.z_rows = zl.rows;
+        fa.z_pitch = zl.pitch;
+        fa.u1 = u1.p;
+        fa.u_row0 = u1.row0;
+        fa.u_rows = u1.rows;
+        fa.u_pitch = u1.pitch;
+        fa.out = outv.p;
+        fa.out_row0 = outv.row0;
+        fa.out_rows = outv.rows;
+        fa.out_pitch = outv.pitch;
+        fa.H = p.H[0];
+        fa.W = p.W[0];
+        fa.H1 = p.H[1];
+        fa.W1 = p.W[1];
+        fa.N = N;
+        fa.o_r0 = r.lo;
+        fa.o_rn = r.n();
+        fa.bank = bank;
+        fa.S = h->S;
+        fa.PS = h->PS;
+        fa.n_phases = h->cfg.n_phases;
+        fa.clamp = clamp;
+        fa.fb_list = a.fb_list;
+        fa.fb_count = a.fb_count;
+        fa.fb_cap = a.fb_cap;
+        LAUNCH("k_stage_fixup", launch(h->sfix, 8 * h->num_sms, 128, 0, st, true, fa, h->down[0]));
       } else {
         const int grid = std::min(h->num_sms, a.n_tiles);  // small levels: one tile per SM
         LAUNCH("k_stage_tma", launch(tv.fn, grid, dim3(32, tv.by * tv.groups), h->tma_smem, st, true, tmz, tmu, tmm, a));
@@ -853,10 +951,11 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
                      cudaStream_t st, bool run_stages, void* const* maps_out, float* const* levels_out) {
   const int L = p.L, N = p.N;
   if (N == 0) return BLADE_OK;
-  const Bufs B = make_bufs(p, in_view, ws, maps_out, levels_out);
+  Bufs B = make_bufs(p, in_view, ws, maps_out, levels_out);
+  B.fuse0 = !maps_out && !levels_out && fused_level0(h, p, B, in_view, out_view, ws, run_stages);
   const CarveScope carve(small_call_carveout(N, p.u[0].n(), p.W[0]));
   const int nsel = L == 1 ? 1 : L - 1;
-  std::vector<DownArgs> fix_args;  // per level, for the merged fix-up launch
+  std::vector<std::pair<int, DownArgs>> fix_args;  // (level, args), for the merged fix-up launch
   const bool merge_fix = fixups_merged(nsel, N, p.H[0], p.W[0]);
   CUDA_TRY(cudaMemsetAsync(B.fb_cnt, 0, sizeof(unsigned int) * nsel, st));
   blade_status s;
@@ -1036,6 +1135,19 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     }
   }
 
+  // ---- fused selector at level 0: the 4-row shared-bank pair stage with the
+  //      configs' bucket layout and a 5 x 5 window
+  if (h->has_tma && h->has_tma4 && !h->tma.phase_split && h->tma4.fsel_fn && !ch3 && !wide &&
+      c.window_size == 5 && c.levels > 1 && h->n_o == 16 && h->n_s == 3 && h->n_c == 3) {
+    const size_t bank = ((size_t)c.n_phases * h->PS_tma * 4 + 127) & ~size_t(127);
+    const size_t smem = 2 * (size_t)h->tma4.fsel_stage_bytes + bank + 32;
+    h->sfix = stage_fixup_kernel(c.fine_size, cnc);
+    if (smem <= (size_t)max_smem && h->sfix) {
+      h->has_fsel = true;
+      h->fsel_smem = smem;
+    }
+  }
+
   // ---- selector parameters per stage (window weights fp64 -> fp32; thresholds pre-transformed)
   const int r = c.window_size / 2;
   double e[8], se = 0.0;
@@ -1119,6 +1231,8 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     ce = cudaFuncSetAttribute(h->tma.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
   if (ce == cudaSuccess && h->has_tma && h->has_tma4)
     ce = cudaFuncSetAttribute(h->tma4.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->tma_smem);
+  if (ce == cudaSuccess && h->has_fsel)
+    ce = cudaFuncSetAttribute(h->tma4.fsel_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->fsel_smem);
   if (ce == cudaSuccess) {
     for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl)
       for (int dc = 0; dc < 2 && ce == cudaSuccess; ++dc)
@@ -1242,8 +1356,12 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
   // k_down + k_stage per stage level, one merged fix-up per kFixMax levels (+ the YCbCr -> RGB
   // conversion with per-channel banks, + the copy-out of a staged level-0 output)
   const int nsel = L == 1 ? 1 : L - 1;
+  // fused level-0 selector (large frames): the level's fix-up is the stage fix-up (one launch
+  // either way), and it leaves the merged fix-ups
+  const bool fused = h->has_fsel && L > 1 && fuse_sel_enabled() && use_ry4(h, N, W, H + (H & 1));
+  const int merged = fused ? nsel - 1 : nsel;
   *count = N == 0 ? 0
-                  : 2 * nsel + (fixups_merged(nsel, N, H, W) ? (nsel + kFixMax - 1) / kFixMax : nsel) +
+                  : 2 * nsel + (fixups_merged(nsel, N, H, W) ? (merged + kFixMax - 1) / kFixMax + (fused ? 1 : 0) : nsel) +
                         (h->cfg.n_filter_channels == 3 ? 1 : 0) + (h->has_tma && W % 4 != 0 ? 1 : 0);
   return BLADE_OK;
 }
@@ -1839,7 +1957,8 @@ blade_status blade_ms_xband_step(blade_ms_t h, int32_t step, const float* in_ban
   cudaStream_t st = (cudaStream_t)stream;
   LevelView inv = make_view(const_cast<float*>(in_band), H, W, Range{in_row0, in_row0 + in_rows});
   LevelView outv = make_view(out_band, H, W, Range{out_row0, out_row0 + out_rows});
-  const Bufs B = make_bufs(p, inv, (char*)ws, nullptr, nullptr);
+  Bufs B = make_bufs(p, inv, (char*)ws, nullptr, nullptr);
+  B.fuse0 = fused_level0(h, p, B, inv, outv, (char*)ws, true);
   if (step < nsel) {
     const int l = step;
     CUDA_TRY(cudaMemsetAsync(B.fb_cnt + l, 0, sizeof(unsigned int), st));

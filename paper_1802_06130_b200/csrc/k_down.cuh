@@ -266,7 +266,9 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
 // grid: ceil(n_tasks / WARPS) CTAs of 32 * WARPS threads; task = (frame, band, strip), strip fastest.
 // COPY (level 0 only): also write the input rows into a.zcopy (16-B row pitch) for the TMA stage
 // when the caller's rows are not 16-B multiples.
-template <bool HILO, bool DEC, bool FAST, bool WIDE, bool COPY = false>
+// SEL = false (level 0 when the stage computes the selector itself, DESIGN.md §6 "fused
+// selector"): decimation (and COPY) only; no map, no fix-up list.
+template <bool HILO, bool DEC, bool FAST, bool WIDE, bool COPY = false, bool SEL = true>
 __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const DownArgs a, const DownParams prm) {
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;  // bucket map entry
   using namespace down;
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
       }
     }
 
-    if (i >= 2) {
+    if (SEL && i >= 2) {
       // ---- fp32 products at row c = r - 1 for columns x, x+1 (unscaled gradients 2g; at l >= 1
       //      (hi1 - hi0) + (lo1 - lo0), relative error ~2u of the exact fp64-level difference).
       //      Packed over the column pair: __ffma2_rn / __fmul2_rn / __fadd2_rn round each element

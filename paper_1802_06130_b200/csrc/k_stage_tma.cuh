@@ -22,6 +22,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "k_down.cuh"
 #include "kernels.cuh"
 
 namespace blade {
@@ -171,18 +172,23 @@ __device__ __forceinline__ void load_tap_row(const float* tp, int dy, float* t) 
 // RY: pixel rows per thread (2 or 4); a tile is always 16 x 128 outputs, so RY = 4 runs 4 warps
 // per group (one window row then feeds 4 pixel rows instead of 2: fewer shared-memory wavefronts
 // per pixel, 8 warps per SM).
-template <int NF, int NC, bool WIDE = false, int RY_ = 2>
+// FSEL (fused selector, level 0): the fine box carries FH = max(RF, 3) halo rows so that the
+// kernel computes the bucket map of its own tile (gradient 1 + window 2 rows) instead of loading
+// it; the FIR reads the box from row FRO = FH - RF.
+template <int NF, int NC, bool WIDE = false, int RY_ = 2, bool FSEL = false>
 struct TmaShape {
   static constexpr int RX = 4, RY = RY_, BX = 32, BY = 16 / RY_;
   static constexpr int threads = BX * BY;
   static constexpr int RF = NF / 2, RC = NC / 2;
+  static constexpr int FH = FSEL ? (RF > 3 ? RF : 3) : RF;
+  static constexpr int FRO = FH - RF;
   static constexpr int TCOLS = BX * RX, TROWS = BY * RY;  // 128 x 16 outputs per tile
   // TMA box starts must be 16-B aligned in the innermost dimension (a box at column 2 faults with
   // an illegal instruction: scripts/probes/tma_probe.cu), so both boxes start 4 columns left of
   // the tile (covers halos up to 4) and the windows start at FO / CO inside.
   static constexpr int FM = 4, CM = 4;
   static constexpr int FO = FM - RF, CO = CM - RC;
-  static constexpr int FR = TROWS + 2 * RF;
+  static constexpr int FR = TROWS + 2 * FH;
   static constexpr int FCB = TCOLS + 2 * FM;            // 136
   static constexpr int CR = NC ? TROWS / 2 + 2 * RC : 0;
   static constexpr int CCB = NC ? TCOLS / 2 + 2 * CM : 0;  // 72
@@ -219,7 +225,109 @@ struct StageTmaArgs {
   int clamp;
   int u_rgb;           // CH3 (k_stage_ph): the coarse input is RGB z^{L-1}, not YCbCr planes
   int z_pitch, u_pitch, out_pitch;  // floats per row of the z^l, u^{l+1} and output buffers
+  // FSEL: the selector of the tile (FAST layout), fp32 with the certificate of k_down; the
+  // uncertified in-range pixels are queued (map-index format of k_down) for k_stage_fixup
+  float sw0, sw1, sw2;            // window weights at offsets 2, 1, 0 (symmetric)
+  float ts2[2], kc2[2];           // DownParams' transformed thresholds
+  int tc_nonpos;
+  unsigned long long* fb_list;
+  unsigned int* fb_count;
+  unsigned int fb_cap;
 };
+
+// FSEL: buckets of the thread's RY x 4 pixels (rows y .. y+RY-1, cols x .. x+3) from the box
+// `sf` (3 planes of FR x FCB, box origin (Y0 - FH, X0 - FM)): the arithmetic of k_down (level 0:
+// exact fp32 inputs) — unscaled central differences, products summed over the channels with
+// fmaf, the 5-tap horizontal window, then the vertical window as the same 4-deep ring of fmaf —
+// and its certified fp32 decision. Streams the RY + 6 box rows y-3 .. y+RY+2 (columns x-4 ..
+// x+7, three LDS.128 per row and channel), one product row per (not unrolled) iteration; the
+// buckets go to the tile's shared map (the thread's own entries, read back by the same thread)
+// and the uncertified in-range pixels to the fix-up list.
+template <int RY, int FR, int FCB, int FH, int TCOLS>
+__device__ __forceinline__ void fused_buckets(const float* sf, uint8_t* smap, int ty, int tx, int n, int y, int x,
+                                              const StageTmaArgs& a) {
+  DownParams prm;
+  prm.ts2[0] = a.ts2[0];
+  prm.ts2[1] = a.ts2[1];
+  prm.kc2[0] = a.kc2[0];
+  prm.kc2[1] = a.kc2[1];
+  prm.tc_nonpos = a.tc_nonpos;
+  const float* zb = sf + (RY * ty + FH - 3) * FCB + 4 * tx;  // box row of y - 3, column of x - 4
+  float zp[3][8], zc[3][10];  // Z(r - 1) at columns x-2 .. x+5, Z(r) at x-3 .. x+6
+  auto load_row = [&](int rr, int c, float* v12) {
+    const float* p = zb + (c * FR + rr) * FCB;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const float4 t = *reinterpret_cast<const float4*>(p + 4 * q);
+      v12[4 * q] = t.x; v12[4 * q + 1] = t.y; v12[4 * q + 2] = t.z; v12[4 * q + 3] = t.w;
+    }
+  };
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    float v[12];
+    load_row(0, c, v);  // y - 3
+#pragma unroll
+    for (int k = 0; k < 8; ++k) zp[c][k] = v[k + 2];
+    load_row(1, c, v);  // y - 2
+#pragma unroll
+    for (int k = 0; k < 10; ++k) zc[c][k] = v[k + 1];
+  }
+  float vA[4][4], vB[4][4], vC[4][4];  // pending window rows (k_down's ring), 4 columns
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) vA[k][j] = vB[k][j] = vC[k][j] = 0.0f;
+  const float w0 = a.sw0, w1 = a.sw1, w2 = a.sw2;
+  // product rows pr = y-2 .. y+RY+1; output row pr - 2 completes from s = 4 on
+#pragma unroll 1
+  for (int s = 0; s < RY + 4; ++s) {
+    float A[8], B[8], C[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) A[k] = B[k] = C[k] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float zn[12];
+      load_row(s + 2, c, zn);  // Z(pr + 1) at columns x-4 .. x+7
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // column x - 2 + k
+        const float gx = zc[c][k + 2] - zc[c][k];
+        const float gy = zn[k + 2] - zp[c][k];
+        A[k] = fmaf(gx, gx, A[k]);
+        B[k] = fmaf(gx, gy, B[k]);
+        C[k] = fmaf(gy, gy, C[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) zp[c][k] = zc[c][k + 1];
+#pragma unroll
+      for (int k = 0; k < 10; ++k) zc[c][k] = zn[k + 1];
+    }
+    const int yy = y + s - 4;
+    uint32_t word = 0;
+    bool emit = s >= 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // output column x + j <-> products k = j + 2
+      const float hA = fmaf(w0, A[j] + A[j + 4], fmaf(w1, A[j + 1] + A[j + 3], w2 * A[j + 2]));
+      const float hB = fmaf(w0, B[j] + B[j + 4], fmaf(w1, B[j + 1] + B[j + 3], w2 * B[j + 2]));
+      const float hC = fmaf(w0, C[j] + C[j + 4], fmaf(w1, C[j + 1] + C[j + 3], w2 * C[j + 2]));
+      const float fa = fmaf(w0, hA, vA[0][j]), fb = fmaf(w0, hB, vB[0][j]), fc = fmaf(w0, hC, vC[0][j]);
+      if (emit) {
+        bool ok = true;
+        const int bk = bucket32<true>(fa, fb, fc, prm, ok);
+        word |= (uint32_t)bk << (8 * j);
+        if (!ok && yy >= a.o_r0 && yy < a.o_r0 + a.o_rn && x + j < a.W) {  // rare
+          const unsigned int slot = atomicAdd(a.fb_count, 1u);
+          if (slot < a.fb_cap)
+            a.fb_list[slot] = ((unsigned long long)n * a.o_rn + (unsigned long long)(yy - a.o_r0)) * a.W + x + j;
+        }
+      }
+      vA[0][j] = fmaf(w1, hA, vA[1][j]); vB[0][j] = fmaf(w1, hB, vB[1][j]); vC[0][j] = fmaf(w1, hC, vC[1][j]);
+      vA[1][j] = fmaf(w2, hA, vA[2][j]); vB[1][j] = fmaf(w2, hB, vB[2][j]); vC[1][j] = fmaf(w2, hC, vC[2][j]);
+      vA[2][j] = fmaf(w1, hA, vA[3][j]); vB[2][j] = fmaf(w1, hB, vB[3][j]); vC[2][j] = fmaf(w1, hC, vC[3][j]);
+      vA[3][j] = w0 * hA;                vB[3][j] = w0 * hB;                vC[3][j] = w0 * hC;
+    }
+    if (emit) *reinterpret_cast<uint32_t*>(smap + (RY * ty + s - 4) * TCOLS + 4 * tx) = word;
+  }
+}
 
 // G = 1: one 256-thread group, double-buffered tiles (TMA of tile i+1 overlaps tile i).
 // G = 2: two 256-thread groups (16 warps) share the bank; each group owns one tile buffer and works
@@ -238,11 +346,12 @@ struct StageTmaArgs {
 #else
 #define BLADE_STAGE_BOUNDS(threads) __launch_bounds__(threads, 1)
 #endif
-template <int NF, int NC, int G, bool CH3, bool WIDE = false, int RY = 2>
+template <int NF, int NC, int G, bool CH3, bool WIDE = false, int RY = 2, bool FSEL = false>
 __global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
     k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
-  using SS = TmaShape<NF, NC, WIDE, RY>;
+  using SS = TmaShape<NF, NC, WIDE, RY, FSEL>;
+  static_assert(!FSEL || (!WIDE && !CH3 && NC > 0), "fused selector: shared-bank pair stages only");
   constexpr int RF = SS::RF, RC = SS::RC;
   constexpr int PL = CH3 ? 1 : 3;
   const int chn = CH3 ? (int)(blockIdx.x % 3) : 0;
@@ -266,7 +375,7 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
     else
       __syncthreads();
   };
-  constexpr uint32_t tx_bytes = SS::fine_bytes + SS::coarse_bytes + SS::map_bytes;
+  constexpr uint32_t tx_bytes = SS::fine_bytes + SS::coarse_bytes + (FSEL ? 0 : SS::map_bytes);
 
   auto tile_coords = [&](int t, int& n, int& X0, int& Y0) {
     n = t / (a.tiles_x * a.tiles_y);
@@ -280,10 +389,10 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
     tile_coords(t, n, X0, Y0);
     unsigned char* sb = buf0 + b * SS::stage_bytes;
     mbar_expect_tx(&mbar[b], tx_bytes);
-    tma_load_3d(sb + SS::fine_off, &tm_z, X0 - SS::FM, Y0 - RF - a.z_row0, n * 3, &mbar[b]);
+    tma_load_3d(sb + SS::fine_off, &tm_z, X0 - SS::FM, Y0 - SS::FH - a.z_row0, n * 3, &mbar[b]);
     if constexpr (NC > 0)
       tma_load_3d(sb + SS::coarse_off, &tm_u, X0 / 2 - SS::CM, Y0 / 2 - RC - a.u_row0, n * 3, &mbar[b]);
-    tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[b]);
+    if constexpr (!FSEL) tma_load_3d(sb + SS::map_off, &tm_map, X0, Y0 - a.map_row0, n, &mbar[b]);
   };
 
   const int ctid = threadIdx.y * SS::BX + threadIdx.x;
@@ -323,18 +432,18 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
 
     // ---- border fix-up: out-of-image cells <- folded samples
     const int FX = X0 - SS::FM, CX = X0 / 2 - SS::CM;  // box origins (columns)
-    const bool fine_border = FX < 0 || FX + SS::FCB > a.W || Y0 - RF < 0 || Y0 + SS::TROWS + RF > a.H;
+    const bool fine_border = FX < 0 || FX + SS::FCB > a.W || Y0 - SS::FH < 0 || Y0 + SS::TROWS + SS::FH > a.H;
     const bool coarse_border = NC > 0 && (CX < 0 || CX + SS::CCB > a.W1 || Y0 / 2 - RC < 0 ||
                                           Y0 / 2 - RC + SS::CR > a.H1);
     if (fine_border || coarse_border) {
       if (fine_border) {
-        const OobBox ob = oob_box(SS::FR, SS::FCB, Y0 - RF, FX, a.H, a.W);
+        const OobBox ob = oob_box(SS::FR, SS::FCB, Y0 - SS::FH, FX, a.H, a.W);
         for (int i = tid; i < ob.n; i += SS::threads) {
           int r, q;
           oob_cell(ob, i, r, q);
-          const int gy = Y0 - RF + r, gx = FX + q;
+          const int gy = Y0 - SS::FH + r, gx = FX + q;
           const int fy = fold_idx(gy, a.H), fx = fold_idx(gx, a.W);
-          const int ry = fy - (Y0 - RF), rx = fx - FX;
+          const int ry = fy - (Y0 - SS::FH), rx = fx - FX;
           const bool in_tile = ry >= 0 && ry < SS::FR && rx >= 0 && rx < SS::FCB;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
@@ -397,6 +506,8 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
     constexpr int KB = WIDE ? 16 : 8;
     constexpr uint64_t KM = WIDE ? 0xffff : 0xff;
     int toff[RY][4];  // filter offsets in the bank: phase (2 (i & 1) + (j & 1)) x PS + bucket x S
+    if constexpr (FSEL)  // this thread's buckets, from the staged tile, into its own map entries
+      fused_buckets<RY, SS::FR, SS::FCB, SS::FH, SS::TCOLS>(sfine, const_cast<uint8_t*>(smap), ty, tx, n, y, x, a);
 #pragma unroll
     for (int i = 0; i < RY; ++i) {
       uint64_t mrow;
@@ -456,7 +567,7 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
       float v[PL][SS::FWIN];
 #pragma unroll
       for (int c = 0; c < PL; ++c)
-        lds_run<SS::FO, SS::FWIN>(sfine + (c * SS::FR + RY * ty + wr) * SS::FCB + 4 * tx + SS::FO, v[c]);
+        lds_run<SS::FO, SS::FWIN>(sfine + (c * SS::FR + RY * ty + wr + SS::FRO) * SS::FCB + 4 * tx + SS::FO, v[c]);
 #pragma unroll
       for (int i = 0; i < RY; ++i) {
         const int dy = wr - i;
@@ -504,6 +615,107 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
     if (G == 2 && tid == 0 && tn < a.n_tiles) {
       fence_proxy_async();
       issue(tn, b);
+    }
+  }
+}
+
+// Fix-up of the fused-selector stage (level 0): the pixels whose fp32 orientation the certificate
+// could not guarantee get their bucket in fp64 (the k_down_fixup arithmetic: one warp per pixel,
+// lanes 0..24 the window taps) and their output recomputed with it: lanes take the taps t = lane,
+// lane + 32, ... of the filter (ABI order: fine block then coarse block, generic bank layout) and
+// the warp sums the three channels' partial dot products. If the list overflowed, every pixel of
+// the launch is recomputed this way.
+struct StageFixArgs {
+  const float* z;  // level-0 input view: [N][3][z_rows][z_pitch], global rows from z_row0
+  int z_row0, z_rows, z_pitch;
+  const float* u1;  // u^1 buffer: [N][3][u_rows][u_pitch], global rows from u_row0
+  int u_row0, u_rows, u_pitch;
+  float* out;       // output view: [N][3][out_rows][out_pitch], global rows from out_row0
+  int out_row0, out_rows, out_pitch;
+  int H, W, H1, W1;
+  int N, o_r0, o_rn;  // computed rows (the list's map-index space: [N][o_rn][W])
+  const float* bank;  // generic layout of this stage: [phase][PS], filter k at k * S
+  int S, PS, n_phases, clamp;
+  const unsigned long long* fb_list;
+  const unsigned int* fb_count;
+  unsigned int fb_cap;
+};
+
+template <int NF, int NC>
+__global__ void __launch_bounds__(128) k_stage_fixup(const StageFixArgs a, const DownParams prm) {
+  constexpr int RF = NF / 2, RC = NC / 2, NT = NF * NF + NC * NC;
+  pdl_trigger();
+  pdl_wait();
+  const unsigned int cnt = *a.fb_count;
+  const bool all = cnt > a.fb_cap;
+  const unsigned long long per_frame = (unsigned long long)a.o_rn * a.W;
+  const unsigned long long items = all ? (unsigned long long)a.N * per_frame : (unsigned long long)cnt;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long warps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const long long zpl = (long long)a.z_rows * a.z_pitch, upl = (long long)a.u_rows * a.u_pitch;
+  auto Z = [&](int n, int c, int yy, int xq) -> float {
+    const int br = min(max(fold_idx(yy, a.H) - a.z_row0, 0), a.z_rows - 1);
+    return a.z[((long long)n * 3 + c) * zpl + (long long)br * a.z_pitch + fold_idx(xq, a.W)];
+  };
+  for (unsigned long long i = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); i < items;
+       i += warps) {
+    const unsigned long long e = all ? i : a.fb_list[i];
+    const int n = (int)(e / per_frame);
+    const unsigned long long r = e - (unsigned long long)n * per_frame;
+    const int y = a.o_r0 + (int)(r / a.W), x = (int)(r % a.W);
+    // ---- fp64 bucket (k_down_fixup)
+    double pa = 0.0, pb = 0.0, pc = 0.0;
+    if (lane < 25) {
+      const int dy = lane / 5 - 2, dx = lane % 5 - 2, yy = y + dy, xq = x + dx;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double gx = (double)Z(n, c, yy, xq + 1) - (double)Z(n, c, yy, xq - 1);
+        const double gy = (double)Z(n, c, yy + 1, xq) - (double)Z(n, c, yy - 1, xq);
+        pa = fma(gx, gx, pa);
+        pb = fma(gx, gy, pb);
+        pc = fma(gy, gy, pc);
+      }
+      const double wgt = prm.wp[dy + 2] * prm.wp[dx + 2];
+      pa *= wgt;
+      pb *= wgt;
+      pc *= wgt;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      pa += __shfl_xor_sync(0xffffffffu, pa, o);
+      pb += __shfl_xor_sync(0xffffffffu, pb, o);
+      pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    }
+    const int k = __shfl_sync(0xffffffffu, bucket_of<true>(pa, pb, pc, prm), 0);
+    // ---- Eq. 9 for this pixel with bucket k
+    const int ph = a.n_phases == 4 ? 2 * (y & 1) + (x & 1) : 0;
+    const float* f = a.bank + (long long)ph * a.PS + (long long)k * a.S;
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+    for (int t = lane; t < NT; t += 32) {
+      const float w = f[t];
+      if (t < NF * NF) {
+        const int dy = t / NF - RF, dx = t % NF - RF;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = fmaf(w, Z(n, c, y + dy, x + dx), acc[c]);
+      } else {
+        const int tc = t - NF * NF, dy = tc / NC - RC, dx = tc % NC - RC;
+        const int br = min(max(fold_idx(y / 2 + dy, a.H1) - a.u_row0, 0), a.u_rows - 1);
+        const long long o = (long long)br * a.u_pitch + fold_idx(x / 2 + dx, a.W1);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = fmaf(w, a.u1[((long long)n * 3 + c) * upl + o], acc[c]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float v = acc[c];
+        if (a.clamp) v = fminf(fmaxf(v, 0.0f), 1.0f);
+        a.out[((long long)n * 3 + c) * a.out_rows * a.out_pitch + (long long)(y - a.out_row0) * a.out_pitch + x] = v;
+      }
     }
   }
 }

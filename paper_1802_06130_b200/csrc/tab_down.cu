@@ -13,6 +13,9 @@ DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy) {
   if (wide) return down_kernel_t<false, true>(hilo, dec, copy);  // FAST implies K = 144
   return fast ? down_kernel_t<true, false>(hilo, dec, copy) : down_kernel_t<false, false>(hilo, dec, copy);
 }
+DownKernel dec_kernel(bool copy) {
+  return copy ? &k_down<false, true, true, false, true, false> : &k_down<false, true, true, false, false, false>;
+}
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide) {
   if (wide) return hilo ? &k_down_fixup<true, false, true> : &k_down_fixup<false, false, true>;
   if (hilo) return fast ? &k_down_fixup<true, true, false> : &k_down_fixup<true, false, false>;

@@ -9,8 +9,21 @@ namespace tables {
 template <int NF, int NC, bool CH3 = false, bool WIDE = false, int RY = 2, int G = BLADE_TMA_GROUPS>
 static TmaVariant make_tma() {
   using SS = TmaShape<NF, NC, WIDE, RY>;
-  return TmaVariant{NF, NC, G, SS::BY, &k_stage_tma<NF, NC, G, CH3, WIDE, RY>, SS::stage_bytes, SS::TROWS,
-                    SS::TCOLS, SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3, WIDE};
+  TmaVariant v{NF, NC, G, SS::BY, &k_stage_tma<NF, NC, G, CH3, WIDE, RY>, SS::stage_bytes, SS::TROWS,
+               SS::TCOLS, SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3, WIDE};
+  if constexpr (!CH3 && !WIDE && NC > 0 && RY == 4) {  // fused-selector form (level 0, 4-row threads)
+    using SF = TmaShape<NF, NC, WIDE, RY, true>;
+    v.fsel_fn = &k_stage_tma<NF, NC, G, CH3, WIDE, RY, true>;
+    v.fsel_stage_bytes = SF::stage_bytes;
+    v.fsel_fr = SF::FR;
+  }
+  return v;
+}
+StageFixKernel stage_fixup_kernel(int nf, int nc) {
+  if (nf == 5 && nc == 5) return &k_stage_fixup<5, 5>;
+  if (nf == 3 && nc == 3) return &k_stage_fixup<3, 3>;
+  if (nf == 5 && nc == 3) return &k_stage_fixup<5, 3>;
+  return nullptr;
 }
 const std::vector<TmaVariant>& tma_variants() {
   static const std::vector<TmaVariant> v = {

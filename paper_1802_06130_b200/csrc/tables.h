@@ -34,7 +34,12 @@ struct TmaVariant {
   bool phase_split;  // k_stage_ph: CTAs specialised by output phase, one phase's bank each
   bool ch3;          // per-channel (Y, Cb, Cr) banks
   bool wide;         // K > 256: uint16 maps, bank read from global memory (NEXT f2)
+  // the fused-selector form of the same kernel (level 0; nullptr if none): taller fine box
+  TmaKernel fsel_fn = nullptr;
+  int fsel_stage_bytes = 0, fsel_fr = 0;
 };
+using StageFixKernel = void (*)(const StageFixArgs, const DownParams);
+StageFixKernel stage_fixup_kernel(int nf, int nc);  // nullptr if none
 // TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
 const std::vector<TmaVariant>& tma_variants();
 // Phase-split TMA stage kernels: pair banks whose four phases do not fit one CTA.
@@ -45,6 +50,8 @@ using DownKernel = void (*)(const DownArgs, const DownParams);
 // wide: uint16 bucket maps (K > 256, NEXT f2)
 DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy = false);
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide);
+// level-0 decimation (+ input copy) without the selector: the fused-selector stage computes s^0
+DownKernel dec_kernel(bool copy);
 using FixupMultiKernel = void (*)(const FixupMulti);
 FixupMultiKernel fixup_multi_kernel(bool fast, bool wide);
 

@@ -1,8 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_train.py -x -q > gpurun_out/pt_train.log 2>&1; tail -2 gpurun_out/pt_train.log
-for g in -1 -1; do
-timeout 300 python bench.py --train --frames 16 --steps 5 --warmup 3 > gpurun_out/tr.log 2>&1
-python -c "import json;d=json.loads([l for l in open('gpurun_out/tr.log') if l.startswith('{')][-1]);print('group=$g', round(d['value']), d['roofline']['frac'])" || tail -3 gpurun_out/tr.log
+for f in 1 0; do
+BLADE_FUSE_SEL=$f timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/fs.log 2>&1
+python -c "import json;d=json.loads([l for l in open('gpurun_out/fs.log') if l.startswith('{')][-1]);print('fuse=$f', round(d['value']), d['kernel_ms_per_step'])" || tail -5 gpurun_out/fs.log
 done
-timeout 300 python bench.py --train --frames 16 --steps 2 --warmup 3 > gpurun_out/tr_plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 70 -c 70 --csv --log-file gpurun_out/tr_launches.csv python bench.py --train --frames 16 --steps 2 --warmup 3 > gpurun_out/tr_ncu.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "c3 or bench_launch or forced or fallback or repeat or band or xband or delta or constant or batch or pipelined or no_writes or ragged or c4 or clamp" > gpurun_out/pt_fs.log 2>&1; tail -15 gpurun_out/pt_fs.log
