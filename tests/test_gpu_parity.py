@@ -424,7 +424,8 @@ def test_c5_paper_bucket_layout_parity(H, W, N):
 
 # ------------------------------------------------------------------------- forced kernel variants
 
-@pytest.mark.parametrize("env", [{"BLADE_TMA_RY": "4"}, {"BLADE_TMA_RY": "2"}, {"BLADE_PDL": "0"}])
+@pytest.mark.parametrize("env", [{"BLADE_TMA_RY": "4"}, {"BLADE_TMA_RY": "2"}, {"BLADE_PDL": "0"},
+                                 {"BLADE_FUSE_SEL": "1", "BLADE_TMA_RY": "4"}, {"BLADE_CARVEOUT": "100"}])
 def test_forced_variants_subprocess(env):
     """The library picks kernel variants by level size (4- vs 2-row TMA stage threads) and
     launches with programmatic dependent launch; the knobs are read once per process, so the
@@ -436,7 +437,8 @@ def test_forced_variants_subprocess(env):
     root = Path(__file__).resolve().parents[1]
     cmd = [sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_parity.py"), "-q", "-x",
            "-p", "no:cacheprovider", "-k",
-           "(ragged_shapes or c1_full or delta_bank or c3_frames_batched) and not forced_variants"]
+           "(ragged_shapes or c1_full or delta_bank or c3_frames_batched or forced_selector_every_pixel or "
+           "xband_bands or repeat_runs or constant_image) and not forced_variants"]
     r = subprocess.run(cmd, cwd=root, env={**os.environ, **env}, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
