@@ -643,7 +643,7 @@ struct StageFixArgs {
 
 template <int NF, int NC>
 __global__ void __launch_bounds__(128) k_stage_fixup(const StageFixArgs a, const DownParams prm) {
-  constexpr int RF = NF / 2, RC = NC / 2, NT = NF * NF + NC * NC;
+  constexpr int RF = NF / 2, RC = NC / 2;
   pdl_trigger();
   pdl_wait();
   const unsigned int cnt = *a.fb_count;
@@ -687,35 +687,23 @@ __global__ void __launch_bounds__(128) k_stage_fixup(const StageFixArgs a, const
       pc += __shfl_xor_sync(0xffffffffu, pc, o);
     }
     const int k = __shfl_sync(0xffffffffu, bucket_of<true>(pa, pb, pc, prm), 0);
-    // ---- Eq. 9 for this pixel with bucket k
+    // ---- Eq. 9 for this pixel with bucket k: lane c < 3 sums channel c with the stage kernels'
+    //      fmaf order (coarse rows, then fine rows; dy, then dx ascending), so the output is the
+    //      one those kernels give with the fp64 bucket (bands and batches stay bit-identical)
     const int ph = a.n_phases == 4 ? 2 * (y & 1) + (x & 1) : 0;
     const float* f = a.bank + (long long)ph * a.PS + (long long)k * a.S;
-    float acc[3] = {0.0f, 0.0f, 0.0f};
-    for (int t = lane; t < NT; t += 32) {
-      const float w = f[t];
-      if (t < NF * NF) {
-        const int dy = t / NF - RF, dx = t % NF - RF;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] = fmaf(w, Z(n, c, y + dy, x + dx), acc[c]);
-      } else {
-        const int tc = t - NF * NF, dy = tc / NC - RC, dx = tc % NC - RC;
-        const int br = min(max(fold_idx(y / 2 + dy, a.H1) - a.u_row0, 0), a.u_rows - 1);
-        const long long o = (long long)br * a.u_pitch + fold_idx(x / 2 + dx, a.W1);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] = fmaf(w, a.u1[((long long)n * 3 + c) * upl + o], acc[c]);
+    if (lane < 3) {
+      const int c = lane;
+      float acc = 0.0f;
+      for (int dy = 0; dy < NC; ++dy) {
+        const int br = min(max(fold_idx(y / 2 + dy - RC, a.H1) - a.u_row0, 0), a.u_rows - 1);
+        const float* urow = a.u1 + ((long long)n * 3 + c) * upl + (long long)br * a.u_pitch;
+        for (int dx = 0; dx < NC; ++dx) acc = fmaf(f[NF * NF + dy * NC + dx], urow[fold_idx(x / 2 + dx - RC, a.W1)], acc);
       }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
-    if (lane == 0) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float v = acc[c];
-        if (a.clamp) v = fminf(fmaxf(v, 0.0f), 1.0f);
-        a.out[((long long)n * 3 + c) * a.out_rows * a.out_pitch + (long long)(y - a.out_row0) * a.out_pitch + x] = v;
-      }
+      for (int dy = 0; dy < NF; ++dy)
+        for (int dx = 0; dx < NF; ++dx) acc = fmaf(f[dy * NF + dx], Z(n, c, y + dy - RF, x + dx - RF), acc);
+      if (a.clamp) acc = fminf(fmaxf(acc, 0.0f), 1.0f);
+      a.out[((long long)n * 3 + c) * a.out_rows * a.out_pitch + (long long)(y - a.out_row0) * a.out_pitch + x] = acc;
     }
   }
 }

@@ -1,6 +1,3 @@
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-for f in 1 0; do
-BLADE_FUSE_SEL=$f timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/fs.log 2>&1
-python -c "import json;d=json.loads([l for l in open('gpurun_out/fs.log') if l.startswith('{')][-1]);print('fuse=$f', round(d['value']), d['kernel_ms_per_step'])" || tail -5 gpurun_out/fs.log
-done
-timeout 900 python -m pytest tests -m gpu -x -q -k "c3 or bench_launch or forced or fallback or repeat or band or xband or delta or constant or batch or pipelined or no_writes or ragged or c4 or clamp" > gpurun_out/pt_fs.log 2>&1; tail -15 gpurun_out/pt_fs.log
+timeout 300 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/st_plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage_tma -s 7 -c 1 -o gpurun_out/st_r4 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/st_ncu.log 2>&1; echo rc=$?
