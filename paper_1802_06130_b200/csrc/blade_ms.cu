@@ -460,7 +460,7 @@ bool use_ry4(const blade_ms* h, int N, int W, int span) {
 }
 
 // The fp64 fix-ups of all selector levels run as one launch after the down pass on small calls
-// (launch-latency-bound: c1 -7 us per call), per level right after each k_down otherwise.
+// (launch-latency-bound: c1 63 -> 58 us warm), per level right after each k_down otherwise.
 // BLADE_FIXUP_MERGE=0 / =1 forces the per-level / merged form on every call (A/B timing of the
 // threshold: scripts/fixup_ab.sh); default by size.
 bool fixups_merged(int nsel, long long N, long long H, long long W) {
@@ -470,7 +470,7 @@ bool fixups_merged(int nsel, long long N, long long H, long long W) {
   }();
   if (nsel <= 1) return false;
   if (force == 0 || force == 1) return force == 1;
-  return N * H * W <= (4LL << 20);
+  return N * H * W <= (3LL << 20);  // crossover 2.07 .. 4.15 MP (profiles/r02_fixup_merge.txt)
 }
 
 // Kernel launch; with `pdl` the launch allows programmatic stream serialisation (PDL): the grid

@@ -1,8 +1,13 @@
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-for lib in main t24 main t24; do
-if [ $lib = main ]; then unset BLADE_MS_LIB; else export BLADE_MS_LIB=$PWD/paper_1802_06130_b200/libblade_ms_$lib.so; fi
-timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/t24.log 2>&1
-python -c "import json;d=json.loads([l for l in open('gpurun_out/t24.log') if l.startswith('{')][-1]);print('$lib', round(d['value']), d['kernel_ms_per_step'])" || tail -5 gpurun_out/t24.log
-done
-export BLADE_MS_LIB=$PWD/paper_1802_06130_b200/libblade_ms_t24.so
-timeout 900 python -m pytest tests -m gpu -x -q -k "c3 or c1 or bench_launch or forced_selector or delta or constant or ragged or band or repeat" > gpurun_out/pt_t24.log 2>&1; tail -5 gpurun_out/pt_t24.log
+rm -f gpurun_out/fixup_ab.txt
+run() { tag=$1; shift; for m in 0 1; do
+BLADE_FIXUP_MERGE=$m timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 1 --graph off "$@" > gpurun_out/fx.log 2>&1
+python -c "import json;d=json.loads([l for l in open('gpurun_out/fx.log') if l.startswith('{')][-1]);print('$tag merge=$m', round(d['config']['frames_per_gpu']*d['config']['H']*d['config']['W']/1e6,2), 'MP', round(d['warm']['ms_per_step']*1e3,1), 'us warm', round(d['ms_per_step']*1e3,1), 'us value')" >> gpurun_out/fixup_ab.txt; done; }
+run c1 --config c1
+run c1x4 --config c1 --frames 4
+run c3f1 --frames 1
+run c3f2 --frames 2
+run c3f4 --frames 4
+run c3f8 --frames 8
+run c3f16 --frames 16
+cat gpurun_out/fixup_ab.txt
