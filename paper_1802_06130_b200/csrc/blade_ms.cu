@@ -778,7 +778,8 @@ blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView
                    aligned16(outv.p) && (L == 1 || (u1.pitch % 4 == 0 && aligned16(u1.p)));
     CUtensorMap tmz, tmu, tmm;
     if (use_tma) {
-      const TmaVariant& tv = h->tma;
+      // box shapes of the variant that will run (the 4-row variant may use taller tiles)
+      const TmaVariant& tv = (fused || use_ry4(h, N, p.W[l], r.hi - y_base)) ? h->tma4 : h->tma;
       use_tma = encode_3d(&tmz, zl.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p.W[l], zl.rows, N * 3, tv.fcb,
                           fused ? h->tma4.fsel_fr : tv.fr, 3, zl.pitch) &&
                 (fused ? true
@@ -1102,8 +1103,9 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->stage_smem = best_smem;
   for (const auto& v : tma_variants()) {
     if (v.ch3 != ch3 || v.wide != wide || v.nf != c.fine_size || v.nc != cnc) continue;
-    if (v.by == 4) {  // 4 pixel rows per thread: same tiles and smem as the 2-row variant
-      if (tma_ry() != 2) {
+    if (v.ry == 4) {  // 4 pixel rows per thread (16-row tiles: same smem as the 2-row variant;
+                      // 20-row tiles = 10 warps per SM measured slower: profiles/r02_fused_selector.txt)
+      if (tma_ry() != 2 && v.trows == 16) {
         h->has_tma4 = true;
         h->tma4 = v;
       }
@@ -1119,6 +1121,14 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
       h->S_tma = v.S;
       h->PS_tma = (int)tps;
     }
+  }
+  if (h->has_tma && h->has_tma4 && h->tma4.stage_bytes != h->tma.stage_bytes) {  // taller tiles
+    const size_t bank = wide ? 0 : ((size_t)c.n_phases * h->PS_tma * 4 + 127) & ~size_t(127);
+    const size_t smem4 = 2 * (size_t)h->tma4.stage_bytes + bank + 32;
+    if (smem4 <= (size_t)max_smem)
+      h->tma_smem = std::max(h->tma_smem, smem4);
+    else
+      h->has_tma4 = false;
   }
   if (!h->has_tma && c.levels > 1 && c.n_phases == 4) {
     for (const auto& v : ph_variants()) {

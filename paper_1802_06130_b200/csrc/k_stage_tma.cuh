@@ -175,9 +175,9 @@ __device__ __forceinline__ void load_tap_row(const float* tp, int dy, float* t) 
 // FSEL (fused selector, level 0): the fine box carries FH = max(RF, 3) halo rows so that the
 // kernel computes the bucket map of its own tile (gradient 1 + window 2 rows) instead of loading
 // it; the FIR reads the box from row FRO = FH - RF.
-template <int NF, int NC, bool WIDE = false, int RY_ = 2, bool FSEL = false>
+template <int NF, int NC, bool WIDE = false, int RY_ = 2, bool FSEL = false, int TR = 16>
 struct TmaShape {
-  static constexpr int RX = 4, RY = RY_, BX = 32, BY = 16 / RY_;
+  static constexpr int RX = 4, RY = RY_, BX = 32, BY = TR / RY_;
   static constexpr int threads = BX * BY;
   static constexpr int RF = NF / 2, RC = NC / 2;
   static constexpr int FH = FSEL ? (RF > 3 ? RF : 3) : RF;
@@ -346,11 +346,11 @@ __device__ __forceinline__ void fused_buckets(const float* sf, uint8_t* smap, in
 #else
 #define BLADE_STAGE_BOUNDS(threads) __launch_bounds__(threads, 1)
 #endif
-template <int NF, int NC, int G, bool CH3, bool WIDE = false, int RY = 2, bool FSEL = false>
-__global__ void BLADE_STAGE_BOUNDS(32 * (16 / RY) * G)
+template <int NF, int NC, int G, bool CH3, bool WIDE = false, int RY = 2, bool FSEL = false, int TR = 16>
+__global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
     k_stage_tma(const __grid_constant__ CUtensorMap tm_z, const __grid_constant__ CUtensorMap tm_u,
                 const __grid_constant__ CUtensorMap tm_map, StageTmaArgs a) {
-  using SS = TmaShape<NF, NC, WIDE, RY, FSEL>;
+  using SS = TmaShape<NF, NC, WIDE, RY, FSEL, TR>;
   static_assert(!FSEL || (!WIDE && !CH3 && NC > 0), "fused selector: shared-bank pair stages only");
   constexpr int RF = SS::RF, RC = SS::RC;
   constexpr int PL = CH3 ? 1 : 3;

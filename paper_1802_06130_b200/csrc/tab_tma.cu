@@ -6,12 +6,13 @@
 #endif
 namespace blade {
 namespace tables {
-template <int NF, int NC, bool CH3 = false, bool WIDE = false, int RY = 2, int G = BLADE_TMA_GROUPS>
+template <int NF, int NC, bool CH3 = false, bool WIDE = false, int RY = 2, int G = BLADE_TMA_GROUPS, int TR = 16>
 static TmaVariant make_tma() {
-  using SS = TmaShape<NF, NC, WIDE, RY>;
-  TmaVariant v{NF, NC, G, SS::BY, &k_stage_tma<NF, NC, G, CH3, WIDE, RY>, SS::stage_bytes, SS::TROWS,
+  using SS = TmaShape<NF, NC, WIDE, RY, false, TR>;
+  TmaVariant v{NF, NC, G, SS::BY, &k_stage_tma<NF, NC, G, CH3, WIDE, RY, false, TR>, SS::stage_bytes, SS::TROWS,
                SS::TCOLS, SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, false, CH3, WIDE};
-  if constexpr (!CH3 && !WIDE && NC > 0 && RY == 4) {  // fused-selector form (level 0, 4-row threads)
+  v.ry = RY;
+  if constexpr (!CH3 && !WIDE && NC > 0 && RY == 4 && TR == 16) {  // fused-selector form (level 0, 4-row threads)
     using SF = TmaShape<NF, NC, WIDE, RY, true>;
     v.fsel_fn = &k_stage_tma<NF, NC, G, CH3, WIDE, RY, true>;
     v.fsel_stage_bytes = SF::stage_bytes;

@@ -37,6 +37,7 @@ struct TmaVariant {
   // the fused-selector form of the same kernel (level 0; nullptr if none): taller fine box
   TmaKernel fsel_fn = nullptr;
   int fsel_stage_bytes = 0, fsel_fr = 0;
+  int ry = 2;  // pixel rows per thread (k_stage_tma)
 };
 using StageFixKernel = void (*)(const StageFixArgs, const DownParams);
 StageFixKernel stage_fixup_kernel(int nf, int nc);  // nullptr if none
