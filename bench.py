@@ -258,6 +258,33 @@ def oracle_sample_rate(cfg, target_s: float):
     return n * cfg.H * W / 1e6 / dt, dt, f"{n} full {cfg.H}x{W} frame(s)", oracle.max_threads()
 
 
+def oracle_single_thread_rate(cfg, target_s: float = 3.0):
+    """The same oracle on ONE host thread (the single-core figure), on a
+    full-width band of frame 0 sized to about target_s seconds; MP/s and what was timed."""
+    import oracle
+    oracle.build()
+    taps = cfg.taps()
+    W = cfg.W
+    nthreads = oracle.max_threads()
+    oracle.set_threads(1)
+    try:
+        rows = min(cfg.H, 16)
+        sub = bs.Config(**{**cfg.__dict__, "H": rows})
+        z = cfg.frame(0, row0=0, rows=rows)
+        t = time.perf_counter()
+        oracle.denoise_config(sub, z, taps)
+        per_px = (time.perf_counter() - t) / (rows * W)
+        rows = int(min(cfg.H, max(16, target_s / per_px / W)))
+        sub = bs.Config(**{**cfg.__dict__, "H": rows})
+        z = cfg.frame(0, row0=0, rows=rows)
+        t = time.perf_counter()
+        oracle.denoise_config(sub, z, taps)
+        dt = time.perf_counter() - t
+    finally:
+        oracle.set_threads(nthreads)
+    return rows * W / 1e6 / dt, f"one {rows}x{W} full-width band of frame 0 (treated as an image), 1 thread, {dt:.1f} s"
+
+
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
@@ -642,6 +669,8 @@ def main():
             cpu = {"value": mps, "unit": "MP/s", "cores": cores, "kind": "oracle",
                    "sample": f"{what} of {cfg.name}, fp64 C oracle, OpenMP over rows "
                              f"({dt:.1f} s of CPU time)"}
+            v1, what1 = oracle_single_thread_rate(cfg)
+            cpu["single_thread"] = {"value": v1, "unit": "MP/s", "cores": 1, "sample": what1}
         except Exception as e:  # the baseline must never break the GPU line
             cpu = {"value": None, "unit": "MP/s", "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {e}"}
