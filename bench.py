@@ -616,6 +616,7 @@ def main():
     fp32_peak = n_sm * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
     w = work[dom]
     traffic = None
+    ent = None
     ncu_path = ROOT / "profiles" / "ncu_summary.json"
     if ncu_path.exists():
         try:
@@ -647,9 +648,15 @@ def main():
             roof["sram"] = {"achieved": sb / (dom_ms / 1e3) / 1e12, "peak": sp, "unit": "TB/s",
                             "frac": sb / (dom_ms / 1e3) / 1e12 / sp,
                             "bytes_per_px": stage_smem_bytes_per_px(cfg, skind, sry),
-                            "note": "conflict-free model (taps 4 B each + window values); ncu "
-                                    "shows L1/TEX ~91% busy, LDS.128 tap loads at ~2x their ideal "
-                                    "wavefronts (bank conflicts)"}
+                            "note": "conflict-free model (taps 4 B each + window values); the ncu "
+                                    "capture of this launch (profiles/ncu_summary.json) gives the "
+                                    "measured wavefronts below: the binding unit"}
+            if ent and ent.get("smem_wavefronts"):
+                roof["sram"]["measured"] = {
+                    "wavefronts_per_launch": ent["smem_wavefronts"],
+                    "bank_conflict_wavefronts": ent.get("smem_bank_conflicts"),
+                    "frac_of_wavefront_slots": ent.get("smem_wavefront_frac"),
+                    "source": "ncu --set full, l1tex__data_pipe_lsu_wavefronts_mem_shared (one launch)"}
     else:
         ach = w["bytes"] / (dom_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": f"k_down level {dom[1]}", "achieved": ach, "peak": hbm_peak,

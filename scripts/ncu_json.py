@@ -22,9 +22,18 @@ def first_launch(rep):
     def val(name):
         return float(r[idx[name]].replace(",", "")) * UNIT.get(units[idx[name]], 1.0)
     rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
-    return {"kernel": r[idx["Kernel Name"]][:60], "dram_read_bytes": rd, "dram_write_bytes": wr,
-            "dram_bytes_per_launch": rd + wr,
-            "duration": f"{r[idx['gpu__time_duration.sum']]} {units[idx['gpu__time_duration.sum']]}"}
+    d = {"kernel": r[idx["Kernel Name"]][:60], "dram_read_bytes": rd, "dram_write_bytes": wr,
+         "dram_bytes_per_launch": rd + wr,
+         "duration": f"{r[idx['gpu__time_duration.sum']]} {units[idx['gpu__time_duration.sum']]}"}
+    # the shared-memory pipe (the stage's binding unit): wavefronts, their share of the launch's
+    # wavefront slots, and the bank-conflict excess
+    for k, name in (("smem_wavefronts", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+                    ("smem_wavefront_frac", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                    ("smem_bank_conflicts", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")):
+        if name in idx:
+            v = float(r[idx[name]].replace(",", ""))
+            d[k] = v / 100.0 if k.endswith("frac") else v
+    return d
 
 
 out = {"note": "per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) from one "
