@@ -403,7 +403,9 @@ __global__ void __launch_bounds__(256) k_train_gram_mma(const TrainArgs a) {
       xs[e][NT] = (double)__ldg(a.uc + ((long long)pn[j] * 3 + c) * plane + ctr[j]);
     }
     __syncthreads();
-    // ---- runs of one segment within the batch (uniform over the CTA)
+    // ---- runs of one segment within the batch (uniform over the CTA). The pixels are sorted by
+    //      segment, so segs[] is non-decreasing: a run ends at the first larger entry (binary
+    //      search; the whole batch when its last pixel is in the first pixel's segment)
     const int ns = 3 * nb;
     int pos = 0;
     while (pos < ns) {
@@ -412,19 +414,36 @@ __global__ void __launch_bounds__(256) k_train_gram_mma(const TrainArgs a) {
         flush();
         cur = sg;
       }
-      int end = pos + 3;
-      while (end < ns && segs[end / 3] == sg) end += 3;
-      for (int k0 = pos & ~3; k0 < end; k0 += 4) {
+      int end;
+      if (segs[nb - 1] == sg) {
+        end = ns;
+      } else {
+        int lo = pos / 3, hi = nb - 1;  // segs[lo] == sg < segs[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (segs[mid] == sg) lo = mid; else hi = mid;
+        }
+        end = 3 * hi;
+      }
+      const int full0 = (pos + 3) & ~3, full1 = end & ~3;  // 4-sample steps wholly inside the run
+      auto step = [&](int k0, bool masked) {
         const int smp = k0 + q;
-        const bool ok = smp >= pos && smp < end;
+        const bool ok = !masked || (smp >= pos && smp < end);
         const double* xr = &xs[ok ? smp : 0][0];
 #pragma unroll
         for (int k = 0; k < TS::BPW; ++k) {
           if (!act[k]) continue;  // warp-uniform
-          const double av = ok ? xr[8 * bI[k] + g] : 0.0;
-          const double bv = ok ? xr[8 * bJ[k] + g] : 0.0;
-          dmma_884(acc[k][0], acc[k][1], av, bv);
+          const double av = xr[8 * bI[k] + g];
+          const double bv = xr[8 * bJ[k] + g];
+          dmma_884(acc[k][0], acc[k][1], ok ? av : 0.0, ok ? bv : 0.0);
         }
+      };
+      if (full0 >= full1) {  // a short run: every step masked
+        for (int k0 = pos & ~3; k0 < end; k0 += 4) step(k0, true);
+      } else {
+        if ((pos & 3) != 0) step(pos & ~3, true);
+        for (int k0 = full0; k0 < full1; k0 += 4) step(k0, false);
+        if (end & 3) step(full1, true);
       }
       pos = end;
     }

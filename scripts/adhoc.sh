@@ -1,6 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-for d in 1 0 1 0; do
-BLADE_DOWN4=$d timeout 120 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/d4.log 2>&1
-python -c "import json;d=json.loads([l for l in open('gpurun_out/d4.log') if l.startswith('{')][-1]);print('down4=$d', round(d['value']), d['kernel_ms_per_step'])" || tail -5 gpurun_out/d4.log
+timeout 600 python -m pytest tests/test_gpu_train.py -x -q > gpurun_out/pt_train.log 2>&1; tail -2 gpurun_out/pt_train.log
+for k in 1 2; do
+timeout 300 python bench.py --train --frames 16 --steps 5 --warmup 3 > gpurun_out/tr.log 2>&1
+python -c "import json;d=json.loads([l for l in open('gpurun_out/tr.log') if l.startswith('{')][-1]);print('train', round(d['value']), d['roofline']['frac'])" || tail -3 gpurun_out/tr.log
 done
-timeout 600 python -m pytest tests -m gpu -x -q -k "c3 or c1 or c0 or c2 or bench_launch or forced_selector or ragged or tiny or band or repeat or selector_and_layout or fallback or overflow or batch or pipelined" > gpurun_out/pt_d4.log 2>&1; tail -3 gpurun_out/pt_d4.log
