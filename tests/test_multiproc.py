@@ -169,3 +169,19 @@ def test_bench_rejects_gpus_world_size_mismatch():
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4", "--dry-run"],
                        capture_output=True, text=True, env=env, timeout=120)
     assert r.returncode == 2 and "disagrees" in r.stderr
+
+
+def test_bench_reference_arm_contract():
+    """bench.py --impl reference (the tier's reference arm: the fp64 oracle on the host cores) prints
+    one JSON line with impl, the metric / unit / higher_is_better of the blade arm, a cpu_baseline
+    describing the run and an e2e with zero host<->device bytes; it runs on CPU (no GPU needed)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "c1",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = _bench_json(r.stdout)
+    assert d["impl"] == "reference" and d["unit"] == "MP/s" and d["higher_is_better"] is True
+    assert d["metric"] == "megapixels/sec full multiscale denoise" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["config"]["workload"] == "c1"
