@@ -505,16 +505,19 @@ def main():
     sampler = ClockSampler(local)
     time.sleep(0.4)  # nvidia-smi start-up
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # an event after every step (markers only): the timed region is e[0] .. e[K]; the per-step
+    # spans give the median and best step beside the mean (SURVEY.md §8(d) timing protocol)
+    evts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     t0 = time.time()
-    e0.record(stream)
-    for _ in range(args.steps):
+    evts[0].record(stream)
+    for k in range(args.steps):
         run()
-    e1.record(stream)
+        evts[k + 1].record(stream)
     torch.cuda.synchronize(dev)
     t1 = time.time()
     barrier()
-    warm_ms = e0.elapsed_time(e1)
+    warm_ms = evts[0].elapsed_time(evts[-1])
+    step_spans = [evts[k].elapsed_time(evts[k + 1]) for k in range(args.steps)]
     flushed_ms = None
     if small:
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -710,7 +713,12 @@ def main():
             "hbm": {"achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": hbm_ach / hbm_peak,
                     "bytes_per_step_per_gpu": step_bytes,
-                    "note": "level-materialised algorithmic bytes of all kernels / step time"},
+                    "floor_frac": 24.0 * units(cfg, shard) / (ms_per_step / 1e3) / 1e9 / hbm_peak,
+                    "note": "level-materialised algorithmic bytes of all kernels / step time; "
+                            "floor_frac: 24 B/px (read the RGB input once, write the output once)"},
+            "step_ms_stats": {"mean": warm_step, "median": float(np.median(step_spans)),
+                              "best": float(np.min(step_spans)),
+                              "note": "back-to-back timed steps of this rank (events between steps)"},
             "kernel_ms_per_step": breakdown,
             "kernel_sum_ms_per_step": step_kernel_ms,
             "cpu_baseline": cpu,
