@@ -483,6 +483,20 @@ bool pdl_enabled() {
   }();
   return on;
 }
+// Small denoise calls (<= 16 Ki px) fix their uncertified pixels inside k_down (IFIX: one warp-wide
+// fp64 pass per pixel, the fix-up kernel's arithmetic) instead of a fix-up launch on the critical
+// path: 64 x 64 c1 38.9 -> 36.9 us, c0 20.5 -> 18.4 us; break-even at 128 x 128 and a loss above
+// (512 x 512: 54 -> 59 us, the warps' serial fix-ups outlast the launch they save),
+// profiles/r02_small_call_critical_path.txt. The selector diagnostic keeps the fix-up list.
+// BLADE_INLINE_FIX=<max px> moves the threshold (0: never; A/B and tests).
+bool inline_fixups(long long N, long long H, long long W, bool run_stages) {
+  static const long long max_px = [] {
+    const char* e = getenv("BLADE_INLINE_FIX");
+    return e ? atoll(e) : (16LL << 10);
+  }();
+  return run_stages && N * H * W <= max_px;
+}
+
 // Shared-memory carveout of the launches of the current (small) call: consecutive kernels with
 // different L1 / shared-memory splits make the SMs reconfigure between launches, which small,
 // latency-bound calls feel (c1 flushed 63 -> 58 us, c0 24.6 -> 23.5 us; large batches keep the
@@ -616,7 +630,8 @@ bool fused_level0(const blade_ms* h, const Plan& p, const Bufs& B, LevelView in_
 // p.z[l+1]); unless `fix_args` collects it for the merged launch, k_down_fixup(l) recomputes the
 // (rare) pixels whose fp32 orientation is uncertified. The level's fix-up counter must be zero.
 blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView in_view, char* ws,
-                        cudaStream_t st, bool run_stages, int l, std::vector<std::pair<int, DownArgs>>* fix_args) {
+                        cudaStream_t st, bool run_stages, int l, std::vector<std::pair<int, DownArgs>>* fix_args,
+                        bool ifix = false) {
   const int L = p.L, N = p.N;
   const std::vector<LevelView>& z32 = B.z32;
   const std::vector<float*>& zlo = B.zlo;
@@ -695,11 +710,11 @@ blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelVi
     const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
     const bool wide = h->K > 256;
     const bool fused = l == 0 && B.fuse0;  // the level-0 stage computes s^0: decimation only
-    auto fn = fused ? dec_kernel(zcopy) : down_kernel(hilo, dec, fast, wide, zcopy);
+    auto fn = fused ? dec_kernel(zcopy) : down_kernel(hilo, dec, fast, wide, zcopy, ifix);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
-    if (fused) {
-      // no map, no fix-up list at this level
+    if (fused || ifix) {
+      // no fix-up launch: no map at this level (fused), or uncertified pixels fixed in k_down (ifix)
     } else if (fix_args) {
       fix_args->emplace_back(l, da);
     } else {
@@ -730,7 +745,7 @@ blade_status merged_fixups(const blade_ms* h, const std::vector<std::pair<int, D
         fm.prm[q] = h->down[fix_args[l0 + q].first];
       }
       LAUNCH("k_down_fixup_multi",
-             launch(fixup_multi_kernel(fast, h->K > 256), 8 * h->num_sms, 128, 0, st, true, fm));
+             launch(fixup_multi_kernel(fast, h->K > 256), h->num_sms, 128, 0, st, true, fm));  // small calls: one CTA per SM dispatches faster than 8
     }
   }
   return BLADE_OK;
@@ -957,11 +972,12 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   const CarveScope carve(small_call_carveout(N, p.u[0].n(), p.W[0]));
   const int nsel = L == 1 ? 1 : L - 1;
   std::vector<std::pair<int, DownArgs>> fix_args;  // (level, args), for the merged fix-up launch
-  const bool merge_fix = fixups_merged(nsel, N, p.H[0], p.W[0]);
+  const bool ifix = inline_fixups(N, p.H[0], p.W[0], run_stages);
+  const bool merge_fix = !ifix && fixups_merged(nsel, N, p.H[0], p.W[0]);
   CUDA_TRY(cudaMemsetAsync(B.fb_cnt, 0, sizeof(unsigned int) * nsel, st));
   blade_status s;
   for (int l = 0; l < nsel; ++l)
-    if ((s = down_level(h, p, B, in_view, ws, st, run_stages, l, merge_fix ? &fix_args : nullptr)) != BLADE_OK)
+    if ((s = down_level(h, p, B, in_view, ws, st, run_stages, l, merge_fix ? &fix_args : nullptr, ifix)) != BLADE_OK)
       return s;
   if (merge_fix && (s = merged_fixups(h, fix_args, st)) != BLADE_OK) return s;
   if (!run_stages) return BLADE_OK;
@@ -991,6 +1007,15 @@ const char* blade_ms_status_string(blade_status s) {
 }
 
 const char* blade_ms_last_error(void) { return g_last_error.c_str(); }
+
+#ifdef BLADE_TRACE
+// Latency probes only (BLADE_TRACE builds): kernel-kind timestamps of the k_down / k_stage_tma
+// translation units, [2][16][3] (entry, griddepcontrol.wait return, exit; %globaltimer ns).
+void blade_ms_trace(unsigned long long* out, int reset) {
+  tables::trace_down(out, reset != 0);
+  tables::trace_tma(out ? out + 48 : nullptr, reset != 0);
+}
+#endif
 
 blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layout* bl, const float* taps,
                              size_t n_taps, int device, blade_ms_t* out) {
@@ -1370,8 +1395,11 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
   // either way), and it leaves the merged fix-ups
   const bool fused = h->has_fsel && L > 1 && fuse_sel_enabled() && use_ry4(h, N, W, H + (H & 1));
   const int merged = fused ? nsel - 1 : nsel;
+  const int fixes = inline_fixups(N, H, W, true)        ? 0
+                    : fixups_merged(nsel, N, H, W) ? (merged + kFixMax - 1) / kFixMax + (fused ? 1 : 0)
+                                                   : nsel;
   *count = N == 0 ? 0
-                  : 2 * nsel + (fixups_merged(nsel, N, H, W) ? (merged + kFixMax - 1) / kFixMax + (fused ? 1 : 0) : nsel) +
+                  : 2 * nsel + fixes +
                         (h->cfg.n_filter_channels == 3 ? 1 : 0) + (h->has_tma && W % 4 != 0 ? 1 : 0);
   return BLADE_OK;
 }

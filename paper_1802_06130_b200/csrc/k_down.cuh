@@ -263,12 +263,68 @@ __device__ __forceinline__ int bucket32(float a, float b, float c, const DownPar
   return (o * prm.n_s + s) * prm.n_c + k;
 }
 
+// The fields of one level a fix-up needs, read once per pixel from the (dynamically indexed)
+// kernel parameters into registers.
+struct FixLevel {
+  const float* zhi;
+  const float* zlo;
+  void* map;
+  const unsigned long long* fb_list;
+  long long in_frame, in_plane;
+  int H, W, in_row0, in_rows, in_pitch, s_r0, s_rn, map_pitch;
+  __device__ __forceinline__ explicit FixLevel(const DownArgs& a)
+      : zhi(a.zhi), zlo(a.zlo), map(a.map), fb_list(a.fb_list), in_frame(a.in_frame), in_plane(a.in_plane),
+        H(a.H), W(a.W), in_row0(a.in_row0), in_rows(a.in_rows), in_pitch(a.in_pitch), s_r0(a.s_r0), s_rn(a.s_rn),
+        map_pitch(a.map_pitch) {}
+};
+
+// The fp64 bucket of pixel (n, y, xx) of a level (whole warp; lane t < 25 evaluates window tap
+// (t / 5 - 2, t % 5 - 2)); every lane returns it.
+template <bool FAST>
+__device__ __forceinline__ int fix_bucket(const FixLevel& a, const DownParams& prm, int n, int y, int xx, int lane) {
+  const bool hilo = a.zlo != nullptr;
+  double pa = 0.0, pb = 0.0, pc = 0.0;
+  if (lane < 25) {
+    const int dy = lane / 5 - 2, dx = lane % 5 - 2;
+    auto Z = [&](int c, int yy, int xq) -> double {
+      int br = fold_idx(yy, a.H) - a.in_row0;
+      br = min(max(br, 0), a.in_rows - 1);
+      const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.in_pitch + fold_idx(xq, a.W);
+      double v = (double)a.zhi[o];
+      if (hilo) v += (double)a.zlo[o];
+      return v;
+    };
+    const int yy = y + dy, xq = xx + dx;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double gx = Z(c, yy, xq + 1) - Z(c, yy, xq - 1);
+      const double gy = Z(c, yy + 1, xq) - Z(c, yy - 1, xq);
+      pa = fma(gx, gx, pa);
+      pb = fma(gx, gy, pb);
+      pc = fma(gy, gy, pc);
+    }
+    const double wgt = prm.wp[dy + 2] * prm.wp[dx + 2];
+    pa *= wgt;
+    pb *= wgt;
+    pc *= wgt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pa += __shfl_xor_sync(0xffffffffu, pa, o);
+    pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  }
+  return bucket_of<FAST>(pa, pb, pc, prm);
+}
+
 // grid: ceil(n_tasks / WARPS) CTAs of 32 * WARPS threads; task = (frame, band, strip), strip fastest.
 // COPY (level 0 only): also write the input rows into a.zcopy (16-B row pitch) for the TMA stage
 // when the caller's rows are not 16-B multiples.
 // SEL = false (level 0 when the stage computes the selector itself, DESIGN.md §6 "fused
 // selector"): decimation (and COPY) only; no map, no fix-up list.
-template <bool HILO, bool DEC, bool FAST, bool WIDE, bool COPY = false, bool SEL = true>
+// IFIX (small calls): an uncertified pixel is recomputed in fp64 by the whole warp right away
+// (fix_bucket, the fix-up kernel's arithmetic) instead of being queued for a fix-up launch.
+template <bool HILO, bool DEC, bool FAST, bool WIDE, bool COPY = false, bool SEL = true, bool IFIX = false>
 __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const DownArgs a, const DownParams prm) {
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;  // bucket map entry
   using namespace down;
@@ -276,9 +332,11 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
   extern __shared__ __align__(16) float dsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x * WARPS + warp;
+  BT_ENTRY(HILO ? 1 : 0);
   pdl_trigger();
   if (task >= a.n_tasks) return;
   pdl_wait();
+  BT_WAITED(HILO ? 1 : 0);
   float* ring = dsm + (size_t)warp * RING * NP * 64 + 2 * lane;  // this lane's 2 columns
 
   const int strip = task % a.n_strips;
@@ -543,7 +601,21 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
         const int bk0 = bucket32<FAST>(fa.x, fb.x, fc.x, prm, safe0);
         const int bk1 = bucket32<FAST>(fa.y, fb.y, fc.y, prm, safe1);
         const bool need_fb = emit && ((x < a.W && !safe0) || (x + 1 < a.W && !safe1));
-        if (need_fb) {  // rare: queue the uncertified pixel(s) for the fp64 fix-up kernel
+        int b0 = bk0, b1 = bk1;
+        if constexpr (IFIX) {  // rare: the uncertified pixels of this row, one fp64 warp pass each
+          unsigned int m0 = __ballot_sync(0xffffffffu, emit && x < a.W && !safe0);
+          unsigned int m1 = __ballot_sync(0xffffffffu, emit && x + 1 < a.W && !safe1);
+          while (m0 | m1) {  // warp-uniform
+            const int j = m0 ? 0 : 1;
+            const int src = __ffs(j == 0 ? m0 : m1) - 1;
+            if (j == 0) m0 &= m0 - 1; else m1 &= m1 - 1;
+            const int xx = __shfl_sync(0xffffffffu, x, src) + j;
+            const int k = fix_bucket<FAST>(FixLevel(a), prm, n, y, xx, lane);
+            if (lane == src) {
+              if (j == 0) b0 = k; else b1 = k;
+            }
+          }
+        } else if (need_fb) {  // rare: queue the uncertified pixel(s) for the fp64 fix-up kernel
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             if (x + j >= a.W) continue;
@@ -556,12 +628,12 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
           MT* mrow = mrow_i;
           if (map16 && x + 1 < a.W) {  // both entries in one store
             if constexpr (WIDE)
-              *reinterpret_cast<uint32_t*>(mrow) = (uint32_t)bk0 | ((uint32_t)bk1 << 16);
+              *reinterpret_cast<uint32_t*>(mrow) = (uint32_t)b0 | ((uint32_t)b1 << 16);
             else
-              *reinterpret_cast<uint16_t*>(mrow) = (uint16_t)(bk0 | (bk1 << 8));
+              *reinterpret_cast<uint16_t*>(mrow) = (uint16_t)(b0 | (b1 << 8));
           } else {
-            mrow[0] = (MT)bk0;
-            if (x + 1 < a.W) mrow[1] = (MT)bk1;
+            mrow[0] = (MT)b0;
+            if (x + 1 < a.W) mrow[1] = (MT)b1;
           }
         }
       }
@@ -583,6 +655,7 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
       lR[c] = nlR[c];
     }
   }
+  BT_EXIT(HILO ? 1 : 0);
 }
 
 // Fix-up of the uncertified pixels of one k_down launch: fp64 (a, b, c) and the bucket rule in
@@ -654,21 +727,6 @@ struct FixupMulti {
   int n;  // levels in use
 };
 
-// The fields of one level a fix-up needs, read once per pixel from the (dynamically indexed)
-// kernel parameters into registers.
-struct FixLevel {
-  const float* zhi;
-  const float* zlo;
-  void* map;
-  const unsigned long long* fb_list;
-  long long in_frame, in_plane;
-  int H, W, in_row0, in_rows, in_pitch, s_r0, s_rn, map_pitch;
-  __device__ __forceinline__ explicit FixLevel(const DownArgs& a)
-      : zhi(a.zhi), zlo(a.zlo), map(a.map), fb_list(a.fb_list), in_frame(a.in_frame), in_plane(a.in_plane),
-        H(a.H), W(a.W), in_row0(a.in_row0), in_rows(a.in_rows), in_pitch(a.in_pitch), s_r0(a.s_r0), s_rn(a.s_rn),
-        map_pitch(a.map_pitch) {}
-};
-
 template <bool FAST, bool WIDE>
 __device__ __forceinline__ void fixup_pixel(const FixLevel& a, const DownParams& prm, unsigned long long i,
                                             bool all, int lane) {
@@ -678,47 +736,18 @@ __device__ __forceinline__ void fixup_pixel(const FixLevel& a, const DownParams&
   const int n = (int)(e / per_frame);
   const unsigned long long r = e - (unsigned long long)n * per_frame;
   const int y = a.s_r0 + (int)(r / a.W), xx = (int)(r % a.W);
-  const bool hilo = a.zlo != nullptr;
-  double pa = 0.0, pb = 0.0, pc = 0.0;
-  if (lane < 25) {
-    const int dy = lane / 5 - 2, dx = lane % 5 - 2;
-    auto Z = [&](int c, int yy, int xq) -> double {
-      int br = fold_idx(yy, a.H) - a.in_row0;
-      br = min(max(br, 0), a.in_rows - 1);
-      const long long o = (long long)n * a.in_frame + c * a.in_plane + (long long)br * a.in_pitch + fold_idx(xq, a.W);
-      double v = (double)a.zhi[o];
-      if (hilo) v += (double)a.zlo[o];
-      return v;
-    };
-    const int yy = y + dy, xq = xx + dx;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double gx = Z(c, yy, xq + 1) - Z(c, yy, xq - 1);
-      const double gy = Z(c, yy + 1, xq) - Z(c, yy - 1, xq);
-      pa = fma(gx, gx, pa);
-      pb = fma(gx, gy, pb);
-      pc = fma(gy, gy, pc);
-    }
-    const double wgt = prm.wp[dy + 2] * prm.wp[dx + 2];
-    pa *= wgt;
-    pb *= wgt;
-    pc *= wgt;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    pa += __shfl_xor_sync(0xffffffffu, pa, o);
-    pb += __shfl_xor_sync(0xffffffffu, pb, o);
-    pc += __shfl_xor_sync(0xffffffffu, pc, o);
-  }
+  const int k = fix_bucket<FAST>(a, prm, n, y, xx, lane);
   if (lane == 0)
     static_cast<MT*>(a.map)[((unsigned long long)n * a.s_rn + (unsigned long long)(y - a.s_r0)) * a.map_pitch + xx] =
-        (MT)bucket_of<FAST>(pa, pb, pc, prm);
+        (MT)k;
 }
 
 template <bool FAST, bool WIDE>
 __global__ void __launch_bounds__(128) k_down_fixup_multi(const __grid_constant__ FixupMulti m) {
+  BT_ENTRY(2);
   pdl_trigger();
   pdl_wait();
+  BT_WAITED(2);
   unsigned long long items[kFixMax];
   bool all[kFixMax];
   unsigned long long total = 0;
@@ -747,6 +776,7 @@ __global__ void __launch_bounds__(128) k_down_fixup_multi(const __grid_constant_
     }
     fixup_pixel<FAST, WIDE>(FixLevel(m.a[l]), m.prm[l], j, all[l], lane);
   }
+  BT_EXIT(2);
 }
 
 }  // namespace blade

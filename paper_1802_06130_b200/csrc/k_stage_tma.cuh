@@ -398,6 +398,8 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
   const int ctid = threadIdx.y * SS::BX + threadIdx.x;
   int t = cta + g * nctas;
   const int tstride = G * nctas;
+  [[maybe_unused]] const int bt_k = 8 + 2 * (a.W >= 512 ? 1 : 0);  // trace kind (probe builds)
+  BT_ENTRY(bt_k);
   pdl_trigger();
   if (ctid == 0) {
     mbar_init(&mbar[0], 1);
@@ -412,9 +414,11 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
     }
   }
   pdl_wait();
+  BT_WAITED(bt_k);
   __syncthreads();
   if (tid == 0 && t < a.n_tiles) issue(t, g);
   if (!WIDE) mbar_wait(&mbar[2], 0);
+  BT_WAITED(bt_k + 1);  // bank resident
 
   for (int it = 0; t < a.n_tiles; ++it, t += tstride) {
     const int b = G == 2 ? g : (it & 1);
@@ -435,12 +439,21 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
     const bool fine_border = FX < 0 || FX + SS::FCB > a.W || Y0 - SS::FH < 0 || Y0 + SS::TROWS + SS::FH > a.H;
     const bool coarse_border = NC > 0 && (CX < 0 || CX + SS::CCB > a.W1 || Y0 / 2 - RC < 0 ||
                                           Y0 / 2 - RC + SS::CR > a.H1);
-    if (fine_border || coarse_border) {
+    // only the box cells some in-range output pixel reads are fixed up (the output rows of the
+    // tile and its in-image columns, +- the footprint): on levels narrower or shorter than a tile
+    // most of the box lies outside the image and is never read (c0: 64 x 64 in a 20 x 136 box)
+    const int py_lo = max(Y0, a.o_r0), py_hi = min(Y0 + SS::TROWS, a.o_r0 + a.o_rn);
+    const int px_hi = min(X0 + SS::TCOLS, a.W);
+    if ((fine_border || coarse_border) && py_lo < py_hi) {
       if (fine_border) {
-        const OobBox ob = oob_box(SS::FR, SS::FCB, Y0 - SS::FH, FX, a.H, a.W);
+        const int r0 = max(0, py_lo - SS::FH - (Y0 - SS::FH)), r1 = min(SS::FR, py_hi + SS::FH - (Y0 - SS::FH));
+        const int c0 = max(0, X0 - SS::FH - FX), c1 = min(SS::FCB, px_hi + SS::FH - FX);
+        const OobBox ob = oob_box(r1 - r0, c1 - c0, Y0 - SS::FH + r0, FX + c0, a.H, a.W);
         for (int i = tid; i < ob.n; i += SS::threads) {
           int r, q;
           oob_cell(ob, i, r, q);
+          r += r0;
+          q += c0;
           const int gy = Y0 - SS::FH + r, gx = FX + q;
           const int fy = fold_idx(gy, a.H), fx = fold_idx(gx, a.W);
           const int ry = fy - (Y0 - SS::FH), rx = fx - FX;
@@ -461,10 +474,14 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
       if constexpr (NC > 0) {
         if (coarse_border) {
           const int CY0 = Y0 / 2 - RC, CX0 = CX;
-          const OobBox ob = oob_box(SS::CR, SS::CCB, CY0, CX0, a.H1, a.W1);
+          const int r0 = max(0, py_lo / 2 - RC - CY0), r1 = min(SS::CR, (py_hi - 1) / 2 + RC + 1 - CY0);
+          const int c0 = max(0, X0 / 2 - RC - CX0), c1 = min(SS::CCB, (px_hi - 1) / 2 + RC + 1 - CX0);
+          const OobBox ob = oob_box(r1 - r0, c1 - c0, CY0 + r0, CX0 + c0, a.H1, a.W1);
           for (int i = tid; i < ob.n; i += SS::threads) {
             int r, q;
             oob_cell(ob, i, r, q);
+            r += r0;
+            q += c0;
             const int gy = CY0 + r, gx = CX0 + q;
             const int fy = fold_idx(gy, a.H1), fx = fold_idx(gx, a.W1);
             const int ry = fy - CY0, rx = fx - CX0;
@@ -617,6 +634,7 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
       issue(tn, b);
     }
   }
+  BT_EXIT(bt_k);
 }
 
 // Fix-up of the fused-selector stage (level 0): the pixels whose fp32 orientation the certificate

@@ -34,6 +34,36 @@ struct LevelView {
 // drains. pdl_wait() blocks until the previous grid has completed and its writes are visible;
 // pdl_trigger() lets the next grid launch. Both are no-ops for a normal launch.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// BLADE_TRACE builds (latency probes only): per kernel kind, the first CTA entry, the last
+// griddepcontrol.wait return and the last warp exit (%globaltimer ns), read by blade_ms_trace().
+#ifdef BLADE_TRACE
+static __device__ unsigned long long g_trace[16][3];
+__device__ __forceinline__ unsigned long long bt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BT_ENTRY(k) \
+  if (threadIdx.x == 0 && threadIdx.y == 0) atomicMin(&g_trace[k][0], bt_now())
+#define BT_WAITED(k) \
+  if (threadIdx.x == 0 && threadIdx.y == 0) atomicMax(&g_trace[k][1], bt_now())
+#define BT_EXIT(k) \
+  if ((threadIdx.x & 31) == 0) atomicMax(&g_trace[k][2], bt_now())
+#define BT_DEFINE_ACCESS(name)                                                              \
+  void name(unsigned long long* out, bool reset) {                                          \
+    if (out) cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));                           \
+    if (reset) {                                                                            \
+      unsigned long long init[16][3];                                                       \
+      for (int i = 0; i < 16; ++i) init[i][0] = ~0ull, init[i][1] = 0, init[i][2] = 0;      \
+      cudaMemcpyToSymbol(g_trace, init, sizeof(init));                                      \
+    }                                                                                       \
+  }
+#else
+#define BT_ENTRY(k)
+#define BT_WAITED(k)
+#define BT_EXIT(k)
+#endif
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // [R2] half-sample symmetric fold, periodic with period 2n.

@@ -48,5 +48,8 @@ const std::vector<TmaVariant>& tma_variants() {
   };
   return v;
 }
+#ifdef BLADE_TRACE
+BT_DEFINE_ACCESS(trace_tma)
+#endif
 }  // namespace tables
 }  // namespace blade

@@ -49,7 +49,7 @@ const std::vector<TmaVariant>& ph_variants();
 using DownKernel = void (*)(const DownArgs, const DownParams);
 // FAST: the configs' bucket layout (16 orientations x 3 strength x 3 coherence bins)
 // wide: uint16 bucket maps (K > 256, NEXT f2)
-DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy = false);
+DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy = false, bool ifix = false);
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide);
 // level-0 decimation (+ input copy) without the selector: the fused-selector stage computes s^0
 DownKernel dec_kernel(bool copy);
@@ -69,5 +69,9 @@ TrainKernel train_hist(bool wide);
 TrainKernel train_scatter(bool wide);
 TrainKernel train_scan();
 
+#ifdef BLADE_TRACE
+void trace_down(unsigned long long* out, bool reset);  // [16][3]: entry, waited, exit (ns)
+void trace_tma(unsigned long long* out, bool reset);
+#endif
 }  // namespace tables
 }  // namespace blade
