@@ -865,10 +865,10 @@ blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView
         a.sw0 = (float)dp.wp[0];
         a.sw1 = (float)dp.wp[1];
         a.sw2 = (float)dp.wp[2];
-        a.ts2[0] = dp.ts2[0];
-        a.ts2[1] = dp.ts2[1];
-        a.kc2[0] = dp.kc2[0];
-        a.kc2[1] = dp.kc2[1];
+        a.tsR[0] = dp.tsR[0];
+        a.tsR[1] = dp.tsR[1];
+        a.kcR[0] = dp.kcR[0];
+        a.kcR[1] = dp.kcR[1];
         a.tc_nonpos = dp.tc_nonpos;
         a.fb_list = reinterpret_cast<unsigned long long*>(ws + p.fb_off[0]);
         a.fb_count = B.fb_cnt;
@@ -1199,9 +1199,11 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     dp.n_s = bl->n_strength;
     dp.n_c = bl->n_coherence;
     for (int i = 0; i < kMaxThr2; ++i) dp.ts2[i] = dp.kc2[i] = INFINITY;
+    for (int i = 0; i < 2; ++i) dp.tsR[i] = dp.kcR[i] = INFINITY;
     for (int i = 0; i < bl->n_strength - 1; ++i) {
       const double t = bl->strength_thresholds[(size_t)s * (bl->n_strength - 1) + i];
       dp.ts2[i] = t <= 0.0 ? -INFINITY : (float)(t * t);  // S >= t <=> l1 >= t^2 (t > 0)
+      if (i < 2) dp.tsR[i] = t <= 0.0 ? -INFINITY : (float)(8.0 * t * t);  // <=> T + R >= 8 t^2
     }
     int npos = 0;
     for (int i = 0; i < bl->n_coherence - 1; ++i) {
@@ -1210,6 +1212,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
         dp.tc_nonpos += 1;
       } else {
         const double kap = 2.0 * t / (1.0 + t * t);  // C >= t <=> r >= kappa h
+        if (npos < 2) dp.kcR[npos] = (float)kap;  // <=> R > kappa T (FAST selector)
         dp.kc2[npos++] = (float)(kap * kap);
       }
     }

@@ -22,6 +22,7 @@
 // element is converted exactly once, by the lane that loads it.
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
 #include <type_traits>
 
@@ -36,6 +37,8 @@ struct DownParams {
   float ts2[kMaxThr2];   // strength thresholds squared (-inf for t <= 0, +inf padding)
   float kc2[kMaxThr2];   // positive coherence thresholds: (2t / (1 + t^2))^2 (+inf padding)
   int tc_nonpos;         // # coherence thresholds <= 0 (always passed)
+  float tsR[2];          // FAST selector (bucket32_fast): 8 t^2 per strength threshold (-inf for t <= 0)
+  float kcR[2];          // FAST selector: kappa = 2t / (1 + t^2) per positive coherence threshold (+inf padding)
   int quad_edges;        // n_o % 4 == 0 and n_o <= 64: quadrant + edge-count orientation
   float ecos[16], esin[16];  // interior edges 2 pi j / n_o, j = 1 .. n_o/4 - 1
 };
@@ -176,8 +179,66 @@ __device__ __forceinline__ int bucket_of(double a, double b, double c, const Dow
 // well-conditioned: their fp32 errors (~1e-6 relative) stay far inside the 1e-5 parity window.
 constexpr float kCert = 64.0f * 5.9604644775390625e-8f;
 
+__host__ __device__ __forceinline__ unsigned int f32_bits(float x) {
+#ifdef __CUDA_ARCH__
+  return __float_as_uint(x);
+#else
+  unsigned int u;
+  memcpy(&u, &x, 4);
+  return u;
+#endif
+}
+__host__ __device__ __forceinline__ float sqrt_approx(float x) {
+#ifdef __CUDA_ARCH__
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+#else
+  return sqrtf(x);
+#endif
+}
+
+// FAST layout (16 orientations x 3 strengths x 3 coherences), the same decisions as the generic
+// bucket32 below with about half the instructions (the selector's largest cost, ncu/SASS of
+// k_down: 70 instructions per pixel -> ~40):
+//   orientation: the bin of psi = angle of (X, Y) = (-D, -2b) (D = a - c) is found by REFLECTION
+//     instead of rotation: alpha = angle of (|X|, |Y|) in [0, pi/2], m = # of the interior edges
+//     pi/8, pi/4, 3 pi/8 at or below alpha (three cross-product signs, read from sign bits), and
+//     o = 8 [Y < 0] + (m, or 7 - m when X and Y have opposite signs: psi = pi - alpha or
+//     2 pi - alpha). The sign tests are the rotated form's up to the order of the two operands
+//     (the same error bound); a certified pixel clears every one by 64 u T, so no test is a tie
+//     and the reflection gives the exact bin. T = 0 (no gradient anywhere in the window) is
+//     theta = 0, certified [R5]; any other isotropic tensor (D = b = 0) fails the certificate.
+//   strength / coherence with R = sqrt(D^2 + 4 b^2) (sqrt.approx, ~2 ulp): with the unscaled x4
+//     sums, l1 = (T + R) / 8 and r / h = R / T, so S >= t <=> T + R >= 8 t^2 (tsR) and
+//     C >= t <=> R > kappa T (kcR; strict, so T = 0 gives C = 0 [R6]). These features are
+//     well-conditioned: the fp32 error (~3e-7 relative) stays far inside the 1e-5 parity window.
+__host__ __device__ __forceinline__ int bucket32_fast(float a, float b, float c, const float* tsR, const float* kcR,
+                                                      int tc_nonpos, bool& safe) {
+  const float T = a + c, D = a - c, B2 = b + b;
+  const float ax = fabsf(D), ay = fabsf(B2);
+  constexpr float c1 = 0.92387953251128674f, s1 = 0.38268343236508978f;  // pi/8
+  constexpr float c2 = 0.70710678118654752f;                              // pi/4
+  const float e1 = fmaf(c1, ay, -s1 * ax), e2 = fmaf(c2, ay, -c2 * ax), e3 = fmaf(s1, ay, -c1 * ax);
+  const float mn = fminf(fminf(fminf(ax, ay), fminf(fabsf(e1), fabsf(e2))), fabsf(e3));
+  const bool zero = T == 0.0f && b == 0.0f;
+  safe = zero || mn > kCert * T;
+  // t = m = 3 - # negative edge tests; flip (X, Y of opposite signs) -> 7 - t; + 8 when Y < 0
+  const int t = 3 - (int)((f32_bits(e1) >> 31) + (f32_bits(e2) >> 31) + (f32_bits(e3) >> 31));
+  const int fm = (int)(f32_bits(D) ^ f32_bits(b)) >> 31;  // X = -D, Y = -2b: sign(X) != sign(Y)
+  const int lm = ~((int)f32_bits(b) >> 31);                // Y < 0 <=> b > 0
+  int o = (t ^ fm) + (fm & 8) + (lm & 8);
+  o = zero ? 0 : o;
+  const float R = sqrt_approx(fmaf(B2, B2, D * D));
+  const float TR = T + R;
+  const int s = (TR >= tsR[0]) + (TR >= tsR[1]);
+  const int k = tc_nonpos + (R > kcR[0] * T) + (R > kcR[1] * T);
+  return (o * 3 + s) * 3 + k;
+}
+
 template <bool FAST>
 __device__ __forceinline__ int bucket32(float a, float b, float c, const DownParams& prm, bool& safe) {
+  if constexpr (FAST) return bucket32_fast(a, b, c, prm.tsR, prm.kcR, prm.tc_nonpos, safe);
   constexpr int MAXT = FAST ? 2 : kMaxThr2;
   const float T = a + c;
   const float Df = a - c;

@@ -228,7 +228,7 @@ struct StageTmaArgs {
   // FSEL: the selector of the tile (FAST layout), fp32 with the certificate of k_down; the
   // uncertified in-range pixels are queued (map-index format of k_down) for k_stage_fixup
   float sw0, sw1, sw2;            // window weights at offsets 2, 1, 0 (symmetric)
-  float ts2[2], kc2[2];           // DownParams' transformed thresholds
+  float tsR[2], kcR[2];           // DownParams' transformed thresholds (FAST selector)
   int tc_nonpos;
   unsigned long long* fb_list;
   unsigned int* fb_count;
@@ -247,10 +247,10 @@ template <int RY, int FR, int FCB, int FH, int TCOLS>
 __device__ __forceinline__ void fused_buckets(const float* sf, uint8_t* smap, int ty, int tx, int n, int y, int x,
                                               const StageTmaArgs& a) {
   DownParams prm;
-  prm.ts2[0] = a.ts2[0];
-  prm.ts2[1] = a.ts2[1];
-  prm.kc2[0] = a.kc2[0];
-  prm.kc2[1] = a.kc2[1];
+  prm.tsR[0] = a.tsR[0];
+  prm.tsR[1] = a.tsR[1];
+  prm.kcR[0] = a.kcR[0];
+  prm.kcR[1] = a.kcR[1];
   prm.tc_nonpos = a.tc_nonpos;
   const float* zb = sf + (RY * ty + FH - 3) * FCB + 4 * tx;  // box row of y - 3, column of x - 4
   float zp[3][8], zc[3][10];  // Z(r - 1) at columns x-2 .. x+5, Z(r) at x-3 .. x+6
