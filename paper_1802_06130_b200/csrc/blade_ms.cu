@@ -497,6 +497,22 @@ bool inline_fixups(long long N, long long H, long long W, bool run_stages) {
   return run_stages && N * H * W <= max_px;
 }
 
+// Small calls run the down pass as k_down_tile (2-D tiles, uncertified pixels fixed inline in
+// fp64; bit-identical to k_down): every phase is spread over a CTA with short independent chains
+// instead of k_down's ~10 dependent rows per warp, and no fix-up launch follows. FAST bucket layout,
+// stage-running calls (the selector diagnostic keeps the fix-up list), level-0 rows that need no
+// 16-B input copy. BLADE_DOWN_TILE=<max px> moves the size threshold (0: never; A/B and tests).
+// c1 recipe, one frame, CUDA graph (profiles/r02_down_tile.txt): 256^2 49.1 -> 36.9 us, 512^2
+// 53.2 -> 45.1, 768^2 63.5 -> 59.4; 1024^2 79.9 -> 84.0 (streaming k_down wins from here).
+bool tile_down(const blade_ms* h, long long N, long long H, long long W, bool run_stages) {
+  static const long long max_px = [] {
+    const char* e = getenv("BLADE_DOWN_TILE");
+    return e ? atoll(e) : (3LL << 18);  // crossover 768^2 .. 1024^2 (scripts/tile_threshold.py)
+  }();
+  const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
+  return run_stages && fast && N * H * W <= max_px && !(h->has_tma && W % 4 != 0);
+}
+
 // Shared-memory carveout of the launches of the current (small) call: consecutive kernels with
 // different L1 / shared-memory splits make the SMs reconfigure between launches, which small,
 // latency-bound calls feel (c1 flushed 63 -> 58 us, c0 24.6 -> 23.5 us; large batches keep the
@@ -631,7 +647,7 @@ bool fused_level0(const blade_ms* h, const Plan& p, const Bufs& B, LevelView in_
 // (rare) pixels whose fp32 orientation is uncertified. The level's fix-up counter must be zero.
 blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView in_view, char* ws,
                         cudaStream_t st, bool run_stages, int l, std::vector<std::pair<int, DownArgs>>* fix_args,
-                        bool ifix = false) {
+                        bool ifix = false, bool tile = false) {
   const int L = p.L, N = p.N;
   const std::vector<LevelView>& z32 = B.z32;
   const std::vector<float*>& zlo = B.zlo;
@@ -710,6 +726,13 @@ blade_status down_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelVi
     const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
     const bool wide = h->K > 256;
     const bool fused = l == 0 && B.fuse0;  // the level-0 stage computes s^0: decimation only
+    if (tile && !fused && !zcopy && fast) {  // small call: the 2-D tile form, fixes inline
+      const dim3 grid((unsigned)((p.W[l] + dtile::TX - 1) / dtile::TX), (unsigned)((span + dtile::TY - 1) / dtile::TY),
+                      (unsigned)N);
+      LAUNCH("k_down_tile", launch(down_tile_kernel(hilo, dec, wide), grid, dtile::THREADS, dtile::smem_bytes(hilo, dec),
+                                   st, l > 0, da, h->down[l]));
+      return BLADE_OK;
+    }
     auto fn = fused ? dec_kernel(zcopy) : down_kernel(hilo, dec, fast, wide, zcopy, ifix);
     const unsigned grid = (unsigned)((da.n_tasks + down::WARPS - 1) / down::WARPS);
     LAUNCH("k_down", launch(fn, grid, 32 * down::WARPS, down_smem(hilo), st, l > 0, da, h->down[l]));
@@ -972,12 +995,14 @@ blade_status enqueue(const blade_ms* h, const Plan& p, LevelView in_view, LevelV
   const CarveScope carve(small_call_carveout(N, p.u[0].n(), p.W[0]));
   const int nsel = L == 1 ? 1 : L - 1;
   std::vector<std::pair<int, DownArgs>> fix_args;  // (level, args), for the merged fix-up launch
-  const bool ifix = inline_fixups(N, p.H[0], p.W[0], run_stages);
-  const bool merge_fix = !ifix && fixups_merged(nsel, N, p.H[0], p.W[0]);
+  const bool tile = !B.fuse0 && tile_down(h, N, p.H[0], p.W[0], run_stages);
+  const bool ifix = !tile && inline_fixups(N, p.H[0], p.W[0], run_stages);
+  const bool merge_fix = !ifix && !tile && fixups_merged(nsel, N, p.H[0], p.W[0]);
   CUDA_TRY(cudaMemsetAsync(B.fb_cnt, 0, sizeof(unsigned int) * nsel, st));
   blade_status s;
   for (int l = 0; l < nsel; ++l)
-    if ((s = down_level(h, p, B, in_view, ws, st, run_stages, l, merge_fix ? &fix_args : nullptr, ifix)) != BLADE_OK)
+    if ((s = down_level(h, p, B, in_view, ws, st, run_stages, l, merge_fix ? &fix_args : nullptr, ifix, tile)) !=
+        BLADE_OK)
       return s;
   if (merge_fix && (s = merged_fixups(h, fix_args, st)) != BLADE_OK) return s;
   if (!run_stages) return BLADE_OK;
@@ -1278,6 +1303,11 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
           for (int cp = 0; cp < 2 && ce == cudaSuccess; ++cp)
             ce = cudaFuncSetAttribute(down_kernel(hl, dc, sm == 1, sm == 2, cp && !hl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)down_smem(hl));
+    for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl)
+      for (int dc = 0; dc < 2 && ce == cudaSuccess; ++dc)
+        for (int wd = 0; wd < 2 && ce == cudaSuccess; ++wd)
+          ce = cudaFuncSetAttribute(down_tile_kernel(hl, dc, wd), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)dtile::smem_bytes(hl, dc));
   }
   for (int hl = 0; hl < 2 && ce == cudaSuccess; ++hl) {
     int oc = 0;
@@ -1398,7 +1428,7 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
   // either way), and it leaves the merged fix-ups
   const bool fused = h->has_fsel && L > 1 && fuse_sel_enabled() && use_ry4(h, N, W, H + (H & 1));
   const int merged = fused ? nsel - 1 : nsel;
-  const int fixes = inline_fixups(N, H, W, true)        ? 0
+  const int fixes = tile_down(h, N, H, W, true) || inline_fixups(N, H, W, true) ? 0
                     : fixups_merged(nsel, N, H, W) ? (merged + kFixMax - 1) / kFixMax + (fused ? 1 : 0)
                                                    : nsel;
   *count = N == 0 ? 0

@@ -49,6 +49,13 @@ struct DownParams {
 #ifndef BLADE_DOWN_PACK
 #define BLADE_DOWN_PACK 1
 #endif
+// CTAs per SM the level >= 1 (hi/lo) variant is compiled for (A/B builds)
+#ifndef BLADE_DOWN_HILO_MINB
+#define BLADE_DOWN_HILO_MINB 3
+#endif
+#ifndef BLADE_DOWN_LO_MINB
+#define BLADE_DOWN_LO_MINB 4
+#endif
 namespace down {
 constexpr int WARPS = 4;        // independent warps per CTA
 #ifndef BLADE_DOWN_RING
@@ -386,7 +393,7 @@ __device__ __forceinline__ int fix_bucket(const FixLevel& a, const DownParams& p
 // IFIX (small calls): an uncertified pixel is recomputed in fp64 by the whole warp right away
 // (fix_bucket, the fix-up kernel's arithmetic) instead of being queued for a fix-up launch.
 template <bool HILO, bool DEC, bool FAST, bool WIDE, bool COPY = false, bool SEL = true, bool IFIX = false>
-__global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const DownArgs a, const DownParams prm) {
+__global__ void __launch_bounds__(32 * down::WARPS, HILO ? BLADE_DOWN_HILO_MINB : BLADE_DOWN_LO_MINB) k_down(const DownArgs a, const DownParams prm) {
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;  // bucket map entry
   using namespace down;
   constexpr int NP = HILO ? 6 : 3;  // planes per ring row (3 channels, x2 with lo)
@@ -480,9 +487,14 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
   }
 
   MT* mapf = static_cast<MT*>(a.map) + (long long)n * a.s_rn * a.map_pitch;
-  const long long ostride = (long long)a.d_buf_rows * a.out_pitch;  // channel plane of z^{l+1}
-  const long long oframe = 3 * (long long)n * ostride;
+  // channel plane of z^{l+1} (< 2^31 floats: a level-1 plane that large would need > 180 GB of
+  // level-0 input and output)
+  const int ostr32 = a.d_buf_rows * a.out_pitch;
   const int Xd = x >> 1;  // decimated column (x even)
+  // offset of z^{l+1} row Yd = (r - 4) / 2 at the lane's column, for the even rows r (odd i; the
+  // first is i = 1, r = Yb - 2); advanced by one row per even r
+  long long oo = 3 * (long long)n * ostr32 + (long long)((Yb - 6) / 2 - a.d_buf_row0) * a.out_pitch + Xd;
+  const bool has_lo = a.olo != nullptr;
   // 2-byte map stores when every map row starts 2-B aligned (x is even)
   const bool map16 = (a.map_pitch & 1) == 0 && (reinterpret_cast<uintptr_t>(a.map) & (2 * sizeof(MT) - 1)) == 0;
 
@@ -561,15 +573,20 @@ __global__ void __launch_bounds__(32 * down::WARPS, HILO ? 3 : 4) k_down(const D
       if (!odd_r) {
         const int Yd = (r - 4) / 2;  // completed row (r even)
         if (out_lane && Yd >= a.d_r0 && Yd < a.d_r0 + a.d_rn && Xd < a.W1 && i >= 7) {
-          const long long o = oframe + (long long)(Yd - a.d_buf_row0) * a.out_pitch + Xd;
+          float* ph = a.ohi + oo;  // channel planes at +ostr32 (one IMAD.WIDE per store)
+          float hi[3];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const double v = dacc[0][c];
-            const float hi = (float)v;
-            a.ohi[o + c * ostride] = hi;
-            if (a.olo) a.olo[o + c * ostride] = (float)(v - (double)hi);
+            hi[c] = (float)dacc[0][c];
+            ph[c * ostr32] = hi[c];
+          }
+          if (has_lo) {
+            float* pl = a.olo + oo;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) pl[c * ostr32] = (float)(dacc[0][c] - (double)hi[c]);
           }
         }
+        oo += a.out_pitch;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           dacc[0][c] = dacc[1][c];

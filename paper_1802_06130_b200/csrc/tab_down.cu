@@ -17,6 +17,13 @@ static DownKernel down_kernel_i(bool hilo, bool dec, bool fast, bool wide, bool 
 DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy, bool ifix) {
   return ifix ? down_kernel_i<true>(hilo, dec, fast, wide, copy) : down_kernel_i<false>(hilo, dec, fast, wide, copy);
 }
+DownKernel down_tile_kernel(bool hilo, bool dec, bool wide) {
+  if (wide)
+    return hilo ? (dec ? &k_down_tile<true, true, true> : &k_down_tile<true, false, true>)
+                : (dec ? &k_down_tile<false, true, true> : &k_down_tile<false, false, true>);
+  return hilo ? (dec ? &k_down_tile<true, true, false> : &k_down_tile<true, false, false>)
+              : (dec ? &k_down_tile<false, true, false> : &k_down_tile<false, false, false>);
+}
 DownKernel dec_kernel(bool copy) {
   return copy ? &k_down<false, true, true, false, true, false> : &k_down<false, true, true, false, false, false>;
 }

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "k_down.cuh"
+#include "k_down_tile.cuh"
 #include "k_stage_ph.cuh"
 #include "k_stage_tma.cuh"
 #include "k_train.cuh"
@@ -51,6 +52,8 @@ using DownKernel = void (*)(const DownArgs, const DownParams);
 // wide: uint16 bucket maps (K > 256, NEXT f2)
 DownKernel down_kernel(bool hilo, bool dec, bool fast, bool wide, bool copy = false, bool ifix = false);
 DownKernel fixup_kernel(bool hilo, bool fast, bool wide);
+// the small-level form of k_down (k_down_tile.cuh: 2-D tiles, inline fp64 fixes; FAST layout)
+DownKernel down_tile_kernel(bool hilo, bool dec, bool wide);
 // level-0 decimation (+ input copy) without the selector: the fused-selector stage computes s^0
 DownKernel dec_kernel(bool copy);
 using FixupMultiKernel = void (*)(const FixupMulti);

@@ -422,11 +422,57 @@ def test_c5_paper_bucket_layout_parity(H, W, N):
     assert h.map_dtype == torch.uint16
 
 
+# ------------------------------------------------------- small-call down pass (k_down_tile)
+
+_TILE_CASES = [("c1", 512, 512, 1), ("c1", 67, 132, 2), ("c0", 64, 64, 1), ("c0", 61, 100, 3),
+               ("c2", 130, 200, 1), ("c4", 203, 332, 1), ("c3", 136, 240, 2), ("c1", 9, 16, 1),
+               ("c1", 1024, 1024, 1)]
+
+
+def _tile_case_outputs(path):
+    outs = {}
+    for name, H, W, N in _TILE_CASES:
+        cfg = _cfg_like(name, H, W, N)
+        h = _handle(cfg)
+        outs[f"{name}_{H}x{W}x{N}"] = h.denoise(torch.from_numpy(cfg.batch()).cuda()).cpu().numpy()
+        outs[f"{name}_{H}x{W}x{N}_launches"] = np.array(h.launch_count(N, H, W))
+    np.savez(path, **outs)
+
+
+def test_down_tile_bit_identical(tmp_path):
+    """Small calls run the down pass as k_down_tile (2-D tiles, fp64 fixes inline) instead of
+    k_down: the same arithmetic in the same order, so the denoised outputs are bit-identical to the
+    streaming kernel's (run in a child process with BLADE_DOWN_TILE=0), with no fix-up launch."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    ref = tmp_path / "stream.npz"
+    code = ("import sys; sys.path.insert(0, %r); from tests.test_gpu_parity import _tile_case_outputs; "
+            "_tile_case_outputs(%r)" % (str(root), str(ref)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, "BLADE_DOWN_TILE": "0"},
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    mine = tmp_path / "tile.npz"
+    env_tile = os.environ.get("BLADE_DOWN_TILE")
+    _tile_case_outputs(mine)
+    a, b = np.load(ref), np.load(mine)
+    for name, H, W, N in _TILE_CASES:
+        k = f"{name}_{H}x{W}x{N}"
+        assert np.array_equal(a[k], b[k]), (k, np.abs(a[k] - b[k]).max())
+        if env_tile is None and N * H * W <= (3 << 18):  # default threshold: a small call
+            L = _cfg_like(name, H, W, N).levels
+            nsel = 1 if L == 1 else L - 1
+            assert int(b[k + "_launches"]) == 2 * nsel + (1 if W % 4 else 0), (k, int(b[k + "_launches"]))
+
+
 # ------------------------------------------------------------------------- forced kernel variants
 
 @pytest.mark.parametrize("env", [{"BLADE_TMA_RY": "4"}, {"BLADE_TMA_RY": "2"}, {"BLADE_PDL": "0"},
                                  {"BLADE_FUSE_SEL": "1", "BLADE_TMA_RY": "4"}, {"BLADE_CARVEOUT": "100"},
-                                 {"BLADE_INLINE_FIX": "0"}, {"BLADE_INLINE_FIX": "100000000"}])
+                                 {"BLADE_INLINE_FIX": "0"}, {"BLADE_INLINE_FIX": "100000000"},
+                                 {"BLADE_DOWN_TILE": "0"}, {"BLADE_DOWN_TILE": "100000000"}])
 def test_forced_variants_subprocess(env):
     """The library picks kernel variants by level size (4- vs 2-row TMA stage threads) and
     launches with programmatic dependent launch; the knobs are read once per process, so the
@@ -620,6 +666,8 @@ def test_deep_pyramid_merged_fixup(levels, H, W):
     # k_down (no fix-up launch); larger ones run the merged fix-up, ceil(nsel / 4) launches
     import os
     inline = H * W <= int(os.environ.get("BLADE_INLINE_FIX", 16384))
+    # small calls run k_down_tile (uncertified pixels fixed inline, no fix-up launch)
+    inline = inline or (H * W <= int(os.environ.get("BLADE_DOWN_TILE", 3 << 18)) and W % 4 == 0)
     # forced fused level-0 selector: level 0's fix-up is the stage fix-up, one more launch
     fused = os.environ.get("BLADE_FUSE_SEL") == "1" and os.environ.get("BLADE_TMA_RY") == "4"
     fixes = 0 if inline else (nsel + 2) // 4 + 1 if fused else (nsel + 3) // 4
