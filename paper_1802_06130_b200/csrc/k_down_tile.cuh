@@ -46,6 +46,46 @@ __host__ __device__ constexpr size_t smem_bytes(bool hilo, bool dec) {
 }
 }  // namespace dtile
 
+// fix_bucket (k_down.cuh) for a tile pixel at box coordinates (r0, q0), reading the staged box
+// instead of global memory: the box holds the same folded samples, converted the same way
+// ((double)hi + (double)lo), and the lanes, products, weights and butterfly order are
+// fix_bucket's, so the fp64 decision is bit-identical — at shared-memory instead of L2 latency
+// (the inline fixes were ~6 us of a 512 x 512 call's 47 us).
+template <bool HILO, bool DEC>
+__device__ __forceinline__ int fix_bucket_box(const float* bh, const float* bl, const double* zd, int r0, int q0,
+                                              const DownParams& prm, int lane) {
+  using namespace dtile;
+  double pa = 0.0, pb = 0.0, pc = 0.0;
+  if (lane < 25) {
+    const int dy = lane / 5 - 2, dx = lane % 5 - 2;
+    auto Z = [&](int c, int r, int q) -> double {
+      const int e = (c * BR + r) * BC + q;
+      if constexpr (DEC) return zd[e];
+      return HILO ? (double)bh[e] + (double)bl[e] : (double)bh[e];
+    };
+    const int r = r0 + dy, q = q0 + dx;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double gx = Z(c, r, q + 1) - Z(c, r, q - 1);
+      const double gy = Z(c, r + 1, q) - Z(c, r - 1, q);
+      pa = fma(gx, gx, pa);
+      pb = fma(gx, gy, pb);
+      pc = fma(gy, gy, pc);
+    }
+    const double wgt = prm.wp[dy + 2] * prm.wp[dx + 2];
+    pa *= wgt;
+    pb *= wgt;
+    pc *= wgt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pa += __shfl_xor_sync(0xffffffffu, pa, o);
+    pb += __shfl_xor_sync(0xffffffffu, pb, o);
+    pc += __shfl_xor_sync(0xffffffffu, pc, o);
+  }
+  return bucket_of<true>(pa, pb, pc, prm);
+}
+
 // grid: ceil(W / TX) x ceil(span / TY) x N CTAs of 256 threads; tile rows from a.base (even).
 template <bool HILO, bool DEC, bool WIDE>
 __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, const DownParams prm) {
@@ -76,7 +116,10 @@ __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, 
     const int fq1 = tx + 32 < BC ? fold_idx(X0 + 29 + tx, a.W) : 0;
     const float* fh = a.zhi + (long long)n * a.in_frame;
     const float* fl = HILO ? a.zlo + (long long)n * a.in_frame : nullptr;
-    for (int r = wp; r < BR; r += NW) {
+#pragma unroll
+    for (int rk = 0; rk < (BR + NW - 1) / NW; ++rk) {
+      const int r = wp + rk * NW;
+      if (r >= BR) break;
       int br = fold_idx(Y0 - 3 + r, a.H) - a.in_row0;
       br = min(max(br, 0), a.in_rows - 1);
       const long long ro = (long long)br * a.in_pitch;
@@ -122,7 +165,10 @@ __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, 
     P[PR * PC + e] = B;
     P[2 * PR * PC + e] = C;
   };
-  for (int i = wp; i < PR; i += NW) {
+#pragma unroll
+  for (int ik = 0; ik < (PR + NW - 1) / NW; ++ik) {
+    const int i = wp + ik * NW;
+    if (i >= PR) break;
     product(i, tx);
     if (tx + 32 < PC) product(i, tx + 32);
   }
@@ -130,7 +176,10 @@ __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, 
   const float w0 = (float)prm.wp[0], w1 = (float)prm.wp[1], w2 = (float)prm.wp[2];  // symmetric
 
   // ---- H: horizontal window at (Y0 - 2 + i, X0 + tx) over P columns tx .. tx + 4
-  for (int i = wp; i < PR; i += NW) {
+#pragma unroll
+  for (int ik = 0; ik < (PR + NW - 1) / NW; ++ik) {
+    const int i = wp + ik * NW;
+    if (i >= PR) break;
 #pragma unroll
     for (int qd = 0; qd < 3; ++qd) {
       const float* p = P + (qd * PR + i) * PC + tx + 2;
@@ -142,7 +191,10 @@ __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, 
     //      box columns 2k .. 2k + 7), k_down's order; (c, r) rows of 16 columns, two per warp
     constexpr double dw0 = -3.0 / 256.0, dw1 = -9.0 / 256.0, dw2 = 29.0 / 256.0, dw3 = 111.0 / 256.0;
     static_assert(DX == 16, "D1 maps 16 decimated columns to a half warp");
-    for (int e = tid; e < 3 * BR * DX; e += THREADS) {
+#pragma unroll
+    for (int ek = 0; ek < (3 * BR * DX + THREADS - 1) / THREADS; ++ek) {
+      const int e = tid + ek * THREADS;
+      if (e >= 3 * BR * DX) break;
       const int cr = e >> 4, k = e & 15;  // cr = c * BR + r
       const double* z = zd + cr * BC + 2 * k + 3;  // input column X0 + 2k
       double h = dw0 * (z[-3] + z[4]);
@@ -156,7 +208,10 @@ __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, 
 
   // ---- V + bucket: pixel (Y0 + i, X0 + j); a warp = one tile row (coalesced map stores)
   MT* mapf = static_cast<MT*>(a.map) + (long long)n * a.s_rn * a.map_pitch;
-  for (int i = wp; i < TY; i += NW) {
+  static_assert(TY % NW == 0, "V: whole warps per tile row");
+#pragma unroll
+  for (int ik = 0; ik < TY / NW; ++ik) {
+    const int i = wp + ik * NW;
     const int j = tx;
     const int y = Y0 + i, x = X0 + j;
     float f[3];
@@ -168,12 +223,16 @@ __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, 
     bool safe = true;
     int bk = bucket32<true>(f[0], f[1], f[2], prm, safe);
     const bool emit = y >= a.s_r0 && y < a.s_r0 + a.s_rn && x < a.W;
+#ifdef BLADE_TILE_NOFIX  // timing probe only: outputs invalid
+    unsigned int m = 0;
+#else
     unsigned int m = __ballot_sync(0xffffffffu, emit && !safe);  // rare: fp64 fix, whole warp
+#endif
     const int lane = tx;
     while (m) {
       const int src = __ffs(m) - 1;
       m &= m - 1;
-      const int k = fix_bucket<true>(FixLevel(a), prm, n, y, __shfl_sync(0xffffffffu, x, src), lane);
+      const int k = fix_bucket_box<HILO, DEC>(bh, bl, zd, i + 3, src + 3, prm, lane);  // j = lane
       if (lane == src) bk = k;
     }
     if (emit) mapf[(long long)(y - a.s_r0) * a.map_pitch + x] = (MT)bk;
@@ -184,7 +243,10 @@ __global__ void __launch_bounds__(dtile::THREADS) k_down_tile(const DownArgs a, 
     //      accumulation order (the ring adds w0 .. w7 in row order onto 0)
     constexpr double dw0 = -3.0 / 256.0, dw1 = -9.0 / 256.0, dw2 = 29.0 / 256.0, dw3 = 111.0 / 256.0;
     static_assert(DY == 8 && DX == 16, "D2 index by shifts");
-    for (int e = tid; e < 3 * DY * DX; e += THREADS) {
+#pragma unroll
+    for (int ek = 0; ek < (3 * DY * DX + THREADS - 1) / THREADS; ++ek) {
+      const int e = tid + ek * THREADS;
+      if (e >= 3 * DY * DX) break;
       const int c = e >> 7, i = (e >> 4) & 7, k = e & 15;
       const int Yd = Y0 / 2 + i, Xd = X0 / 2 + k;
       if (Yd < a.d_r0 || Yd >= a.d_r0 + a.d_rn || Xd >= a.W1) continue;
