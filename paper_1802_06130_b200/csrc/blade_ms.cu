@@ -448,15 +448,16 @@ int tma_ry() {
 }
 
 // Rows per thread of the TMA stage kernel for a level of width W whose computed rows span
-// `span`: large, wide levels (many tiles per SM, few border / partial tiles) take 4, others 2
-// (measured: c3 level 0 2.56 -> 2.36 ms, but level 1 (7.5 tiles wide) 0.75 -> 0.80 ms, and the
+// `span`: large levels (many tiles per SM) at least 8 tiles wide take 4, others 2 (measured: c3
+// level 0 2.56 -> 2.36 ms; c3 level 1, 7.5 tiles wide, 0.718 -> 0.675 ms on the round-2 build
+// (0.75 -> 0.80 in round 1, before the border fix-up was limited to the cells pixels read); the
 // latency-bound small levels are slower with 8 warps per SM).
 bool use_ry4(const blade_ms* h, int N, int W, int span) {
   if (!h->has_tma4 || tma_ry() == 2) return false;
   if (tma_ry() == 4) return true;
   const int tiles_x = (W + h->tma.tcols - 1) / h->tma.tcols;
   const long long tiles = (long long)N * tiles_x * ((span + h->tma.trows - 1) / h->tma.trows);
-  return tiles_x >= 12 && tiles >= 8LL * h->num_sms;
+  return tiles_x >= 8 && tiles >= 8LL * h->num_sms;
 }
 
 // The fp64 fix-ups of all selector levels run as one launch after the down pass on small calls

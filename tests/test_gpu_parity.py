@@ -494,13 +494,13 @@ def test_forced_variants_subprocess(env):
 
 def test_stage_kernel_selection():
     """The variant each level runs (blade_ms_stage_kernel): the bench's c3 level 0 takes the
-    4-row TMA kernel, its 7.5-tile-wide level 1 the 2-row one; 7x7 / 9x9 pairs the phase-split
+    4-row TMA kernel, and so does its 7.5-tile-wide level 1; a small call the 2-row one; 7x7 / 9x9 pairs the phase-split
     kernel; every width takes TMA (levels >= 1 live in the workspace with padded rows; a level-0
     width that is not a multiple of 4 reads the 16-B-row copy of the input k_down writes)."""
     c3 = bs.load_config("c3")
     h = _handle(c3)
     assert h.stage_kernel(64, 1080, 1920, 0) == ("k_stage_tma", 4)
-    assert h.stage_kernel(64, 1080, 1920, 1) == ("k_stage_tma", 2)
+    assert h.stage_kernel(64, 1080, 1920, 1) == ("k_stage_tma", 4)
     assert h.stage_kernel(1, 512, 512, 0) == ("k_stage_tma", 2)
     assert h.stage_kernel(1, 130, 259, 0) == ("k_stage_tma", 2)  # reads k_down's 16-B-row input copy
     assert h.stage_kernel(1, 130, 259, 1) == ("k_stage_tma", 2)  # workspace levels are padded
