@@ -439,6 +439,14 @@ bool sync_debug() {
 
 // BLADE_TMA_RY=2 / =4 forces the 2- / 4-row TMA stage variant on every level (A/B timing);
 // default 0 = by level size.
+int tma4_rows() {  // tile rows of the 4-row-thread stage variant (16: two groups; A/B builds may
+                   // instantiate others, e.g. 12-row tiles in three groups: slower, r02_stage_groups)
+  static const int v = [] {
+    const char* e = getenv("BLADE_TMA4_ROWS");
+    return e ? atoi(e) : 16;
+  }();
+  return v;
+}
 int tma_ry() {
   static const int v = [] {
     const char* e = getenv("BLADE_TMA_RY");
@@ -1154,9 +1162,12 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->stage_smem = best_smem;
   for (const auto& v : tma_variants()) {
     if (v.ch3 != ch3 || v.wide != wide || v.nf != c.fine_size || v.nc != cnc) continue;
-    if (v.ry == 4) {  // 4 pixel rows per thread (16-row tiles: same smem as the 2-row variant;
-                      // 20-row tiles = 10 warps per SM measured slower: profiles/r02_fused_selector.txt)
-      if (tma_ry() != 2 && v.trows == 16) {
+    if (v.ry == 4) {  // 4 pixel rows per thread: 16-row tiles in two groups (BLADE_TMA4_ROWS
+                      // selects another instantiated height; 20-row tiles = 10 warps per SM and
+                      // 12-row tiles in three groups measured slower: profiles/r02_fused_selector.txt,
+                      // profiles/r02_stage_groups.txt)
+      // (the per-channel banks have the 16-row form only)
+      if (tma_ry() != 2 && (v.trows == tma4_rows() || (v.trows == 16 && !(h->has_tma4 && h->tma4.trows == tma4_rows())))) {
         h->has_tma4 = true;
         h->tma4 = v;
       }
@@ -1173,9 +1184,9 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
       h->PS_tma = (int)tps;
     }
   }
-  if (h->has_tma && h->has_tma4 && h->tma4.stage_bytes != h->tma.stage_bytes) {  // taller tiles
+  if (h->has_tma && h->has_tma4) {  // its tile buffers (one per group, at least two) next to the bank
     const size_t bank = wide ? 0 : ((size_t)c.n_phases * h->PS_tma * 4 + 127) & ~size_t(127);
-    const size_t smem4 = 2 * (size_t)h->tma4.stage_bytes + bank + 32;
+    const size_t smem4 = (size_t)std::max(2, h->tma4.groups) * h->tma4.stage_bytes + bank + 32;
     if (smem4 <= (size_t)max_smem)
       h->tma_smem = std::max(h->tma_smem, smem4);
     else

@@ -330,6 +330,9 @@ __device__ __forceinline__ void fused_buckets(const float* sf, uint8_t* smap, in
 }
 
 // G = 1: one 256-thread group, double-buffered tiles (TMA of tile i+1 overlaps tile i).
+// G >= 3 (A/B builds): G groups, one buffer each — e.g. three 3-warp groups on 12-row tiles fill
+//        the shared memory (3 x 36 KB + the 120 KB bank) so that two groups compute while one
+//        waits for its TMA; measured slower than two 4-warp groups (profiles/r02_stage_groups.txt).
 // G = 2: two 256-thread groups (16 warps) share the bank; each group owns one tile buffer and works
 //        on every other tile, so one group computes while the other waits for its TMA (twice the
 //        resident warps for the same shared memory).
@@ -361,16 +364,17 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
   // layout: [stage buffers x2][bank][mbarriers]
   unsigned char* buf0 = tma_smem;
   const int bank_floats = a.n_phases * a.PS;
-  float* sbank = reinterpret_cast<float*>(tma_smem + 2 * SS::stage_bytes);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(tma_smem + 2 * SS::stage_bytes +
+  constexpr int NB = G >= 2 ? G : 2;  // tile buffers: one per group, or a double buffer (G = 1)
+  float* sbank = reinterpret_cast<float*>(tma_smem + NB * SS::stage_bytes);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tma_smem + NB * SS::stage_bytes +
                                                (WIDE ? 0 : ((bank_floats * 4 + 127) & ~127)));
   const float* bank = WIDE ? a.bank + (long long)chn * bank_floats : sbank;
 
-  const int g = G == 2 ? (int)(threadIdx.y / SS::BY) : 0;  // thread group
+  const int g = G >= 2 ? (int)(threadIdx.y / SS::BY) : 0;  // thread group
   const int ty = (int)(threadIdx.y % SS::BY), tx = threadIdx.x;
   const int tid = ty * SS::BX + tx;  // thread index within the group
   auto group_sync = [&]() {
-    if constexpr (G == 2)
+    if constexpr (G >= 2)
       asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(SS::threads) : "memory");
     else
       __syncthreads();
@@ -402,26 +406,25 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
   BT_ENTRY(bt_k);
   pdl_trigger();
   if (ctid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    mbar_init(&mbar[2], 1);
+#pragma unroll
+    for (int q = 0; q <= NB; ++q) mbar_init(&mbar[q], 1);  // [0, NB): tile buffers, NB: the bank
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // ---- the bank -> shared memory, once, by one bulk copy (constant data: issued before
     //      waiting on the previous grid)
     if (!WIDE) {
-      mbar_expect_tx(&mbar[2], (uint32_t)bank_floats * 4u);
-      bulk_g2s(sbank, a.bank + (long long)chn * bank_floats, (uint32_t)bank_floats * 4u, &mbar[2]);
+      mbar_expect_tx(&mbar[NB], (uint32_t)bank_floats * 4u);
+      bulk_g2s(sbank, a.bank + (long long)chn * bank_floats, (uint32_t)bank_floats * 4u, &mbar[NB]);
     }
   }
   pdl_wait();
   BT_WAITED(bt_k);
   __syncthreads();
   if (tid == 0 && t < a.n_tiles) issue(t, g);
-  if (!WIDE) mbar_wait(&mbar[2], 0);
+  if (!WIDE) mbar_wait(&mbar[NB], 0);
   BT_WAITED(bt_k + 1);  // bank resident
 
   for (int it = 0; t < a.n_tiles; ++it, t += tstride) {
-    const int b = G == 2 ? g : (it & 1);
+    const int b = G >= 2 ? g : (it & 1);
     const int tn = t + tstride;
     if (G == 1 && tid == 0 && tn < a.n_tiles) {
       fence_proxy_async();  // generic-proxy accesses of buffer b^1 (previous tile) are ordered
@@ -429,7 +432,7 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
     }
     int n, X0, Y0;
     tile_coords(t, n, X0, Y0);
-    mbar_wait(&mbar[b], G == 2 ? (it & 1) : ((it >> 1) & 1));
+    mbar_wait(&mbar[b], G >= 2 ? (it & 1) : ((it >> 1) & 1));
     float* sfine = reinterpret_cast<float*>(buf0 + b * SS::stage_bytes + SS::fine_off);
     float* scoarse = reinterpret_cast<float*>(buf0 + b * SS::stage_bytes + SS::coarse_off);
     const uint8_t* smap = buf0 + b * SS::stage_bytes + SS::map_off;
@@ -629,7 +632,7 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
     }
     }  // active
     group_sync();  // buffer b is free for the next TMA into it
-    if (G == 2 && tid == 0 && tn < a.n_tiles) {
+    if (G >= 2 && tid == 0 && tn < a.n_tiles) {
       fence_proxy_async();
       issue(tn, b);
     }

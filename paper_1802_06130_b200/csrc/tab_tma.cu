@@ -34,6 +34,8 @@ const std::vector<TmaVariant>& tma_variants() {
       make_tma<3, 0, false, false, 4>(), make_tma<5, 0, false, false, 4>(), make_tma<7, 0, false, false, 4>(),
       make_tma<9, 0, false, false, 4>(), make_tma<3, 3, false, false, 4>(), make_tma<5, 5, false, false, 4>(),
       make_tma<5, 3, false, false, 4>(),
+      // (three groups of 12-row tiles, 3 buffers: built and measured slower, c3 stage0 2.38 ->
+      //  2.62 ms; profiles/r02_stage_groups.txt)
       make_tma<3, 0, true, false, 4>(), make_tma<5, 0, true, false, 4>(), make_tma<7, 0, true, false, 4>(),
       make_tma<9, 0, true, false, 4>(), make_tma<3, 3, true, false, 4>(), make_tma<5, 5, true, false, 4>(),
       make_tma<5, 3, true, false, 4>(),
