@@ -3,7 +3,8 @@
     python -m paper_1802_06130_b200.build [--force]
 
 Flags: -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo, static cudart.
-No --use_fast_math: the selector's sqrt/div/atan2 must stay IEEE (H1).
+No --use_fast_math: the selector's div/atan2 must stay IEEE (H1; the FAST selector's
+strength / coherence tests use sqrt.approx.f32 explicitly, R22).
 """
 from __future__ import annotations
 

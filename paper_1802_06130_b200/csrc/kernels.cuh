@@ -5,7 +5,9 @@
 //   k_stage     (this file)       : Eq. 9 stage, generic fallback: CTAs specialised by output-row
 //                                   parity so 7x7 / 9x9 pair banks fit; synchronous staging (K3')
 //
-// All arithmetic is FP32 on the CUDA cores (no fast-math: IEEE sqrt/div, accurate atan2f).
+// All arithmetic is FP32 on the CUDA cores (no fast-math flag: IEEE div, accurate atan2f; the one
+// approximate operation is sqrt.approx.f32 in the FAST selector's strength / coherence tests,
+// DESIGN.md R22).
 // Tensor cores are not used: every pixel contracts with its own selected filter, so the
 // contraction is a batched dot product, not a GEMM.
 //
