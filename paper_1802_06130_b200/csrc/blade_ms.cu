@@ -519,7 +519,9 @@ bool tile_down(const blade_ms* h, long long N, long long H, long long W, bool ru
     return e ? atoll(e) : (3LL << 18);  // crossover 768^2 .. 1024^2 (scripts/tile_threshold.py)
   }();
   const bool fast = h->n_o == 16 && h->n_s == 3 && h->n_c == 3;
-  return run_stages && fast && N * H * W <= max_px && !(h->has_tma && W % 4 != 0);
+  // (frames map to gridDim.z, tile rows to gridDim.y: both <= 65535)
+  return run_stages && fast && N * H * W <= max_px && !(h->has_tma && W % 4 != 0) && N <= 65535 &&
+         (H + 1) / 16 + 1 <= 65535;
 }
 
 // Shared-memory carveout of the launches of the current (small) call: consecutive kernels with

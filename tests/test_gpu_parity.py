@@ -467,6 +467,18 @@ def test_down_tile_bit_identical(tmp_path):
             assert int(b[k + "_launches"]) == 2 * nsel + (1 if W % 4 else 0), (k, int(b[k + "_launches"]))
 
 
+def test_many_tiny_frames_grid_limits():
+    """65,535 frames (the ABI's per-call maximum) of 2 x 4 px: a small call whose frames fill
+    k_down_tile's gridDim.z to its limit; equal bit for bit to the same frames in two calls."""
+    n = 65535
+    cfg = _cfg_like("c1", 2, 4, n)
+    h = _handle(cfg)
+    x = torch.rand(n, 3, 2, 4, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    full = h.denoise(x)
+    halves = torch.cat([h.denoise(x[:n // 2].contiguous()), h.denoise(x[n // 2:].contiguous())])
+    assert torch.equal(full, halves)
+
+
 # ------------------------------------------------------------------------- forced kernel variants
 
 @pytest.mark.parametrize("env", [{"BLADE_TMA_RY": "4"}, {"BLADE_TMA_RY": "2"}, {"BLADE_PDL": "0"},
