@@ -196,7 +196,10 @@ blade_status blade_ms_train_solve(blade_ms_t h, const double* E, const uint64_t*
 
 /* Diagnostic (synchronous): after a blade_ms_denoise / _selector call of N x H x W frames with
  * workspace ws has completed, counts[l] (l < n_stages) = the number of pixels of selector level l
- * whose fp32 orientation bin was not certified and was recomputed in fp64 (DESIGN.md §6 H1). */
+ * whose fp32 orientation bin was not certified and was recomputed in fp64 (DESIGN.md §6 H1).
+ * Small denoise calls (DESIGN.md §6 "Small calls": <= 16 Ki px, or <= 768 Ki px with the 16 x 3 x 3
+ * bucket layout) recompute those pixels inside the down-pass kernel and leave the counts at 0;
+ * blade_ms_selector always counts. */
 blade_status blade_ms_fallback_count(blade_ms_t h, int32_t N, int32_t H, int32_t W, const void* ws,
                                      size_t ws_bytes, uint32_t* counts);
 
