@@ -211,12 +211,15 @@ def algorithmic_work(cfg, N):
 def stage_smem_bytes_per_px(cfg, kind="k_stage_tma", ry=2):
     """Algorithmic (conflict-free) shared-memory bytes per output pixel of the stage kernel:
     every tap of the pixel's filter once (4 B), plus the window values a thread reads per pixel
-    (k_stage_tma: ry x 4 pixels per thread share window rows; k_stage_ph: 2 x 2 sub-lattice)."""
+    (k_stage_tma: ry x 4 pixels per thread share window rows; k_stage_ph: 2 x 2 sub-lattice;
+    k_stage_p2: 2 rows 2 apart x 4 consecutive pixels)."""
     nf = cfg.fine_size
     nc = cfg.coarse_size if cfg.levels > 1 else 0
     taps = 4 * (nf * nf + nc * nc)
     if kind == "k_stage_ph":  # phase-split kernel, 2 x 2 sub-lattice pixels per thread
         vals = (nf + 2) * (nf + 2) * 12 / 4 + (nc + 1) * (nc + 1) * 12 / 4
+    elif kind == "k_stage_p2":  # row-parity kernel: 2 rows (2 apart) x 4 consecutive pixels
+        vals = (nf + 2) * (nf + 3) * 12 / 8 + (nc + 1) * (nc + 1) * 12 / 8
     else:                     # ry x 4 pixels per thread
         vals = (nf + ry - 1) * (nf + 3) * 12 / (4 * ry) + \
             ((nc + ry // 2 - 1) * (nc + 1) * 12 / (4 * ry) if nc else 0)

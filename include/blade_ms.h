@@ -303,7 +303,8 @@ blade_status blade_ms_launch_count(blade_ms_t h, int32_t N, int32_t H, int32_t W
 
 /* Diagnostic: the stage kernel blade_ms_denoise(N, H, W) runs at stage `level` (0 .. n_stages-1)
  * with 16-byte aligned buffers: *kind = 0 generic k_stage, 1 k_stage_tma, 2 k_stage_ph (phase-
- * split); *rows_per_thread = output rows per thread of k_stage_tma (2 or 4; 2 otherwise). Used by
+ * split), 3 k_stage_p2 (row-parity CTAs with two phases each); *rows_per_thread = output rows per
+ * thread of k_stage_tma (2 or 4; 2 otherwise). Used by
  * bench.py's shared-memory roofline model and the tests. EINVAL for a bad level. */
 blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W, int32_t level,
                                    int32_t* kind, int32_t* rows_per_thread);

@@ -256,7 +256,7 @@ class BladeMS:
         _check(lib().blade_ms_launch_count(self._h, N, H, W, ctypes.byref(c)))
         return c.value
 
-    STAGE_KINDS = ("k_stage", "k_stage_tma", "k_stage_ph")
+    STAGE_KINDS = ("k_stage", "k_stage_tma", "k_stage_ph", "k_stage_p2")
 
     def stage_kernel(self, N: int, H: int, W: int, level: int) -> tuple[str, int]:
         """(kernel name, output rows per thread) of stage `level` for a denoise(N, H, W) call."""

@@ -447,6 +447,14 @@ int tma4_rows() {  // tile rows of the 4-row-thread stage variant (16: two group
   }();
   return v;
 }
+// BLADE_P2=0 keeps pair banks that fit two phases per CTA on the one-phase kernel (A/B timing)
+bool p2_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BLADE_P2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 int tma_ry() {
   static const int v = [] {
     const char* e = getenv("BLADE_TMA_RY");
@@ -879,8 +887,9 @@ blade_status up_level(const blade_ms* h, const Plan& p, const Bufs& B, LevelView
       a.z_pitch = zl.pitch;
       a.u_pitch = L > 1 ? u1.pitch : zl.pitch;
       a.out_pitch = outv.pitch;
-      if (tv.phase_split) {  // 4 phase-CTAs (x 3 channels) per tile group, 2 workers per CTA
-        const int types = tv.ch3 ? 12 : 4;
+      if (tv.phase_split) {  // 4 phase-CTAs (x 3 channels) or 2 row-parity CTAs per tile group,
+                             // 2 workers per CTA
+        const int types = tv.ch3 ? 12 : tv.ptypes;
         // one tile per worker group first: small levels spread over as many SMs as they have
         // tiles (a CTA's two groups share its SM's shared-memory bandwidth)
         const int per_type = std::max(1, std::min(h->num_sms / types, a.n_tiles));
@@ -1194,6 +1203,21 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
     else
       h->has_tma4 = false;
   }
+  if (!h->has_tma && c.levels > 1 && c.n_phases == 4 && !ch3 && !wide && p2_enabled()) {
+    // row-parity CTAs holding two phases each (4 consecutive pixels per thread row)
+    for (const auto& v : p2_variants()) {
+      if (v.nf != c.fine_size || v.nc != cnc) continue;
+      const size_t tps = (size_t)K * v.S;
+      const size_t smem = 2 * (size_t)v.stage_bytes + ((2 * tps * 4 + 127) & ~size_t(127)) + 32;
+      if (smem <= (size_t)max_smem && get_encode()) {
+        h->has_tma = true;
+        h->tma = v;
+        h->tma_smem = smem;
+        h->S_tma = v.S;
+        h->PS_tma = (int)tps;
+      }
+    }
+  }
   if (!h->has_tma && c.levels > 1 && c.n_phases == 4) {
     for (const auto& v : ph_variants()) {
       if (v.nf != c.fine_size || v.nc != cnc || v.ch3 != ch3 || v.wide != wide) continue;
@@ -1467,7 +1491,7 @@ blade_status blade_ms_stage_kernel(blade_ms_t h, int32_t N, int32_t H, int32_t W
     *kind = 0;
     *rows_per_thread = 2;
   } else if (h->tma.phase_split) {
-    *kind = 2;
+    *kind = h->tma.ptypes == 2 ? 3 : 2;
     *rows_per_thread = 2;
   } else {
     *kind = 1;

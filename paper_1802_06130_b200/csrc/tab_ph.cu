@@ -18,5 +18,18 @@ const std::vector<TmaVariant>& ph_variants() {
   };
   return v;
 }
+template <int NF, int NC>
+static TmaVariant make_p2() {
+  using SS = PhShape<NF, NC>;
+  TmaVariant v{NF, NC, 2, 4, &k_stage_p2<NF, NC>, SS::stage_bytes, SS::TROWS, SS::TCOLS,
+               SS::FCB, SS::FR, SS::CCB, SS::CR, SS::RF, SS::RC, SS::S, true, false, false};
+  v.ptypes = 2;
+  return v;
+}
+const std::vector<TmaVariant>& p2_variants() {
+  // two phases fit next to two 16 x 128 tile buffers for these pair banks (7x7 + 7x7: 2 x 57.6 KB)
+  static const std::vector<TmaVariant> v = {make_p2<7, 7>(), make_p2<7, 5>(), make_p2<5, 7>()};
+  return v;
+}
 }  // namespace tables
 }  // namespace blade

@@ -39,6 +39,8 @@ struct TmaVariant {
   TmaKernel fsel_fn = nullptr;
   int fsel_stage_bytes = 0, fsel_fr = 0;
   int ry = 2;  // pixel rows per thread (k_stage_tma)
+  int ptypes = 4;  // phase-split kernels: CTA types per channel (k_stage_ph: 4 phases; k_stage_p2: 2
+                   // row parities holding two phases each)
 };
 using StageFixKernel = void (*)(const StageFixArgs, const DownParams);
 StageFixKernel stage_fixup_kernel(int nf, int nc);  // nullptr if none
@@ -46,6 +48,8 @@ StageFixKernel stage_fixup_kernel(int nf, int nc);  // nullptr if none
 const std::vector<TmaVariant>& tma_variants();
 // Phase-split TMA stage kernels: pair banks whose four phases do not fit one CTA.
 const std::vector<TmaVariant>& ph_variants();
+// Row-parity TMA stage kernels (two phases per CTA): pair banks whose two phases fit one CTA.
+const std::vector<TmaVariant>& p2_variants();
 
 using DownKernel = void (*)(const DownArgs, const DownParams);
 // FAST: the configs' bucket layout (16 orientations x 3 strength x 3 coherence bins)

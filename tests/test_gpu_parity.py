@@ -483,7 +483,7 @@ def test_many_tiny_frames_grid_limits():
 
 @pytest.mark.parametrize("env", [{"BLADE_TMA_RY": "4"}, {"BLADE_TMA_RY": "2"}, {"BLADE_PDL": "0"},
                                  {"BLADE_FUSE_SEL": "1", "BLADE_TMA_RY": "4"}, {"BLADE_CARVEOUT": "100"},
-                                 {"BLADE_INLINE_FIX": "0"}, {"BLADE_INLINE_FIX": "100000000"},
+                                 {"BLADE_INLINE_FIX": "0"}, {"BLADE_INLINE_FIX": "100000000"}, {"BLADE_P2": "0"},
                                  {"BLADE_DOWN_TILE": "0"}, {"BLADE_DOWN_TILE": "100000000"}])
 def test_forced_variants_subprocess(env):
     """The library picks kernel variants by level size (4- vs 2-row TMA stage threads) and
@@ -506,7 +506,8 @@ def test_forced_variants_subprocess(env):
 
 def test_stage_kernel_selection():
     """The variant each level runs (blade_ms_stage_kernel): the bench's c3 level 0 takes the
-    4-row TMA kernel, and so does its 7.5-tile-wide level 1; a small call the 2-row one; 7x7 / 9x9 pairs the phase-split
+    4-row TMA kernel, and so does its 7.5-tile-wide level 1; a small call the 2-row one; 7x7 pairs
+    the row-parity kernel (two phases per CTA), 9x9 pairs the phase-split
     kernel; every width takes TMA (levels >= 1 live in the workspace with padded rows; a level-0
     width that is not a multiple of 4 reads the 16-B-row copy of the input k_down writes)."""
     c3 = bs.load_config("c3")
@@ -518,7 +519,7 @@ def test_stage_kernel_selection():
     assert h.stage_kernel(1, 130, 259, 1) == ("k_stage_tma", 2)  # workspace levels are padded
     assert h.stage_kernel(1, 130, 392, 0) == ("k_stage_tma", 2)  # W % 16 == 8: padded map rows
     assert h.stage_kernel(1, 130, 260, 0) == ("k_stage_tma", 2)  # level-1 width 130, padded to 132
-    assert _handle(bs.load_config("c2")).stage_kernel(1, 3000, 4000, 0)[0] == "k_stage_ph"
+    assert _handle(bs.load_config("c2")).stage_kernel(1, 3000, 4000, 0)[0] == "k_stage_p2"
     assert _handle(bs.load_config("c4")).stage_kernel(1, 6000, 8000, 0)[0] == "k_stage_ph"
     from paper_1802_06130_b200.blade_ms import BladeError
     with pytest.raises(BladeError):
