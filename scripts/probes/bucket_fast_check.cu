@@ -4,6 +4,7 @@
 // parity window of a threshold. Build: nvcc -std=c++17 -I paper_1802_06130_b200/csrc
 //   scripts/probes/bucket_fast_check.cu -o /tmp/bfc && /tmp/bfc
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <random>
 
@@ -41,7 +42,8 @@ static int bucket_rot(float a, float b, float c, const float* ts2, const float* 
   return (o * 3 + s) * 3 + k;
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const long iters = argc > 1 ? atol(argv[1]) : 20000000;
   std::mt19937_64 rng(12345);
   std::uniform_real_distribution<double> U(0.0, 1.0);
   const double tS[2] = {0.08075755089521408, 0.1473740190267563}, tC[2] = {0.07864788919687271, 0.14669400453567505};
@@ -73,7 +75,7 @@ int main() {
     s_mis += (br / 3) % 3 != (bn / 3) % 3;
     k_mis += br % 3 != bn % 3;
   };
-  for (int i = 0; i < 20000000; ++i) {
+  for (long i = 0; i < iters; ++i) {
     // a, c >= 0, b^2 <= a c (a Gram matrix); magnitudes over many decades
     const double sc = std::pow(10.0, -8.0 + 10.0 * U(rng));
     const double a = sc * U(rng), c = sc * U(rng);
