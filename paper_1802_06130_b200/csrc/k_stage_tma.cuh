@@ -130,6 +130,28 @@ __device__ __forceinline__ void lds_run(const float* p, float* v) {
   lds_run_at<A, 0, N, MAXV>(p, v);
 }
 
+// The fine window row of a thread (N floats from a column congruent to A mod 4). For the 5 x 5
+// fine block (A = 2, N = 8: LDS.64, LDS.128, LDS.64) the two 8-byte end loads of a half warp
+// (lanes 16 B apart) hit every bank twice: lanes tx and tx + 8 share banks. Lanes 8..15 of each
+// half warp therefore load the right pair first and the left pair second, so each LDS.64 covers
+// the 32 banks once (2 wavefronts instead of 4; the values are swapped back by 4 selects).
+// Other shapes: lds_run.
+template <int A, int N>
+__device__ __forceinline__ void lds_fine(const float* p, float* v, bool swap) {
+  if constexpr (A == 2 && N == 8) {
+    const float2 P = *reinterpret_cast<const float2*>(p + (swap ? 6 : 0));
+    const float4 M = *reinterpret_cast<const float4*>(p + 2);
+    const float2 Q = *reinterpret_cast<const float2*>(p + (swap ? 0 : 6));
+    v[0] = swap ? Q.x : P.x;
+    v[1] = swap ? Q.y : P.y;
+    v[2] = M.x; v[3] = M.y; v[4] = M.z; v[5] = M.w;
+    v[6] = swap ? P.x : Q.x;
+    v[7] = swap ? P.y : Q.y;
+  } else {
+    lds_run<A, N>(p, v);
+  }
+}
+
 // Tap layout of one (phase, bucket) filter for this kernel (LDS.128-friendly): for every row of
 // the fine block (NF x NF) and then of the coarse block (NC x NC), the first 4 floor(n / 4) taps as
 // float4 chunks; after all chunks, the remaining n % 4 taps of every row. The filter stride S is
@@ -582,12 +604,14 @@ __global__ void BLADE_STAGE_BOUNDS(32 * (TR / RY) * G)
       }
     }
     // fine rows local RY ty .. RY ty + NF + RY - 2, cols 4tx .. 4tx+NF+2
+    const bool swap8 = (tx >> 3) & 1;  // lds_fine: half-warp halves take the two end pairs in turn
 #pragma unroll
     for (int wr = 0; wr < NF + RY - 1; ++wr) {
       float v[PL][SS::FWIN];
 #pragma unroll
       for (int c = 0; c < PL; ++c)
-        lds_run<SS::FO, SS::FWIN>(sfine + (c * SS::FR + RY * ty + wr + SS::FRO) * SS::FCB + 4 * tx + SS::FO, v[c]);
+        lds_fine<SS::FO, SS::FWIN>(sfine + (c * SS::FR + RY * ty + wr + SS::FRO) * SS::FCB + 4 * tx + SS::FO, v[c],
+                                   swap8);
 #pragma unroll
       for (int i = 0; i < RY; ++i) {
         const int dy = wr - i;
