@@ -183,6 +183,14 @@ struct blade_ms {
   // streams are handle-wide, so one call's record-then-wait pairs must not interleave with
   // another's (a re-recorded pipe_fork would let a chunk wait on the wrong caller stream)
   std::mutex pipe_mu;
+  // blade_ms_denoise_host: its copy streams and chunk events, created on first use and kept (a
+  // small call paid ~0.2 ms of stream / event creation and destruction per call); host_mu
+  // serialises whole host calls on this handle (they are synchronous anyway)
+  static constexpr int kHostChunks = 32;
+  cudaStream_t host_in = nullptr, host_out = nullptr;
+  cudaEvent_t host_start = nullptr;
+  cudaEvent_t host_ev_in[kHostChunks] = {}, host_ev_done[kHostChunks] = {};
+  std::mutex host_mu;
 };
 
 namespace {
@@ -1418,6 +1426,13 @@ blade_status blade_ms_destroy(blade_ms_t h) {
     if (h->pipe_join[i]) cudaEventDestroy(h->pipe_join[i]);
   }
   if (h->pipe_fork) cudaEventDestroy(h->pipe_fork);
+  if (h->host_in) cudaStreamDestroy(h->host_in);
+  if (h->host_out) cudaStreamDestroy(h->host_out);
+  if (h->host_start) cudaEventDestroy(h->host_start);
+  for (int i = 0; i < blade_ms::kHostChunks; ++i) {
+    if (h->host_ev_in[i]) cudaEventDestroy(h->host_ev_in[i]);
+    if (h->host_ev_done[i]) cudaEventDestroy(h->host_ev_done[i]);
+  }
   cudaFree(h->d_bank);
   cudaFree(h->d_bank_tma);
   delete h;
@@ -2092,58 +2107,80 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
   if (ranges_overlap(d_in, fbytes * N, d_out, fbytes * N)) return fail(BLADE_EINVAL, "d_out overlaps d_in");
   DeviceGuard guard(h->device);
   cudaStream_t st = (cudaStream_t)stream;
-  // chunked frame pipeline: H2D (chunk i+1) || compute (chunk i) || D2H (chunk i-1)
+  // chunked pipeline: H2D (chunk i+1) || compute (chunk i) || D2H (chunk i-1). Chunks are groups
+  // of frames; a batch of fewer frames than chunks whose frames are large is cut into row bands
+  // instead (blade_ms_denoise_rows' plan: each band computes its output rows from its dependency
+  // cone of input rows, bit-identical to the whole frame), so one big image overlaps its copies
+  // with its compute too.
   static const int max_chunks = [] {  // BLADE_E2E_CHUNKS overrides (A/B timing: 16 / 32 / 64 chunks
     const char* e = getenv("BLADE_E2E_CHUNKS");  // of a c3 batch: 34.8 / 34.6 / 35.9 ms, PCIe bound 31.7)
-    return e ? std::max(1, atoi(e)) : 32;
+    return e ? std::min(blade_ms::kHostChunks, std::max(1, atoi(e))) : blade_ms::kHostChunks;
   }();
-  const int nchunks = std::min<int>(N, max_chunks);
-  cudaStream_t s_in = nullptr, s_out = nullptr;
-  std::vector<cudaEvent_t> ev_in(nchunks, nullptr), ev_done(nchunks, nullptr);
-  cudaEvent_t ev_start = nullptr;
-  blade_status rs = BLADE_OK;
-  auto cleanup = [&]() {
-    for (auto& e : ev_in)
-      if (e) cudaEventDestroy(e);
-    for (auto& e : ev_done)
-      if (e) cudaEventDestroy(e);
-    if (ev_start) cudaEventDestroy(ev_start);
-    if (s_in) cudaStreamDestroy(s_in);
-    if (s_out) cudaStreamDestroy(s_out);
-  };
-  cudaError_t ce = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
-  if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
-  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  static const int band_chunks = [] {  // BLADE_E2E_BANDS: row bands of a single large frame (0: off)
+    const char* e = getenv("BLADE_E2E_BANDS");
+    return e ? std::min(blade_ms::kHostChunks, std::max(0, atoi(e))) : 8;
+  }();
+  const bool banded = N == 1 && band_chunks > 1 && (long long)H * W >= (4LL << 20) && H >= 16 * band_chunks;
+  const int nchunks = banded ? band_chunks : std::min<int>(N, max_chunks);
+  std::lock_guard<std::mutex> lock(h->host_mu);
+  cudaError_t ce = cudaSuccess;
+  if (!h->host_in) ce = cudaStreamCreateWithFlags(&h->host_in, cudaStreamNonBlocking);
+  if (ce == cudaSuccess && !h->host_out) ce = cudaStreamCreateWithFlags(&h->host_out, cudaStreamNonBlocking);
+  if (ce == cudaSuccess && !h->host_start) ce = cudaEventCreateWithFlags(&h->host_start, cudaEventDisableTiming);
   for (int i = 0; i < nchunks && ce == cudaSuccess; ++i) {
-    ce = cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming);
-    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming);
+    if (!h->host_ev_in[i]) ce = cudaEventCreateWithFlags(&h->host_ev_in[i], cudaEventDisableTiming);
+    if (ce == cudaSuccess && !h->host_ev_done[i]) ce = cudaEventCreateWithFlags(&h->host_ev_done[i], cudaEventDisableTiming);
   }
-  if (ce == cudaSuccess) ce = cudaEventRecord(ev_start, st);
-  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_in, ev_start, 0);
-  if (ce != cudaSuccess) {
-    cleanup();
-    return fail(BLADE_ECUDA, "stream/event setup: %s", cudaGetErrorString(ce));
-  }
-  int f0 = 0;
+  cudaStream_t s_in = h->host_in, s_out = h->host_out;
+  if (ce == cudaSuccess) ce = cudaEventRecord(h->host_start, st);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_in, h->host_start, 0);
+  if (ce != cudaSuccess) return fail(BLADE_ECUDA, "stream/event setup: %s", cudaGetErrorString(ce));
+  blade_status rs = BLADE_OK;
+  // rows [r0, r1) of the three planes of frame 0 between host and device
+  auto copy_rows = [&](float* dst, const float* src, int r0, int r1, cudaMemcpyKind kind, cudaStream_t cs) {
+    cudaError_t e = cudaSuccess;
+    for (int c = 0; c < 3 && e == cudaSuccess && r1 > r0; ++c) {
+      const size_t o = ((size_t)c * H + r0) * W;
+      e = cudaMemcpyAsync(dst + o, src + o, sizeof(float) * (size_t)(r1 - r0) * W, kind, cs);
+    }
+    return e;
+  };
+  int f0 = 0, copied = 0;
   for (int i = 0; i < nchunks && rs == BLADE_OK; ++i) {
-    const int nf = (N - f0) / (nchunks - i);
-    const size_t off = (size_t)f0 * 3 * H * W;
-    ce = cudaMemcpyAsync(d_in + off, in_host + off, fbytes * nf, cudaMemcpyHostToDevice, s_in);
-    if (ce == cudaSuccess) ce = cudaEventRecord(ev_in[i], s_in);
-    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(st, ev_in[i], 0);
+    Plan p;
+    size_t off = 0;
+    int nf = 1, r0 = 0, r1 = H;
+    if (banded) {
+      r0 = (int)((long long)H * i / nchunks);
+      r1 = (int)((long long)H * (i + 1) / nchunks);
+      plan_rows(h, 1, H, W, r0, r1 - r0, p);
+      if (p.ws_bytes > ws_bytes) {
+        rs = fail(BLADE_ESHAPE, "band workspace %zu bytes > %zu", p.ws_bytes, ws_bytes);
+        break;
+      }
+      ce = copy_rows(d_in, in_host, copied, std::max(copied, p.z[0].hi), cudaMemcpyHostToDevice, s_in);
+      copied = std::max(copied, p.z[0].hi);
+    } else {
+      nf = (N - f0) / (nchunks - i);
+      off = (size_t)f0 * 3 * H * W;
+      plan_rows(h, nf, H, W, 0, H, p);
+      ce = cudaMemcpyAsync(d_in + off, in_host + off, fbytes * nf, cudaMemcpyHostToDevice, s_in);
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(h->host_ev_in[i], s_in);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(st, h->host_ev_in[i], 0);
     if (ce != cudaSuccess) {
       rs = fail(BLADE_ECUDA, "H2D: %s", cudaGetErrorString(ce));
       break;
     }
-    Plan p;
-    plan_rows(h, nf, H, W, 0, H, p);
     LevelView inv = make_view(d_in + off, H, W, Range{0, H});
     LevelView outv = make_view(d_out + off, H, W, Range{0, H});
     rs = enqueue(h, p, inv, outv, (char*)ws, st, true, nullptr, nullptr);
     if (rs != BLADE_OK) break;
-    ce = cudaEventRecord(ev_done[i], st);
-    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_out, ev_done[i], 0);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(out_host + off, d_out + off, fbytes * nf, cudaMemcpyDeviceToHost, s_out);
+    ce = cudaEventRecord(h->host_ev_done[i], st);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s_out, h->host_ev_done[i], 0);
+    if (ce == cudaSuccess)
+      ce = banded ? copy_rows(out_host, d_out, r0, r1, cudaMemcpyDeviceToHost, s_out)
+                  : cudaMemcpyAsync(out_host + off, d_out + off, fbytes * nf, cudaMemcpyDeviceToHost, s_out);
     if (ce != cudaSuccess) {
       rs = fail(BLADE_ECUDA, "D2H: %s", cudaGetErrorString(ce));
       break;
@@ -2151,9 +2188,9 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
     f0 += nf;
   }
   ce = cudaStreamSynchronize(s_out);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s_in);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
   if (rs == BLADE_OK && ce != cudaSuccess) rs = fail(BLADE_ECUDA, "sync: %s", cudaGetErrorString(ce));
-  cleanup();
   return rs;
 }
 

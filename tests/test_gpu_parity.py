@@ -270,6 +270,25 @@ def test_denoise_host_equals_device():
     assert torch.equal(outh, ref.cpu())
 
 
+@pytest.mark.parametrize("name,H,W", [("c4", 2100, 2000), ("c2", 2048, 2052), ("c1", 2049, 2048)])
+def test_denoise_host_single_frame_bands_equal_device(name, H, W):
+    """blade_ms_denoise_host on ONE large frame pipelines row bands (H2D of band i+1, compute of
+    band i, D2H of band i-1; each band computes its rows from its input dependency cone): the
+    output equals the device-resident whole-frame call bit for bit; repeated calls on the handle
+    (its cached copy streams and events) too."""
+    cfg = _cfg_like(name, H, W, 1)
+    h = _handle(cfg)
+    xh = torch.from_numpy(cfg.batch()).pin_memory()
+    ref = h.denoise(xh.cuda()).cpu()
+    outh = torch.empty_like(xh).pin_memory()
+    d_in, d_out = torch.empty_like(xh, device="cuda"), torch.empty_like(xh, device="cuda")
+    ws = h.workspace(1, H, W)
+    for _ in range(2):
+        outh.zero_()
+        h.denoise_host(xh, outh, d_in, d_out, ws)
+        assert torch.equal(outh, ref)
+
+
 def test_clamp_output_flag():
     cfg = _cfg_like("c1", 64, 64, 1)
     x = torch.from_numpy(cfg.batch()).cuda()
