@@ -128,7 +128,7 @@ blade_status blade_ms_denoise(blade_ms_t h, const float* in, float* out, int32_t
  * End-to-end variant with HOST buffers: copies in_host -> d_in, denoises into d_out and copies
  * d_out -> out_host, all on `cuda_stream`, chunk-pipelined (up to 32 frame chunks: the copy in
  * of chunk n+1 and the copy out of chunk n-1 overlap the compute of chunk n) when the host
- * buffers are page-locked. A single frame of >= 4 Mi px is pipelined as 8 row bands instead (each
+ * buffers are page-locked. A single frame of >= 4 Mi px is pipelined as 12 row bands instead (each
  * band computed from its input dependency cone, as blade_ms_denoise_rows: bit-identical to the
  * whole frame). d_in / d_out: device staging buffers of N*3*H*W floats each. Synchronises the
  * stream before returning (the output is in out_host on return). Calls on one handle are

@@ -2118,7 +2118,7 @@ blade_status blade_ms_denoise_host(blade_ms_t h, const float* in_host, float* ou
   }();
   static const int band_chunks = [] {  // BLADE_E2E_BANDS: row bands of a single large frame (0: off)
     const char* e = getenv("BLADE_E2E_BANDS");
-    return e ? std::min(blade_ms::kHostChunks, std::max(0, atoi(e))) : 8;
+    return e ? std::min(blade_ms::kHostChunks, std::max(0, atoi(e))) : 12;  // 8 / 12 / 16 bands: c4 e2e 3,287 / 3,591 / 3,605, c2 2,926 / 3,076 / 3,022 MP/s
   }();
   const bool banded = N == 1 && band_chunks > 1 && (long long)H * W >= (4LL << 20) && H >= 16 * band_chunks;
   const int nchunks = banded ? band_chunks : std::min<int>(N, max_chunks);
