@@ -102,6 +102,12 @@ typedef struct {
  *         (fine) or (floor(y/2)+dy, floor(x/2)+dx) of u^{l+1} (coarse): correlation, as in
  *         Eq. 1 "z_{i+j}" [R12]. Copied (and re-laid for the kernels) at create; the caller
  *         may free its arrays on return.
+ * Every odd fine / coarse size in 1..9 is built. The pairs 5+5, 3+3, 5+3 (whole bank in shared
+ * memory), 7+7, 7+5 (two phases per CTA) and 9+9, 9+7 (one phase per CTA) have TMA-staged kernels;
+ * the other pairs, widths that are not multiples of 4 and tiny levels run the generic stage
+ * kernel. A shared (K <= 256) bank whose two phases do not fit a CTA's shared memory (e.g. 5+9 at
+ * K = 256) is read from global memory like the K > 256 banks. EUNSUPPORTED remains for K > 256
+ * with per-channel banks and for GPU training of footprints without a Gram kernel.
  * Errors: EINVAL (null/bad config), ESHAPE (n_taps), ENONFINITE, EUNSUPPORTED, EDEVICE,
  *         ENOMEM, ECUDA. On error *out is set to NULL.
  */

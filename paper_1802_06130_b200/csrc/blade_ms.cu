@@ -1148,21 +1148,30 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   const StageVariant* best = nullptr;
   size_t best_smem = 0;
   const bool ch3 = c.n_filter_channels == 3;
-  for (const auto& v : stage_variants()) {
-    if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs || v.ch3 != ch3 || v.wide != wide) continue;
-    const int nph_cta = c.n_phases == 4 ? (v.rs == 2 ? 2 : 4) : 1;
-    const size_t bank_f = wide ? 0 : (((size_t)nph_cta * PS) + 3) / 4 * 4;
-    const size_t smem = sizeof(float) * (bank_f + (size_t)v.tile_floats);
-    if (smem > (size_t)max_smem) continue;
-    if (!best || v.by > best->by) {
+  for (const auto* list : {&stage_variants(), &stage_variants_pairs(), &stage_variants_pairs2()})
+    for (const auto& v : *list) {
+      if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs || v.ch3 != ch3 || v.wide != wide) continue;
+      const int nph_cta = c.n_phases == 4 ? (v.rs == 2 ? 2 : 4) : 1;
+      const size_t bank_f = wide ? 0 : (((size_t)nph_cta * PS) + 3) / 4 * 4;
+      const size_t smem = sizeof(float) * (bank_f + (size_t)v.tile_floats);
+      if (smem > (size_t)max_smem) continue;
+      if (!best || v.by > best->by) {
+        best = &v;
+        best_smem = smem;
+      }
+    }
+  if (!best)  // no shared-bank variant fits: the bank stays in global memory (L2-resident), uint8 maps
+    for (const auto& v : stage_variants_gbank()) {
+      if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs || v.ch3 != ch3 || wide) continue;
+      const size_t smem = sizeof(float) * (size_t)v.tile_floats;
+      if (smem > (size_t)max_smem) continue;
       best = &v;
       best_smem = smem;
     }
-  }
   if (!best)
     return fail(BLADE_EUNSUPPORTED,
-                "no stage kernel for fine %d / coarse %d with K = %lld (built: 3/5/7/9 single-level; 3+3, 5+5, "
-                "7+7, 9+9, 7+5, 5+3, 9+7 pairs)",
+                "no stage kernel for fine %d / coarse %d with K = %lld (every odd fine / coarse size 1..9 is "
+                "built for shared and per-channel banks)",
                 c.fine_size, c.coarse_size, K);
 
   blade_ms* h = new blade_ms();

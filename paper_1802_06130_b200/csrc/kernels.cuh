@@ -145,15 +145,18 @@ struct StageShape {
 // z^{L-1} (RGB), else it is plane c of the YCbCr u^{l+1}; the output is plane c of a YCbCr u^l
 // (level 0 is converted back to RGB by k_ycc_to_rgb).
 // WIDE (NEXT f2, K > 256): uint16 bucket maps and the bank read from global memory (L2-resident).
-template <int NF, int NC, int RS, int BY, bool CH3, bool WIDE = false>
+// GBANK: the bank read from global memory (default: when WIDE); with uint8 maps it serves the
+// K <= 256 banks whose two phases do not fit next to a tile (e.g. 5 + 9 taps at K = 256: 219 KB).
+template <int NF, int NC, int RS, int BY, bool CH3, bool WIDE = false, bool GBANK = WIDE>
 __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
+  static_assert(GBANK || !WIDE, "K > 256 banks are read from global memory");
   using SS = StageShape<NF, NC, RS, BY, CH3>;
   using MT = typename std::conditional<WIDE, uint16_t, uint8_t>::type;
   constexpr int PL = SS::PL;
   constexpr int RF = SS::RF, RC = SS::RC;
   extern __shared__ __align__(16) float smem[];
   const int nph_cta = a.n_phases == 4 ? SS::NPH_CTA : 1;
-  const int bank_floats = WIDE ? 0 : nph_cta * a.PS;
+  const int bank_floats = GBANK ? 0 : nph_cta * a.PS;
   float* sbank = smem;
   float* sfine = smem + ((bank_floats + 3) & ~3);
   float* scoarse = sfine + PL * SS::FR * SS::FCP;
@@ -166,11 +169,11 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
   const int tid = threadIdx.y * SS::BX + threadIdx.x;
   pdl_trigger();
 
-  // ---- filterbank -> shared memory, once per CTA (WIDE: read in place from global memory)
+  // ---- filterbank -> shared memory, once per CTA (GBANK: read in place from global memory)
   const int ph0 = (a.n_phases == 4 && RS == 2) ? 2 * par : 0;
   const long long boff = (long long)(chn * a.n_phases + ph0) * a.PS;
-  const float* bank = WIDE ? a.bank + boff : sbank;
-  if (!WIDE) {
+  const float* bank = GBANK ? a.bank + boff : sbank;
+  if (!GBANK) {
     const float4* g4 = reinterpret_cast<const float4*>(a.bank + boff);
     float4* s4 = reinterpret_cast<float4*>(sbank);
     const int n4 = bank_floats >> 2;
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
           for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int dx = 0; dx < NC; ++dx) {
-              const float tap = WIDE ? __ldg(tp[i][j] + NF * NF + dy * NC + dx) : tp[i][j][NF * NF + dy * NC + dx];
+              const float tap = GBANK ? __ldg(tp[i][j] + NF * NF + dy * NC + dx) : tp[i][j][NF * NF + dy * NC + dx];
 #pragma unroll
               for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(tap, v[c][dx], acc[i][j][c]);
             }
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(32 * BY) k_stage(StageArgs a) {
         for (int j = 0; j < 2; ++j)
 #pragma unroll
           for (int dx = 0; dx < NF; ++dx) {
-            const float tap = WIDE ? __ldg(tp[i][j] + dy * NF + dx) : tp[i][j][dy * NF + dx];
+            const float tap = GBANK ? __ldg(tp[i][j] + dy * NF + dx) : tp[i][j][dy * NF + dx];
 #pragma unroll
             for (int c = 0; c < PL; ++c) acc[i][j][c] = fmaf(tap, v[c][j + dx], acc[i][j][c]);
           }

@@ -22,9 +22,17 @@ struct StageVariant {
   int tile_floats, threads, trows, tcols;
   bool ch3;   // per-channel (Y, Cb, Cr) banks: CTAs specialised by channel (NEXT f1)
   bool wide;  // K > 256: uint16 maps, bank read from global memory (NEXT f2)
+  bool gbank = false;  // uint8 maps with the bank read from global memory (K <= 256 banks too large for shared memory)
 };
 // Generic stage kernels (any shape; row-parity CTAs for the big pair banks).
 const std::vector<StageVariant>& stage_variants();
+// the remaining fine / coarse pairs of the ABI's range (tab_stage_pairs.cu: shared banks;
+// tab_stage_pairs2.cu: per-channel and K > 256 banks)
+const std::vector<StageVariant>& stage_variants_pairs();
+const std::vector<StageVariant>& stage_variants_pairs2();
+// every footprint with uint8 maps and the bank in global memory (tab_stage_gbank.cu): the fallback
+// when no shared-bank variant fits
+const std::vector<StageVariant>& stage_variants_gbank();
 
 using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
 struct TmaVariant {

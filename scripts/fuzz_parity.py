@@ -1,0 +1,40 @@
+"""Randomised parity sweep on one GPU: random shapes, pyramid depths, footprints, bucket layouts,
+windows and batch sizes through the C ABI against the fp64 oracle with the GPU suite's rule
+(tests/test_gpu_parity._full_parity). A measurement / hardening aid: prints one line per case
+and a summary; failures are listed with their seed so they can be turned into a test.
+
+    python scripts/fuzz_parity.py [cases] [seed]
+"""
+import sys
+import traceback
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+from tests.fuzz_cases import draw, run_case  # noqa: E402
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    rng = np.random.default_rng(seed0)
+    fails = []
+    for i in range(cases):
+        p = draw(rng)
+        seed = seed0 * 1000 + i
+        try:
+            worst = run_case(p, seed)
+            print(f"ok   seed={seed} {p} max|gpu-oracle|={worst:.2e}", flush=True)
+        except Exception as e:  # noqa: BLE001 (report and continue)
+            fails.append((seed, p, repr(e)[:300]))
+            print(f"FAIL seed={seed} {p}: {e!r}"[:600], flush=True)
+            traceback.print_exc(limit=3)
+    print(f"{cases - len(fails)}/{cases} cases within the parity rule; failures: {fails}")
+    return 1 if fails else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -363,7 +363,11 @@ def test_no_writes_outside_buffers(name, H, W, N):
 def test_ycc_channel_banks_parity(name, H, W, N):
     """NEXT f1: per-channel Y/Cb/Cr banks with the shared RGB selector against the oracle's
     denoise_ycc (same parity rule: outputs within 1e-4 outside the cone of bucket mismatches)."""
-    cfg = _cfg_like(name, H, W, N)
+    _ycc_parity(_cfg_like(name, H, W, N), name)
+
+
+def _ycc_parity(cfg, name):
+    N = cfg.N
     taps = cfg.taps(channels=3)
     h = _handle(cfg, taps)
     x_np = cfg.batch()
@@ -595,6 +599,57 @@ def test_footprint_variants(levels, nf, nc, shape):
     cfg.strength_thresholds = [list(_TS1)] * nst
     cfg.coherence_thresholds = [list(_TC1)] * nst
     _full_parity(cfg, cfg.batch(), label=f"L{levels} {nf}+{nc}@{H}x{W}")
+
+
+_ALL_PAIRS = [(nf, nc) for nf in (1, 3, 5, 7, 9) for nc in (1, 3, 5, 7, 9)]
+
+
+@pytest.mark.parametrize("nf,nc", _ALL_PAIRS)
+def test_every_footprint_pair_of_the_abi_range(nf, nc):
+    """Every fine / coarse pair the ABI accepts (odd sizes 1..9 each): the pairs without a
+    specialised TMA kernel run the generic stage kernel; a ragged two-frame shape, L = 3."""
+    cfg = _cfg_like("c1", 77, 190, 2, levels=3, fine_size=nf, coarse_size=nc)
+    cfg.strength_thresholds = [list(_TS1)] * 2
+    cfg.coherence_thresholds = [list(_TC1)] * 2
+    _full_parity(cfg, cfg.batch(), label=f"{nf}+{nc}")
+
+
+@pytest.mark.parametrize("nf,nc,H,W", [(5, 9, 129, 132), (9, 9, 64, 256), (7, 9, 33, 77)])
+def test_big_bank_read_from_global_memory(nf, nc, H, W):
+    """K = 256 (the uint8 limit) with footprints whose two-phase bank (219 - 333 KB) fits no CTA's
+    shared memory: the stage reads the bank from global memory (uint8 maps), same parity rule."""
+    over = dict(LAYOUTS["16x4x4_K256"])
+    ts, tc = over.pop("ts"), over.pop("tc")
+    cfg = _cfg_like("c1", H, W, 2, levels=3, fine_size=nf, coarse_size=nc, **over)
+    cfg.strength_thresholds = [list(ts)] * 2
+    cfg.coherence_thresholds = [list(tc)] * 2
+    _full_parity(cfg, cfg.batch(), label=f"K256 {nf}+{nc}@{H}x{W}")
+
+
+@pytest.mark.parametrize("nf,nc", [(5, 7), (3, 9), (9, 1)])
+def test_new_footprint_pairs_ycc_and_wide(nf, nc):
+    """The added pairs through the per-channel (f1) and K > 256 (f2) generic kernels."""
+    cfg = _cfg_like("c1", 67, 129, 1, levels=2, fine_size=nf, coarse_size=nc)
+    cfg.strength_thresholds = [list(_TS1)]
+    cfg.coherence_thresholds = [list(_TC1)]
+    _ycc_parity(cfg, f"{nf}+{nc}")
+    over = dict(LAYOUTS["20x4x4_K320"])
+    tsw, tcw = over.pop("ts"), over.pop("tc")
+    cfgw = _cfg_like("c1", 67, 129, 1, levels=2, fine_size=nf, coarse_size=nc, **over)
+    cfgw.strength_thresholds = [list(tsw)]
+    cfgw.coherence_thresholds = [list(tcw)]
+    _full_parity(cfgw, cfgw.batch(), label=f"K320 {nf}+{nc}")
+
+
+def test_random_parity_cases():
+    """40 random cases (tests/fuzz_cases.py: shapes around tile and vector boundaries, depths 1-5,
+    every footprint pair, bucket layouts up to K = 320, windows 1 / 3 / 5, 1 or 4 phases) under the
+    suite's parity rule; scripts/fuzz_parity.py runs longer sweeps of the same generator."""
+    from tests.fuzz_cases import draw, run_case
+    rng = np.random.default_rng(7)
+    for i in range(40):
+        p = draw(rng)
+        run_case(p, 7000 + i)
 
 
 @pytest.mark.parametrize("name", ["c1", "c5"])
