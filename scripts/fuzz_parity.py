@@ -3,7 +3,10 @@ windows and batch sizes through the C ABI against the fp64 oracle with the GPU s
 (tests/test_gpu_parity._full_parity). A measurement / hardening aid: prints one line per case
 and a summary; failures are listed with their seed so they can be turned into a test.
 
-    python scripts/fuzz_parity.py [cases] [seed]
+    python scripts/fuzz_parity.py [cases] [seed] [identity] [big]
+
+`identity` runs the bit-identity properties instead (per-frame calls, row bands, chunked schedule,
+host-buffer call against blade_ms_denoise; no oracle).
 """
 import sys
 import traceback
@@ -14,19 +17,24 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
-from tests.fuzz_cases import draw, run_case  # noqa: E402
+from tests.fuzz_cases import draw, run_case, run_identity_case  # noqa: E402
 
 
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     seed0 = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    ident = "identity" in sys.argv[3:]
     rng = np.random.default_rng(seed0)
     fails = []
     for i in range(cases):
-        p = draw(rng)
+        p = draw(rng, big="big" in sys.argv[3:])
         seed = seed0 * 1000 + i
         try:
-            worst = run_case(p, seed)
+            worst = 0.0
+            if ident:
+                run_identity_case(p, seed)
+            else:
+                worst = run_case(p, seed)
             print(f"ok   seed={seed} {p} max|gpu-oracle|={worst:.2e}", flush=True)
         except Exception as e:  # noqa: BLE001 (report and continue)
             fails.append((seed, p, repr(e)[:300]))

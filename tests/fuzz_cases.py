@@ -6,7 +6,9 @@ from __future__ import annotations
 import numpy as np
 
 
-def draw(rng):
+def draw(rng, big=False):
+    """big: 0.4 - 1.6 MP frames (the streaming k_down, multi-tile TMA stages, merged fix-up launches)
+    instead of the small-call paths."""
     levels = int(rng.choice([1, 2, 2, 3, 3, 4, 5]))
     nf = int(rng.choice([3, 5, 5, 7, 9]))
     nc = int(rng.choice([3, 5, 5, 7, 9])) if levels > 1 else 0
@@ -16,6 +18,10 @@ def draw(rng):
     else:
         H, W = int(rng.integers(1, 300)), int(rng.integers(1, 420))
     N = int(rng.choice([1, 1, 2, 3]))
+    if big:
+        H = int(rng.integers(600, 1100))
+        W = int(rng.choice([1024, 1280, 1284, 1000, 1002, 1337, 1536]))
+        N = int(rng.choice([1, 2]))
     n_o = int(rng.choice([1, 4, 6, 8, 12, 16, 16, 16, 20]))
     n_s = int(rng.choice([1, 2, 3, 3, 4]))
     n_c = int(rng.choice([1, 2, 3, 3, 4]))
@@ -34,18 +40,51 @@ def _T():
 
 
 def run_case(p, seed):
+    cfg = make_cfg(p, seed)
+    _, _, worst = _T()._full_parity(cfg, cfg.batch(), label=str(p))
+    return worst
+
+
+def make_cfg(p, seed):
+    """The blade_synth.Config of a drawn case (thresholds and window sigma from the case seed)."""
     rng = np.random.default_rng(seed)
     cfg = _T()._cfg_like("c1", p["H"], p["W"], p["N"], levels=p["levels"], fine_size=p["nf"],
-                      coarse_size=p["nc"] if p["levels"] > 1 else 5, n_phases=p["n_ph"],
-                      n_orient=p["n_o"], n_strength=p["n_s"], n_coherence=p["n_c"],
-                      window_size=p["win"], window_sigma=float(rng.uniform(0.6, 2.0)), noise=p["noise"],
-                      seed=int(seed))
+                         coarse_size=p["nc"] if p["levels"] > 1 else 5, n_phases=p["n_ph"],
+                         n_orient=p["n_o"], n_strength=p["n_s"], n_coherence=p["n_c"],
+                         window_size=p["win"], window_sigma=float(rng.uniform(0.6, 2.0)), noise=p["noise"],
+                         seed=int(seed))
     if p["noise"] == "signal":
         cfg.p0, cfg.p1 = 0.01, 0.0004
     nst = max(p["levels"] - 1, 1)
     cfg.strength_thresholds = [sorted(rng.uniform(0.02, 0.25, p["n_s"] - 1).tolist()) for _ in range(nst)]
     cfg.coherence_thresholds = [sorted(rng.uniform(0.02, 0.3, p["n_c"] - 1).tolist()) for _ in range(nst)]
-    _, _, worst = _T()._full_parity(cfg, cfg.batch(), label=str(p))
-    return worst
+    return cfg
 
 
+def run_identity_case(p, seed):
+    """The bit-identity properties of the boundary on a drawn case, no oracle involved: per-frame
+    calls, row bands (blade_ms_denoise_rows over a random partition), the chunked schedule
+    (blade_ms_denoise_pipelined) and the host-buffer call all equal blade_ms_denoise bit for bit."""
+    import torch
+    rng = np.random.default_rng(seed + 17)
+    cfg = make_cfg(p, seed)
+    h = _T()._handle(cfg)
+    H, W, N = p["H"], p["W"], p["N"]
+    xh = torch.from_numpy(cfg.batch()).pin_memory()
+    x = xh.cuda()
+    ref = h.denoise(x)
+    n = int(rng.integers(0, N))
+    assert torch.equal(h.denoise(x[n:n + 1].contiguous())[0], ref[n]), "per-frame call"
+    # row bands of frame n over a random partition
+    nb = int(rng.integers(1, min(5, H) + 1))
+    cuts = sorted(set([0, H] + rng.integers(1, max(H, 2), nb - 1).clip(1, max(H - 1, 1)).tolist())) if H > 1 else [0, H]
+    parts = []
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        i0, ni = h.band_rows(H, int(r0), int(r1 - r0))
+        parts.append(h.denoise_rows(x[n, :, i0:i0 + ni].contiguous(), i0, int(r0), int(r1 - r0), H))
+    assert torch.equal(torch.cat(parts, 1), ref[n]), f"row bands {cuts}"
+    chunk, streams = int(rng.integers(1, N + 2)), int(rng.integers(1, 5))
+    assert torch.equal(h.denoise_pipelined(x, chunk=chunk, n_streams=streams), ref), f"pipelined {chunk}/{streams}"
+    outh = torch.empty_like(xh).pin_memory()
+    h.denoise_host(xh, outh, torch.empty_like(ref), torch.empty_like(ref), h.workspace(N, H, W))
+    assert torch.equal(outh, ref.cpu()), "host-buffer call"

@@ -652,6 +652,16 @@ def test_random_parity_cases():
         run_case(p, 7000 + i)
 
 
+def test_random_identity_cases():
+    """25 random cases of the same generator through the bit-identity properties of the boundary
+    (per-frame calls, a random row-band partition, the chunked schedule, the host-buffer call: all
+    equal blade_ms_denoise bit for bit)."""
+    from tests.fuzz_cases import draw, run_identity_case
+    rng = np.random.default_rng(11)
+    for i in range(25):
+        run_identity_case(draw(rng), 11000 + i)
+
+
 @pytest.mark.parametrize("name", ["c1", "c5"])
 def test_fixup_list_overflow_recomputes_everything(name):
     """A frame whose top half is an exact 45-degree ramp puts every pixel there on an orientation
