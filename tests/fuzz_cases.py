@@ -88,3 +88,13 @@ def run_identity_case(p, seed):
     outh = torch.empty_like(xh).pin_memory()
     h.denoise_host(xh, outh, torch.empty_like(ref), torch.empty_like(ref), h.workspace(N, H, W))
     assert torch.equal(outh, ref.cpu()), "host-buffer call"
+
+
+def run_ycc_case(p, seed):
+    """Per-channel (Y, Cb, Cr) banks (NEXT f1) on a drawn case against oracle.denoise_ycc; K > 256
+    with per-channel banks is not built (BLADE_EUNSUPPORTED) and is skipped."""
+    cfg = make_cfg(p, seed)
+    if cfg.K > 256:
+        return False
+    _T()._ycc_parity(cfg, str(p))
+    return True

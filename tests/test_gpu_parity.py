@@ -378,7 +378,8 @@ def _ycc_parity(cfg, name):
     for n in range(N):
         parts = oracle.cascade_parts(cfg, x_np[n], taps[:, :1])
         ref = oracle.denoise_ycc(x_np[n], cfg.levels, cfg.fine_size, cfg.coarse_size, cfg.n_phases,
-                                 cfg.n_orient, cfg.n_strength, cfg.n_coherence, ts, tc, taps)
+                                 cfg.n_orient, cfg.n_strength, cfg.n_coherence, ts, tc, taps,
+                                 cfg.window_size, cfg.window_sigma)
         mism = [check_buckets(maps[l][n], parts["buckets"][l], parts["features"][l], cfg.n_orient,
                               ts[l], tc[l], f"{name} ycc level {l}")[0]
                 for l in range(len(parts["buckets"]))]
