@@ -41,6 +41,8 @@ def exchange_local(workspaces, layouts, step: int) -> None:
 
 def band_edges(H: int, G: int) -> list[tuple[int, int]]:
     """Output rows [r0, r1) of G bands partitioning H rows (shares differ by at most one)."""
+    if not 1 <= G <= H:
+        raise ValueError(f"cannot split {H} rows into {G} non-empty bands")
     return [(g * H // G, (g + 1) * H // G) for g in range(G)]
 
 

@@ -3,7 +3,7 @@ windows and batch sizes through the C ABI against the fp64 oracle with the GPU s
 (tests/test_gpu_parity._full_parity). A measurement / hardening aid: prints one line per case
 and a summary; failures are listed with their seed so they can be turned into a test.
 
-    python scripts/fuzz_parity.py [cases] [seed] [identity|ycc] [big]
+    python scripts/fuzz_parity.py [cases] [seed] [identity|ycc|xband] [big]
 
 `identity` runs the bit-identity properties instead (per-frame calls, row bands, chunked schedule,
 host-buffer call against blade_ms_denoise; no oracle).
@@ -17,7 +17,7 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
-from tests.fuzz_cases import draw, run_case, run_identity_case, run_ycc_case  # noqa: E402
+from tests.fuzz_cases import draw, run_case, run_identity_case, run_xband_case, run_ycc_case  # noqa: E402
 
 
 def main():
@@ -35,6 +35,9 @@ def main():
                 run_identity_case(p, seed)
             elif "ycc" in sys.argv[3:]:
                 run_ycc_case(p, seed)
+            elif "xband" in sys.argv[3:]:
+                ran = run_xband_case(p, seed)
+                worst = 0.0 if ran else float("nan")  # nan: the layout refused the split
             else:
                 worst = run_case(p, seed)
             print(f"ok   seed={seed} {p} max|gpu-oracle|={worst:.2e}", flush=True)

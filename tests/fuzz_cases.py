@@ -98,3 +98,29 @@ def run_ycc_case(p, seed):
         return False
     _T()._ycc_parity(cfg, str(p))
     return True
+
+
+def run_xband_case(p, seed):
+    """Halo-exchange row bands (NEXT f3 (b), the single-GPU form of the NCCL exchange) on frame 0 of
+    a drawn case: G bands reproduce blade_ms_denoise bit for bit, or the layout refuses the split
+    (BLADE_EUNSUPPORTED: a band would own fewer rows of some level than its neighbours need)."""
+    import torch
+    from paper_1802_06130_b200.blade_ms import BladeError
+    from paper_1802_06130_b200.xband import denoise_bands_local
+    rng = np.random.default_rng(seed + 29)
+    p = dict(p, N=1)
+    cfg = make_cfg(p, seed)
+    h = _T()._handle(cfg)
+    x = torch.from_numpy(cfg.batch()).cuda()
+    full = h.denoise(x)[0]
+    G = int(rng.integers(2, 9))
+    if G > p["H"]:  # more bands than rows: xband.band_edges refuses (ValueError)
+        return False
+    try:
+        got = denoise_bands_local(h, x, G)
+    except BladeError as e:
+        assert e.status == 7, e  # refused cleanly
+        return False
+    torch.cuda.synchronize()
+    assert torch.equal(got, full), f"xband G={G}"
+    return True
