@@ -43,9 +43,35 @@ def _gpu_E_to_G_m(E, nt):
 @pytest.mark.parametrize("name,H,W,N", [("c1", 96, 128, 2), ("c0", 70, 90, 1), ("c2", 64, 96, 1),
                                         ("wide", 80, 112, 1)])
 def test_train_accumulators_match_oracle(name, H, W, N):
-    from paper_1802_06130_b200 import BladeMS
     cfg = _wide_cfg() if name == "wide" else bs.load_config(name)
     cfg.H, cfg.W, cfg.N = H, W, N
+    _train_parity(cfg)
+
+
+TRAIN_FOOTPRINTS = [(3, 0), (5, 0), (7, 0), (9, 0), (3, 3), (5, 3), (5, 5), (7, 5), (7, 7)]  # Gram kernels built
+
+
+def test_train_random_cases():
+    """20 random cases (tests/fuzz_cases.py generator, footprints restricted to the built Gram
+    kernels): accumulators, counts and the solve against oracle/train.py."""
+    from tests.fuzz_cases import draw, make_cfg
+    rng = np.random.default_rng(13)
+    done = 0
+    while done < 20:
+        p = draw(rng)
+        if p["H"] < 12 or p["W"] < 12:
+            continue
+        nf, nc = TRAIN_FOOTPRINTS[int(rng.integers(len(TRAIN_FOOTPRINTS)))]
+        p.update(nf=nf, nc=nc, levels=1 if nc == 0 else max(p["levels"], 2))
+        if nc == 0:
+            p["n_ph"] = 1
+        _train_parity(make_cfg(p, 13000 + done))
+        done += 1
+
+
+def _train_parity(cfg):
+    from paper_1802_06130_b200 import BladeMS
+    H, W, N = cfg.H, cfg.W, cfg.N
     z = cfg.batch()
     clean = np.stack([bs.scene(cfg.seed, i, H, W, cfg.n_grat, cfg.n_disk, "none", 0.0, 0.0)
                       for i in range(N)]).astype(np.float32)
