@@ -653,6 +653,55 @@ def test_random_parity_cases():
         run_case(p, 7000 + i)
 
 
+def test_concurrent_calls_on_one_handle():
+    """include/blade_ms.h "Thread safety": concurrent calls on ONE handle with distinct workspaces,
+    outputs and streams are safe - four host threads mix blade_ms_denoise, _denoise_pipelined (the
+    handle's shared internal streams, serialised by its mutex) and _denoise_host for several rounds
+    on different inputs; every output equals the same call made alone, bit for bit."""
+    import threading
+    cfg = _cfg_like("c3", 120, 200, 4)
+    h = _handle(cfg)
+    T, R = 4, 6
+    xs = [torch.from_numpy(cfg.batch(frame0=4 * t)).cuda() for t in range(T)]
+    refs = [h.denoise(x).clone() for x in xs]
+    torch.cuda.synchronize()
+    errs = []
+
+    def work(t):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            x, ref = xs[t], refs[t]
+            xh = x.cpu().pin_memory()
+            outh = torch.empty_like(xh).pin_memory()
+            d_in, d_out = torch.empty_like(x), torch.empty_like(x)
+            ws = h.workspace(4, 120, 200)
+            out = torch.empty_like(x)
+            for r in range(R):
+                kind = (t + r) % 3
+                out.zero_()
+                if kind == 0:
+                    h.denoise(x, out, workspace=ws, stream=st)
+                elif kind == 1:
+                    h.denoise_pipelined(x, out, chunk=1 + (r % 2), n_streams=2 + (t % 2), stream=st)
+                else:
+                    h.denoise_host(xh, outh, d_in, d_out, ws, stream=st)
+                    out.copy_(outh)
+                st.synchronize()
+                torch.cuda.synchronize()
+                if not torch.equal(out, ref):
+                    errs.append((t, r, kind, float((out - ref).abs().max())))
+        except Exception as e:  # noqa: BLE001
+            errs.append((t, repr(e)))
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(T)]
+    for q in th:
+        q.start()
+    for q in th:
+        q.join()
+    assert not errs, errs
+
+
 def test_random_identity_cases():
     """25 random cases of the same generator through the bit-identity properties of the boundary
     (per-frame calls, a random row-band partition, the chunked schedule, the host-buffer call: all
