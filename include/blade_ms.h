@@ -58,7 +58,7 @@ typedef enum {
   BLADE_EDEVICE = 4,      /* pointer not on the handle's device, or bad device ordinal   */
   BLADE_ENOMEM = 5,       /* device allocation failed at create                          */
   BLADE_ECUDA = 6,        /* a CUDA call or launch failed (message in last_error)        */
-  BLADE_EUNSUPPORTED = 7  /* valid per the paper but not built (e.g. per-channel banks)  */
+  BLADE_EUNSUPPORTED = 7  /* valid per the paper but not built (see blade_ms_create)     */
 } blade_status;
 
 typedef struct {
@@ -106,8 +106,9 @@ typedef struct {
  * memory), 7+7, 7+5 (two phases per CTA) and 9+9, 9+7 (one phase per CTA) have TMA-staged kernels;
  * the other pairs, widths that are not multiples of 4 and tiny levels run the generic stage
  * kernel. A shared (K <= 256) bank whose two phases do not fit a CTA's shared memory (e.g. 5+9 at
- * K = 256) is read from global memory like the K > 256 banks. EUNSUPPORTED remains for K > 256
- * with per-channel banks and for GPU training of footprints without a Gram kernel.
+ * K = 256) is read from global memory like the K > 256 banks. K > 256 with per-channel banks (the
+ * paper's own 16 x 16 x 16 x {Y, Cb, Cr} layout) runs too. EUNSUPPORTED remains for GPU training of
+ * footprints without a Gram kernel.
  * Errors: EINVAL (null/bad config), ESHAPE (n_taps), ENONFINITE, EUNSUPPORTED, EDEVICE,
  *         ENOMEM, ECUDA. On error *out is set to NULL.
  */

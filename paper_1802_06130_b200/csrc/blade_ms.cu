@@ -1099,8 +1099,6 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   const long long K = (long long)bl->n_orient * bl->n_strength * bl->n_coherence;
   if (K > 65536) return fail(BLADE_EUNSUPPORTED, "K = %lld > 65536 (uint16 bucket maps)", K);
   const bool wide = K > 256;  // uint16 maps, bank read from global memory (NEXT f2)
-  if (wide && c.n_filter_channels == 3)
-    return fail(BLADE_EUNSUPPORTED, "K > 256 with per-channel banks is not built");
   if ((bl->n_strength > 1 && !bl->strength_thresholds) || (bl->n_coherence > 1 && !bl->coherence_thresholds))
     return fail(BLADE_EINVAL, "threshold arrays must be non-NULL");
   const int n_stages = std::max(c.levels - 1, 1);
@@ -1148,7 +1146,7 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   const StageVariant* best = nullptr;
   size_t best_smem = 0;
   const bool ch3 = c.n_filter_channels == 3;
-  for (const auto* list : {&stage_variants(), &stage_variants_pairs(), &stage_variants_pairs2()})
+  for (const auto* list : {&stage_variants(), &stage_variants_pairs(), &stage_variants_pairs2(), &stage_variants_ch3_wide()})
     for (const auto& v : *list) {
       if (v.nf != c.fine_size || v.nc != cnc || v.rs != want_rs || v.ch3 != ch3 || v.wide != wide) continue;
       const int nph_cta = c.n_phases == 4 ? (v.rs == 2 ? 2 : 4) : 1;
@@ -1188,7 +1186,8 @@ blade_status blade_ms_create(const blade_ms_config* cfg, const blade_bucket_layo
   h->num_sms = nsm;
   h->stage = *best;
   h->stage_smem = best_smem;
-  for (const auto& v : tma_variants()) {
+  for (const auto* tlist : {&tma_variants(), &tma_variants_ch3_wide()})
+  for (const auto& v : *tlist) {
     if (v.ch3 != ch3 || v.wide != wide || v.nf != c.fine_size || v.nc != cnc) continue;
     if (v.ry == 4) {  // 4 pixel rows per thread: 16-row tiles in two groups (BLADE_TMA4_ROWS
                       // selects another instantiated height; 20-row tiles = 10 warps per SM and

@@ -33,6 +33,8 @@ const std::vector<StageVariant>& stage_variants_pairs2();
 // every footprint with uint8 maps and the bank in global memory (tab_stage_gbank.cu): the fallback
 // when no shared-bank variant fits
 const std::vector<StageVariant>& stage_variants_gbank();
+// per-channel banks with K > 256 (tab_stage_ch3wide.cu): uint16 maps, bank in global memory
+const std::vector<StageVariant>& stage_variants_ch3_wide();
 
 using TmaKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, StageTmaArgs);
 struct TmaVariant {
@@ -54,6 +56,8 @@ using StageFixKernel = void (*)(const StageFixArgs, const DownParams);
 StageFixKernel stage_fixup_kernel(int nf, int nc);  // nullptr if none
 // TMA stage kernels: the shapes whose whole (all-phase) bank fits next to two staging buffers.
 const std::vector<TmaVariant>& tma_variants();
+// the same for per-channel banks with K > 256 (tab_tma_ch3wide.cu)
+const std::vector<TmaVariant>& tma_variants_ch3_wide();
 // Phase-split TMA stage kernels: pair banks whose four phases do not fit one CTA.
 const std::vector<TmaVariant>& ph_variants();
 // Row-parity TMA stage kernels (two phases per CTA): pair banks whose two phases fit one CTA.

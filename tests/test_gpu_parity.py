@@ -389,6 +389,13 @@ def _ycc_parity(cfg, name):
         assert err <= OUT_ATOL, f"{name} ycc frame {n}: max |gpu - oracle| = {err}"
 
 
+@pytest.mark.parametrize("H,W,N", [(256, 384, 2), (130, 200, 1), (9, 17, 1)])
+def test_c5_per_channel_banks_parity(H, W, N):
+    """The paper's own layout: 16 x 16 x 16 buckets (uint16 maps, global-memory bank) WITH one
+    bank per Y / Cb / Cr channel (f1 x f2), against oracle.denoise_ycc."""
+    _ycc_parity(_cfg_like("c5", H, W, N), "c5 ycc")
+
+
 def test_ycc_equal_banks_match_rgb_path():
     cfg = _cfg_like("c1", 130, 200, 2)
     t1 = cfg.taps()
