@@ -11,3 +11,5 @@ python scripts/ncu_lines.py $O/k_stage_full.ncu-rep 40 > $P/${R}_k_stage_tma_lin
 python scripts/ncu_lines.py $O/k_down_full.ncu-rep 40 > $P/${R}_k_down_lines.txt
 python scripts/ncu_json.py c3:stage:0=$O/k_stage_full.ncu-rep c3:selector:0=$O/k_down_full.ncu-rep > $P/ncu_summary.json
 cp $O/xband_cost.jsonl $P/${R}_xband_cost.jsonl 2>/dev/null; python scripts/sass_census.py > $P/${R}_sass_census.txt
+
+( for f in $O/fuzz_*.log; do echo "$(basename $f): $(tail -1 $f | cut -c1-400)"; done ) > $P/${R}_fuzz_last_refresh.txt 2>/dev/null

@@ -11,9 +11,14 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')
 for c in c3 c0 c1 c2 c4 c5; do
   timeout 600 python bench.py --config $c > $O/bench_$c.jsonl 2> $O/bench_$c.err
 done
-for c in c3 c1; do
+for c in c3 c1 c5; do  # c5 --ycc: the paper's own layout (4096 buckets x per-channel banks)
   timeout 600 python bench.py --config $c --ycc --no-cpu-baseline > $O/bench_${c}_ycc.jsonl 2> $O/bench_${c}_ycc.err
 done
+# random sweeps (tests/fuzz_cases.py): parity, bit-identity, per-channel banks, halo-exchange bands
+for m in "" identity ycc xband; do
+  timeout 600 python scripts/fuzz_parity.py 200 41 $m > $O/fuzz_${m:-parity}.log 2>&1
+done
+timeout 600 python scripts/fuzz_parity.py 40 42 big > $O/fuzz_big.log 2>&1
 timeout 600 python bench.py --train --frames 16 --steps 5 --warmup 3 > $O/bench_c3_train.jsonl 2> $O/bench_c3_train.err
 timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > $O/bench_reference.jsonl 2> $O/bench_reference.err
 timeout 600 python scripts/xband_cost.py > $O/xband_cost.jsonl 2> $O/xband_cost.err
