@@ -5,7 +5,7 @@ and a summary; failures are listed with their seed so they can be turned into a 
 
     python scripts/fuzz_parity.py [cases] [seed] [identity|ycc|xband] [big]
 
-`identity` runs the bit-identity properties instead (per-frame calls, row bands, chunked schedule,
+`identity` (optionally with `ycc`: per-channel banks) runs the bit-identity properties instead (per-frame calls, row bands, chunked schedule,
 host-buffer call against blade_ms_denoise; no oracle).
 """
 import sys
@@ -32,12 +32,12 @@ def main():
         try:
             worst = 0.0
             if ident:
-                run_identity_case(p, seed)
+                run_identity_case(p, seed, channels=3 if "ycc" in sys.argv[3:] else 1)
+            elif "xband" in sys.argv[3:]:
+                ran = run_xband_case(p, seed, channels=3 if "ycc" in sys.argv[3:] else 1)
+                worst = 0.0 if ran else float("nan")  # nan: the layout refused the split
             elif "ycc" in sys.argv[3:]:
                 run_ycc_case(p, seed)
-            elif "xband" in sys.argv[3:]:
-                ran = run_xband_case(p, seed)
-                worst = 0.0 if ran else float("nan")  # nan: the layout refused the split
             else:
                 worst = run_case(p, seed)
             print(f"ok   seed={seed} {p} max|gpu-oracle|={worst:.2e}", flush=True)

@@ -61,14 +61,14 @@ def make_cfg(p, seed):
     return cfg
 
 
-def run_identity_case(p, seed):
+def run_identity_case(p, seed, channels=1):
     """The bit-identity properties of the boundary on a drawn case, no oracle involved: per-frame
     calls, row bands (blade_ms_denoise_rows over a random partition), the chunked schedule
     (blade_ms_denoise_pipelined) and the host-buffer call all equal blade_ms_denoise bit for bit."""
     import torch
     rng = np.random.default_rng(seed + 17)
     cfg = make_cfg(p, seed)
-    h = _T()._handle(cfg)
+    h = _T()._handle(cfg, cfg.taps(channels=channels) if channels != 1 else None)
     H, W, N = p["H"], p["W"], p["N"]
     xh = torch.from_numpy(cfg.batch()).pin_memory()
     x = xh.cuda()
@@ -98,7 +98,7 @@ def run_ycc_case(p, seed):
     return True
 
 
-def run_xband_case(p, seed):
+def run_xband_case(p, seed, channels=1):
     """Halo-exchange row bands (NEXT f3 (b), the single-GPU form of the NCCL exchange) on frame 0 of
     a drawn case: G bands reproduce blade_ms_denoise bit for bit, or the layout refuses the split
     (BLADE_EUNSUPPORTED: a band would own fewer rows of some level than its neighbours need)."""
@@ -108,7 +108,7 @@ def run_xband_case(p, seed):
     rng = np.random.default_rng(seed + 29)
     p = dict(p, N=1)
     cfg = make_cfg(p, seed)
-    h = _T()._handle(cfg)
+    h = _T()._handle(cfg, cfg.taps(channels=channels) if channels != 1 else None)
     x = torch.from_numpy(cfg.batch()).cuda()
     full = h.denoise(x)[0]
     G = int(rng.integers(2, 9))
