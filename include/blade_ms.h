@@ -107,8 +107,9 @@ typedef struct {
  * the other pairs, widths that are not multiples of 4 and tiny levels run the generic stage
  * kernel. A shared (K <= 256) bank whose two phases do not fit a CTA's shared memory (e.g. 5+9 at
  * K = 256) is read from global memory like the K > 256 banks. K > 256 with per-channel banks (the
- * paper's own 16 x 16 x 16 x {Y, Cb, Cr} layout) runs too. EUNSUPPORTED remains for GPU training of
- * footprints without a Gram kernel.
+ * paper's own 16 x 16 x 16 x {Y, Cb, Cr} layout) runs too. EUNSUPPORTED remains for GPU training
+ * (blade_ms_train_*) of footprints with n_f^2 + n_c^2 > 123 (7+9, 9+7, 9+9), of K > 256 banks other
+ * than 7, 5+5, 7+5, 7+7, and of per-channel banks.
  * Errors: EINVAL (null/bad config), ESHAPE (n_taps), ENONFINITE, EUNSUPPORTED, EDEVICE,
  *         ENOMEM, ECUDA. On error *out is set to NULL.
  */

@@ -20,7 +20,7 @@ INCLUDE = PKG.parent / "include"
 LIB = PKG / "libblade_ms.so"
 SOURCES = [CSRC / "blade_ms.cu", CSRC / "tab_down.cu", CSRC / "tab_stage.cu", CSRC / "tab_stage_pairs.cu",
            CSRC / "tab_stage_pairs2.cu", CSRC / "tab_stage_gbank.cu", CSRC / "tab_stage_ch3wide.cu", CSRC / "tab_tma.cu", CSRC / "tab_tma_ch3wide.cu",
-           CSRC / "tab_ph.cu", CSRC / "tab_train.cu"]
+           CSRC / "tab_ph.cu", CSRC / "tab_train.cu", CSRC / "tab_train_pairs.cu"]
 DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [INCLUDE / "blade_ms.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

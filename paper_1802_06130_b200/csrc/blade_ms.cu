@@ -1697,8 +1697,9 @@ static int train_nt(const blade_ms* h) {
 }
 static const TrainVariant* train_variant(const blade_ms* h) {
   const int cnc = h->cfg.levels > 1 ? h->cfg.coarse_size : 0;
-  for (const auto& v : train_variants())
-    if (v.nf == h->cfg.fine_size && v.nc == cnc && v.wide == (h->K > 256)) return &v;
+  for (const auto* list : {&train_variants(), &train_variants_pairs()})
+    for (const auto& v : *list)
+      if (v.nf == h->cfg.fine_size && v.nc == cnc && v.wide == (h->K > 256)) return &v;
   return nullptr;
 }
 

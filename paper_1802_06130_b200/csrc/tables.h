@@ -84,6 +84,7 @@ struct TrainVariant {
   TrainKernel gram_dfma; // the same on the FP64 CUDA cores (BLADE_TRAIN_MMA=0)
 };
 const std::vector<TrainVariant>& train_variants();
+const std::vector<TrainVariant>& train_variants_pairs();  // the other footprints with n_f^2 + n_c^2 <= 123
 TrainKernel train_hist(bool wide);
 TrainKernel train_scatter(bool wide);
 TrainKernel train_scan();
