@@ -3,10 +3,10 @@
 Builds the oracle's level-0 bucket map of a band of c3 frame 0 and counts, for the lane -> pixel
 mapping of k_stage_tma (32 thread columns of a tile row, 4 px apart, one (phase, bucket) filter
 per lane), the shared-memory wavefronts of one tap load under the two service models:
-LDS.128 per quarter warp (8 bank groups of 16 B), LDS.32 per warp (32 banks). Host only; uses the
-oracle for the bucket map (a measurement aid, not a product path).
+LDS.128 per quarter warp (8 bank groups of 16 B), LDS.32 per warp (32 banks). Host only; it lives under
+tests/ because it uses the oracle for the bucket map (test infrastructure, never a product path).
 
-    python scripts/probes/tap_conflict_model.py [rows]
+    python tests/tools/tap_conflict_model.py [rows]
 """
 import sys
 from pathlib import Path
